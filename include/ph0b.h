@@ -1,0 +1,178 @@
+/* ph0b — B200-native (sm_100a) H0 persistent-homology barcode pipeline, C ABI.
+ *
+ * Drop-in for the reference library's hot path (namespace ph0, /root/reference/proj):
+ *
+ *     pairwise_distances        proj/include/ph0/filtration.hpp:35   (proj/src/filtration.cpp:8-18)
+ *   ∘ build_filtration          proj/include/ph0/filtration.hpp:40   (proj/src/filtration.cpp:20-35)
+ *   ∘ build_boundary_matrix     proj/include/ph0/boundary_matrix.hpp:30 (proj/src/boundary_matrix.cpp:15-28)
+ *   ∘ reduce / reduce_parallel  proj/include/ph0/reduction.hpp:33,39 (proj/src/reduction.cpp:129-138)
+ *   ∘ extract_barcode           proj/include/ph0/reduction.hpp:43   (proj/src/reduction.cpp:140-150)
+ *
+ * composed exactly as in proj/src/bench.cpp:45-59, proj/tools/ph0_cli.cpp:58-71 and
+ * proj/tests/acceptance.cpp:56-68.  Input: point cloud X (N x d, f64).  Output: the finite
+ * bars (0, b) in filtration order — death grade (1-based index into D) and death length —
+ * the essential count, and the deduplicated, strictly increasing distance list D
+ * (Filtration::scale, proj/include/ph0/filtration.hpp:28-31).  Results are bit-identical
+ * to the reference on the same X.
+ *
+ * Plain C types only; no CUDA or torch types in any signature (`stream` is a cudaStream_t
+ * passed as void*).  Every call is synchronous from the caller's view unless stated.
+ */
+#ifndef PH0B_H
+#define PH0B_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define PH0B_ABI_VERSION 1u
+
+/* Return codes.  The message of ph0b_last_error() repeats the reference's exception text
+ * where the reference has one. */
+#define PH0B_OK 0
+#define PH0B_ERR_INVALID_ARGUMENT 1 /* std::invalid_argument in the reference */
+#define PH0B_ERR_NONFINITE 2        /* "point cloud contains non-finite coordinates" (point_cloud.cpp:17) */
+#define PH0B_ERR_TOO_LARGE 3        /* N above this build's limit (PH0B_MAX_POINTS) or N > 2^32-1 */
+#define PH0B_ERR_CUDA 4             /* CUDA runtime / launch failure */
+#define PH0B_ERR_OUT_OF_MEMORY 5    /* device or pinned-host allocation failed */
+#define PH0B_ERR_NO_DEVICE 6        /* no sm_100 device visible */
+#define PH0B_ERR_CAPACITY 7         /* caller-provided output buffer too small */
+
+/* Vertex ids are packed 16+16 bits into one u32 per edge column (u << 16 | v); the
+ * reference allows N <= 2^32-1 (filtration.cpp:10-11) but its K x N-bit matrix cannot go
+ * past N ~ 10^4 in practice. */
+#define PH0B_MAX_POINTS 65536u
+
+/* Layout of X. */
+#define PH0B_COL_MAJOR 0u /* Eigen::MatrixXd storage (point_cloud.hpp:30): x(i,j) at j*N + i */
+#define PH0B_ROW_MAJOR 1u /* one point per contiguous row: x(i,j) at i*d + j */
+
+/* ph0b_options.flags */
+#define PH0B_FLAG_NO_SCALE 0x1u   /* do not copy D back (n_scale is still reported) */
+
+typedef struct ph0b_options {
+    uint32_t struct_size; /* sizeof(ph0b_options); 0 = all defaults */
+    int32_t device;       /* CUDA device ordinal; default 0 */
+    uint32_t flags;       /* PH0B_FLAG_* */
+    /* ReductionOptions (reduction.hpp:11-17): accepted for drop-in compatibility and
+     * result-neutral, exactly as in the reference (pivot on/off and any worker count give
+     * identical reduced matrices, reduction.hpp:35-39).  workers == 0 is rejected with the
+     * reference's message "worker count must be at least 1" (reduction.cpp:134). */
+    uint32_t pivoting;
+    uint32_t workers;
+} ph0b_options;
+
+/* Per-stage device milliseconds of the last run (CUDA events on the pipeline stream). */
+typedef struct ph0b_stage_times {
+    float distance_ms;  /* K1 tiled distance kernel                     */
+    float sort_ms;      /* K2 radix sort (all passes)                   */
+    float unique_ms;    /* K2c/K3 flag-and-scan unique -> D, M          */
+    float reduce_ms;    /* K4 column reduction                          */
+    float collect_ms;   /* K5 barcode collect                           */
+    float total_ms;     /* first kernel start -> last kernel end        */
+    uint32_t sort_passes;
+    uint32_t reduce_rounds;
+    uint64_t columns_scanned; /* edge columns streamed by the reduction */
+} ph0b_stage_times;
+
+/* Host-side result of ph0b_h0_barcode; arrays are owned by the library. */
+typedef struct ph0b_result {
+    uint64_t n_finite;        /* = Barcode::finite.size()                      */
+    uint64_t* death_grade;    /* [n_finite], Interval::death_grade (1-based)   */
+    double* death_length;     /* [n_finite], Interval::death_length            */
+    uint64_t essential_count; /* Barcode::essential_count                      */
+    uint64_t n_scale;         /* |D|                                           */
+    double* scale;            /* [n_scale] D, or NULL with PH0B_FLAG_NO_SCALE  */
+    ph0b_stage_times times;
+} ph0b_result;
+
+/* ---- drop-in entry point --------------------------------------------------------------
+ * X (host memory) -> barcode + D (host memory, allocated by the library; free with
+ * ph0b_result_free).  Replaces the five-call composition above. */
+int ph0b_h0_barcode(const double* X, uint64_t n, uint64_t d, uint32_t layout,
+                    const ph0b_options* opt, ph0b_result* out);
+void ph0b_result_free(ph0b_result* r);
+
+/* Same, writing into caller-provided host buffers (no allocation inside the call; pinned
+ * buffers from ph0b_host_alloc give full PCIe bandwidth).  death_* need n-1 entries,
+ * scale needs scale_capacity >= |D| (|D| <= n(n-1)/2) or may be NULL. */
+int ph0b_h0_barcode_into(const double* X, uint64_t n, uint64_t d, uint32_t layout,
+                         const ph0b_options* opt, uint64_t* death_grade, double* death_length,
+                         uint64_t* n_finite, uint64_t* essential_count, double* scale,
+                         uint64_t scale_capacity, uint64_t* n_scale, ph0b_stage_times* times);
+
+/* ---- stage-level mirrors (parity surfaces for the reference's own tests) ---------------
+ * pairwise_distances (filtration.cpp:8-18): lengths of all pairs u < v in u-major order. */
+int ph0b_pairwise_distances(const double* X, uint64_t n, uint64_t d, uint32_t layout,
+                            const ph0b_options* opt, double* lengths);
+
+/* pairwise_distances ∘ build_filtration ∘ build_boundary_matrix (filtration.cpp:20-35,
+ * boundary_matrix.cpp:15-28): column j of M in filtration order is {u[j], v[j]} at grade
+ * grade[j]; scale receives D. Arrays have K = n(n-1)/2 entries (scale: >= |D|). */
+int ph0b_build_filtration(const double* X, uint64_t n, uint64_t d, uint32_t layout,
+                          const ph0b_options* opt, uint32_t* u, uint32_t* v, uint64_t* grade,
+                          double* scale, uint64_t* n_scale);
+
+/* Claimed low of every surviving column after reduce() — the row the reference's
+ * claimed_by_ table (reduction.cpp:44-45,121) maps to it — in filtration order (n-1
+ * entries).  Stronger-than-barcode parity surface. */
+int ph0b_claimed_lows(const double* X, uint64_t n, uint64_t d, uint32_t layout,
+                      const ph0b_options* opt, uint32_t* lows, uint64_t* n_lows);
+
+/* ---- device-resident path (benchmarks, multi-GPU orchestration) ----------------------- */
+typedef struct ph0b_context ph0b_context;
+
+int ph0b_context_create(int device, ph0b_context** ctx);
+void ph0b_context_destroy(ph0b_context* ctx);
+/* Pre-size the device workspace for clouds up to (n, d); optional. */
+int ph0b_context_reserve(ph0b_context* ctx, uint64_t n, uint64_t d);
+uint64_t ph0b_context_workspace_bytes(const ph0b_context* ctx);
+
+typedef struct ph0b_device_result {
+    uint64_t n_finite;
+    uint64_t essential_count;
+    uint64_t n_scale;
+    const double* d_scale;         /* device pointer into the context workspace [n_scale] */
+    const uint64_t* d_death_grade; /* device [n_finite] */
+    const double* d_death_length;  /* device [n_finite] */
+    ph0b_stage_times times;
+} ph0b_device_result;
+
+/* X is a DEVICE pointer (layout as above).  Outputs stay on the device, valid until the
+ * next call on this context.  Blocks until done (reads back n_scale). */
+int ph0b_run_device(ph0b_context* ctx, const double* dX, uint64_t n, uint64_t d,
+                    uint32_t layout, void* stream, ph0b_device_result* out);
+
+/* Host X -> host outputs through the context (reuses workspace and pinned staging). */
+int ph0b_run_host(ph0b_context* ctx, const double* X, uint64_t n, uint64_t d, uint32_t layout,
+                  void* stream, uint64_t* death_grade, double* death_length,
+                  uint64_t* n_finite, uint64_t* essential_count, double* scale,
+                  uint64_t scale_capacity, uint64_t* n_scale, ph0b_stage_times* times);
+
+/* ---- utilities ------------------------------------------------------------------------ */
+const char* ph0b_last_error(void);
+uint32_t ph0b_abi_version(void);
+/* Pinned host memory (cudaHostAlloc) for zero-staging D2H of D. */
+void* ph0b_host_alloc(uint64_t bytes);
+void ph0b_host_free(void* p);
+/* Number of kernel launches issued by the last run on this thread (evidence counter). */
+uint64_t ph0b_last_launch_count(void);
+
+/* Synthetic clouds of the BASELINE.json configs; column-major output.
+ * kind: 0 = generate_uniform_cloud(n, d, seed) exactly (point_cloud.cpp:20-29);
+ *       1 = Gaussian mixture: `clusters` centres U[lo,hi]^d, isotropic sigma;
+ *       2 = noisy unit circle (z=0 plane) + n_background uniform points in [lo,hi]^d (C2);
+ *       3 = two equal Gaussian clusters centred at (lo,..,lo) and (hi,..,hi) (config C1).
+ * All randomness is SplitMix64 (splitmix64.hpp:20-43). */
+int ph0b_generate_cloud(uint32_t kind, uint64_t n, uint64_t d, uint64_t seed, uint32_t clusters,
+                        double sigma, double lo, double hi, uint64_t n_background,
+                        double* out_colmajor);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* PH0B_H */

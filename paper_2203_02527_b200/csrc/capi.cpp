@@ -1,0 +1,345 @@
+// C ABI (include/ph0b.h): validation with the reference's error behaviour, result marshalling.
+#include <cuda_runtime.h>
+
+#include <cmath>
+#include <cstdlib>
+#include <cstring>
+#include <new>
+#include <string>
+#include <vector>
+
+#include "../../include/ph0b.h"
+#include "pipeline.h"
+
+using ph0b::Context;
+using ph0b::RunOutputs;
+using ph0b::Status;
+using ph0b::StopAfter;
+
+namespace {
+
+thread_local std::string g_last_error;
+thread_local uint64_t g_last_launches = 0;
+
+int fail(const Status& s) {
+    g_last_error = s.msg;
+    return s.code;
+}
+int fail(int code, const std::string& msg) {
+    g_last_error = msg;
+    return code;
+}
+
+struct Opts {
+    int device = 0;
+    uint32_t flags = 0;
+    uint32_t workers = 1;
+};
+
+// Validation mirrors the reference's throws: filtration.cpp:10-11 (N > 2^32-1),
+// reduction.cpp:134 (workers < 1); PH0B_MAX_POINTS is this build's packing limit.
+int parse(const ph0b_options* opt, uint64_t n, uint32_t layout, Opts* o) {
+    if (opt && opt->struct_size != 0) {
+        if (opt->struct_size < sizeof(ph0b_options))
+            return fail(PH0B_ERR_INVALID_ARGUMENT, "ph0b_options.struct_size too small");
+        o->device = opt->device;
+        o->flags = opt->flags;
+        o->workers = opt->workers;
+        if (opt->workers < 1)
+            return fail(PH0B_ERR_INVALID_ARGUMENT, "worker count must be at least 1");
+    }
+    if (layout != PH0B_COL_MAJOR && layout != PH0B_ROW_MAJOR)
+        return fail(PH0B_ERR_INVALID_ARGUMENT, "layout must be PH0B_COL_MAJOR or PH0B_ROW_MAJOR");
+    if (n > 0xFFFFFFFFull)
+        return fail(PH0B_ERR_TOO_LARGE, "point cloud too large for 32-bit vertex indices");
+    if (n > PH0B_MAX_POINTS)
+        return fail(PH0B_ERR_TOO_LARGE,
+                    "point cloud too large for this build (N <= " +
+                        std::to_string(PH0B_MAX_POINTS) + ")");
+    return PH0B_OK;
+}
+
+// Host-side finiteness check (PointCloud ctor, point_cloud.cpp:15-18) before any device work.
+bool all_finite(const double* x, uint64_t count) {
+    for (uint64_t i = 0; i < count; ++i)
+        if (!std::isfinite(x[i])) return false;
+    return true;
+}
+
+Context* ctx_for(int device, int* rc) {
+    Status st;
+    Context* c = ph0b::default_context(device, &st);
+    if (!c) *rc = fail(st);
+    return c;
+}
+
+int copy_out(Context* c, const RunOutputs& r, cudaStream_t s, uint64_t* death_grade,
+             double* death_length, double* scale, uint64_t scale_capacity, bool want_scale) {
+    if (r.n_finite) {
+        if (cudaMemcpyAsync(death_grade, r.d_death_grade, r.n_finite * 8, cudaMemcpyDeviceToHost,
+                            s) != cudaSuccess ||
+            cudaMemcpyAsync(death_length, r.d_death_length, r.n_finite * 8,
+                            cudaMemcpyDeviceToHost, s) != cudaSuccess)
+            return fail(PH0B_ERR_CUDA, std::string("D2H bars: ") +
+                                           cudaGetErrorString(cudaGetLastError()));
+    }
+    if (want_scale && r.n_scale) {
+        if (!scale || scale_capacity < r.n_scale)
+            return fail(PH0B_ERR_CAPACITY, "scale buffer too small: need " +
+                                               std::to_string(r.n_scale) + " entries");
+        if (cudaMemcpyAsync(scale, r.d_scale, r.n_scale * 8, cudaMemcpyDeviceToHost, s) !=
+            cudaSuccess)
+            return fail(PH0B_ERR_CUDA, std::string("D2H scale: ") +
+                                           cudaGetErrorString(cudaGetLastError()));
+    }
+    const cudaError_t e = cudaStreamSynchronize(s);
+    if (e != cudaSuccess) return fail(PH0B_ERR_CUDA, std::string("D2H: ") + cudaGetErrorString(e));
+    (void)c;
+    return PH0B_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+const char* ph0b_last_error(void) { return g_last_error.c_str(); }
+uint32_t ph0b_abi_version(void) { return PH0B_ABI_VERSION; }
+uint64_t ph0b_last_launch_count(void) { return g_last_launches; }
+
+void* ph0b_host_alloc(uint64_t bytes) {
+    void* p = nullptr;
+    if (cudaHostAlloc(&p, bytes ? bytes : 1, cudaHostAllocDefault) != cudaSuccess) {
+        cudaGetLastError();
+        return nullptr;
+    }
+    return p;
+}
+void ph0b_host_free(void* p) {
+    if (p) cudaFreeHost(p);
+}
+
+int ph0b_context_create(int device, ph0b_context** out) {
+    if (!out) return fail(PH0B_ERR_INVALID_ARGUMENT, "null context pointer");
+    auto* c = new (std::nothrow) Context(device);
+    if (!c) return fail(PH0B_ERR_OUT_OF_MEMORY, "host allocation failed");
+    Status s = c->init();
+    if (!s.good()) {
+        delete c;
+        return fail(s);
+    }
+    *out = reinterpret_cast<ph0b_context*>(c);
+    return PH0B_OK;
+}
+
+void ph0b_context_destroy(ph0b_context* ctx) { delete reinterpret_cast<Context*>(ctx); }
+
+int ph0b_context_reserve(ph0b_context* ctx, uint64_t n, uint64_t d) {
+    Context* c = reinterpret_cast<Context*>(ctx);
+    std::lock_guard<std::mutex> lk(c->mu);
+    Status s = c->reserve(n, d);
+    return s.good() ? PH0B_OK : fail(s);
+}
+
+uint64_t ph0b_context_workspace_bytes(const ph0b_context* ctx) {
+    return reinterpret_cast<const Context*>(ctx)->workspace_bytes();
+}
+
+int ph0b_run_device(ph0b_context* ctx, const double* dX, uint64_t n, uint64_t d, uint32_t layout,
+                    void* stream, ph0b_device_result* out) {
+    Opts o;
+    int rc = parse(nullptr, n, layout, &o);
+    if (rc) return rc;
+    Context* c = reinterpret_cast<Context*>(ctx);
+    std::lock_guard<std::mutex> lk(c->mu);
+    RunOutputs r;
+    Status s = c->run(dX, n, d, layout, static_cast<cudaStream_t>(stream), StopAfter::Barcode,
+                      false, &r);
+    g_last_launches = c->launches;
+    if (!s.good()) return fail(s);
+    if (out) {
+        out->n_finite = r.n_finite;
+        out->essential_count = r.essential;
+        out->n_scale = r.n_scale;
+        out->d_scale = r.d_scale;
+        out->d_death_grade = r.d_death_grade;
+        out->d_death_length = r.d_death_length;
+        out->times = r.times;
+    }
+    return PH0B_OK;
+}
+
+int ph0b_run_host(ph0b_context* ctx, const double* X, uint64_t n, uint64_t d, uint32_t layout,
+                  void* stream, uint64_t* death_grade, double* death_length, uint64_t* n_finite,
+                  uint64_t* essential_count, double* scale, uint64_t scale_capacity,
+                  uint64_t* n_scale, ph0b_stage_times* times) {
+    Opts o;
+    int rc = parse(nullptr, n, layout, &o);
+    if (rc) return rc;
+    if (n * d && !X) return fail(PH0B_ERR_INVALID_ARGUMENT, "null point cloud");
+    if (!all_finite(X, n * d))
+        return fail(PH0B_ERR_NONFINITE, "point cloud contains non-finite coordinates");
+    Context* c = reinterpret_cast<Context*>(ctx);
+    std::lock_guard<std::mutex> lk(c->mu);
+    cudaStream_t s = stream ? static_cast<cudaStream_t>(stream) : c->own_stream();
+    RunOutputs r;
+    Status st = c->run_host_input(X, n, d, layout, s, StopAfter::Barcode, false, &r);
+    g_last_launches = c->launches;
+    if (!st.good()) return fail(st);
+    rc = copy_out(c, r, s, death_grade, death_length, scale, scale_capacity, scale != nullptr);
+    if (rc) return rc;
+    if (n_finite) *n_finite = r.n_finite;
+    if (essential_count) *essential_count = r.essential;
+    if (n_scale) *n_scale = r.n_scale;
+    if (times) *times = r.times;
+    return PH0B_OK;
+}
+
+int ph0b_h0_barcode_into(const double* X, uint64_t n, uint64_t d, uint32_t layout,
+                         const ph0b_options* opt, uint64_t* death_grade, double* death_length,
+                         uint64_t* n_finite, uint64_t* essential_count, double* scale,
+                         uint64_t scale_capacity, uint64_t* n_scale, ph0b_stage_times* times) {
+    Opts o;
+    int rc = parse(opt, n, layout, &o);
+    if (rc) return rc;
+    if (n * d && !X) return fail(PH0B_ERR_INVALID_ARGUMENT, "null point cloud");
+    if (!all_finite(X, n * d))
+        return fail(PH0B_ERR_NONFINITE, "point cloud contains non-finite coordinates");
+    Context* c = ctx_for(o.device, &rc);
+    if (!c) return rc;
+    if (o.flags & PH0B_FLAG_NO_SCALE) scale = nullptr;
+    return ph0b_run_host(reinterpret_cast<ph0b_context*>(c), X, n, d, layout, nullptr,
+                         death_grade, death_length, n_finite, essential_count, scale,
+                         scale_capacity, n_scale, times);
+}
+
+int ph0b_h0_barcode(const double* X, uint64_t n, uint64_t d, uint32_t layout,
+                    const ph0b_options* opt, ph0b_result* out) {
+    if (!out) return fail(PH0B_ERR_INVALID_ARGUMENT, "null result");
+    std::memset(out, 0, sizeof(*out));
+    Opts o;
+    int rc = parse(opt, n, layout, &o);
+    if (rc) return rc;
+    if (n * d && !X) return fail(PH0B_ERR_INVALID_ARGUMENT, "null point cloud");
+    if (!all_finite(X, n * d))
+        return fail(PH0B_ERR_NONFINITE, "point cloud contains non-finite coordinates");
+    Context* c = ctx_for(o.device, &rc);
+    if (!c) return rc;
+    std::lock_guard<std::mutex> lk(c->mu);
+    cudaStream_t s = c->own_stream();
+    RunOutputs r;
+    Status st = c->run_host_input(X, n, d, layout, s, StopAfter::Barcode, false, &r);
+    g_last_launches = c->launches;
+    if (!st.good()) return fail(st);
+    const bool want_scale = !(o.flags & PH0B_FLAG_NO_SCALE);
+    out->death_grade = static_cast<uint64_t*>(std::malloc(std::max<uint64_t>(1, r.n_finite) * 8));
+    out->death_length = static_cast<double*>(std::malloc(std::max<uint64_t>(1, r.n_finite) * 8));
+    if (want_scale)
+        out->scale = static_cast<double*>(std::malloc(std::max<uint64_t>(1, r.n_scale) * 8));
+    if (!out->death_grade || !out->death_length || (want_scale && !out->scale)) {
+        ph0b_result_free(out);
+        return fail(PH0B_ERR_OUT_OF_MEMORY, "host allocation of the result failed");
+    }
+    rc = copy_out(c, r, s, out->death_grade, out->death_length, out->scale, r.n_scale, want_scale);
+    if (rc) {
+        ph0b_result_free(out);
+        return rc;
+    }
+    out->n_finite = r.n_finite;
+    out->essential_count = r.essential;
+    out->n_scale = r.n_scale;
+    out->times = r.times;
+    return PH0B_OK;
+}
+
+void ph0b_result_free(ph0b_result* r) {
+    if (!r) return;
+    std::free(r->death_grade);
+    std::free(r->death_length);
+    std::free(r->scale);
+    r->death_grade = nullptr;
+    r->death_length = nullptr;
+    r->scale = nullptr;
+}
+
+int ph0b_pairwise_distances(const double* X, uint64_t n, uint64_t d, uint32_t layout,
+                            const ph0b_options* opt, double* lengths) {
+    Opts o;
+    int rc = parse(opt, n, layout, &o);
+    if (rc) return rc;
+    if (n * d && !X) return fail(PH0B_ERR_INVALID_ARGUMENT, "null point cloud");
+    if (!all_finite(X, n * d))
+        return fail(PH0B_ERR_NONFINITE, "point cloud contains non-finite coordinates");
+    Context* c = ctx_for(o.device, &rc);
+    if (!c) return rc;
+    std::lock_guard<std::mutex> lk(c->mu);
+    cudaStream_t s = c->own_stream();
+    RunOutputs r;
+    Status st = c->run_host_input(X, n, d, layout, s, StopAfter::Distance, false, &r);
+    g_last_launches = c->launches;
+    if (!st.good()) return fail(st);
+    if (r.k && cudaMemcpyAsync(lengths, r.d_lengths_umajor, r.k * 8, cudaMemcpyDeviceToHost, s) !=
+                   cudaSuccess)
+        return fail(PH0B_ERR_CUDA, "D2H lengths");
+    if (cudaStreamSynchronize(s) != cudaSuccess) return fail(PH0B_ERR_CUDA, "D2H lengths");
+    return PH0B_OK;
+}
+
+int ph0b_build_filtration(const double* X, uint64_t n, uint64_t d, uint32_t layout,
+                          const ph0b_options* opt, uint32_t* u, uint32_t* v, uint64_t* grade,
+                          double* scale, uint64_t* n_scale) {
+    Opts o;
+    int rc = parse(opt, n, layout, &o);
+    if (rc) return rc;
+    if (n * d && !X) return fail(PH0B_ERR_INVALID_ARGUMENT, "null point cloud");
+    if (!all_finite(X, n * d))
+        return fail(PH0B_ERR_NONFINITE, "point cloud contains non-finite coordinates");
+    Context* c = ctx_for(o.device, &rc);
+    if (!c) return rc;
+    std::lock_guard<std::mutex> lk(c->mu);
+    cudaStream_t s = c->own_stream();
+    RunOutputs r;
+    Status st = c->run_host_input(X, n, d, layout, s, StopAfter::Filtration, true, &r);
+    g_last_launches = c->launches;
+    if (!st.good()) return fail(st);
+    if (n_scale) *n_scale = r.n_scale;
+    if (r.k == 0) return PH0B_OK;
+    std::vector<uint32_t> uv(r.k), g(r.k);
+    if (cudaMemcpyAsync(uv.data(), r.d_uv_sorted, r.k * 4, cudaMemcpyDeviceToHost, s) ||
+        cudaMemcpyAsync(g.data(), r.d_grade, r.k * 4, cudaMemcpyDeviceToHost, s) ||
+        (scale && cudaMemcpyAsync(scale, r.d_scale, r.n_scale * 8, cudaMemcpyDeviceToHost, s)) ||
+        cudaStreamSynchronize(s))
+        return fail(PH0B_ERR_CUDA, "D2H filtration");
+    for (uint64_t i = 0; i < r.k; ++i) {
+        if (u) u[i] = uv[i] >> 16;
+        if (v) v[i] = uv[i] & 0xFFFFu;
+        if (grade) grade[i] = g[i];
+    }
+    return PH0B_OK;
+}
+
+int ph0b_claimed_lows(const double* X, uint64_t n, uint64_t d, uint32_t layout,
+                      const ph0b_options* opt, uint32_t* lows, uint64_t* n_lows) {
+    Opts o;
+    int rc = parse(opt, n, layout, &o);
+    if (rc) return rc;
+    if (n * d && !X) return fail(PH0B_ERR_INVALID_ARGUMENT, "null point cloud");
+    if (!all_finite(X, n * d))
+        return fail(PH0B_ERR_NONFINITE, "point cloud contains non-finite coordinates");
+    Context* c = ctx_for(o.device, &rc);
+    if (!c) return rc;
+    std::lock_guard<std::mutex> lk(c->mu);
+    cudaStream_t s = c->own_stream();
+    RunOutputs r;
+    Status st = c->run_host_input(X, n, d, layout, s, StopAfter::Barcode, false, &r);
+    if (!st.good()) return fail(st);
+    if (n_lows) *n_lows = r.n_finite;
+    if (r.n_finite == 0) return PH0B_OK;
+    st = c->claimed_lows(r, (uint32_t)n, c->lows_buffer(), s);
+    g_last_launches = c->launches;
+    if (!st.good()) return fail(st);
+    if (cudaMemcpy(lows, c->lows_buffer(), r.n_finite * 4, cudaMemcpyDeviceToHost) != cudaSuccess)
+        return fail(PH0B_ERR_CUDA, "D2H lows");
+    return PH0B_OK;
+}
+
+}  // extern "C"

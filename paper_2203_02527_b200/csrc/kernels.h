@@ -1,0 +1,105 @@
+// Host-side launchers for the sm_100a kernels (one .cu per subsystem).  Internal header.
+#pragma once
+
+#include <cstdint>
+#include <cuda_runtime.h>
+
+namespace ph0b {
+
+// ---- K1: tiled upper-triangle distance kernel (distance.cu) ----------------------------
+struct DistanceArgs {
+    const double* xpad;   // device, coordinate-major [d][ldx], zero padded (ldx % 128 == 0)
+    uint64_t ldx;
+    uint32_t n, d;
+    uint64_t* keys;       // [K] f64 length bits, u-major edge order
+    uint32_t* vals;       // [K] u << 16 | v
+    uint64_t* minmax;     // [2] running min / max key (init ~0 / 0)
+    uint32_t* hist0;      // [256] histogram of raw key bits 0..7
+};
+// Returns number of kernel launches issued (0 on error; check cudaGetLastError).
+int launch_distance(const DistanceArgs& a, cudaStream_t s, int num_sms);
+
+// Reorders a host-provided cloud into the padded coordinate-major layout.
+int launch_pack_points(const double* x, uint32_t layout, uint32_t n, uint32_t d, double* xpad,
+                       uint64_t ldx, uint32_t* nonfinite_flag, cudaStream_t s);
+
+// ---- K2: onesweep LSD radix sort (radix_sort.cu) ---------------------------------------
+struct SortPlan {
+    uint32_t passes;      // digit passes actually executed
+    uint32_t shift[8];    // bit position of each executed digit
+};
+struct SortArgs {
+    uint64_t count;
+    uint64_t kmin;              // keys are ordered by (key - kmin)
+    uint64_t* keys[2];          // ping-pong
+    uint32_t* vals[2];          // ping-pong (may be null: keys only)
+    uint64_t* status;           // look-back status [tiles][256]
+    uint32_t* hist;             // [8][256] global digit histograms (device)
+    uint32_t* tile_counter;     // [8] dynamic tile ids per pass
+    uint32_t epoch_base;        // look-back epoch of pass 0 (unique per pass, per call)
+    uint32_t hist0_rot;         // hist row 0 is indexed (digit + rot) & 255 (raw low byte)
+};
+uint64_t sort_tiles(uint64_t count);
+// Runs the passes listed in plan; returns the buffer index (0/1) holding the result.
+// hist[p][*] must already hold the digit-p histogram of (key-kmin) for p = 0 (the
+// remaining histograms are produced by the passes themselves).
+int launch_sort_passes(const SortArgs& a, const SortPlan& plan, cudaStream_t s, int num_sms,
+                       int* launches);
+// Histogram of digit `shift` of (key - kmin) over all keys (used when hist0 is unusable).
+int launch_digit_histogram(const uint64_t* keys, uint64_t count, uint64_t kmin, uint32_t shift,
+                           uint32_t* hist, cudaStream_t s, int num_sms);
+
+// ---- K2c/K3: flag-and-scan unique -> D, and boundary matrix grades (unique.cu) ----------
+struct UniqueArgs {
+    const uint64_t* keys;   // sorted raw keys (f64 length bits)
+    uint64_t count;
+    double* scale;          // out: D
+    uint32_t* grade;        // out (optional): 1-based grade per column
+    uint64_t* status;       // look-back status [tiles]
+    uint32_t* tile_counter;
+    uint64_t* n_scale;      // out: |D| (device)
+    uint32_t epoch;
+};
+int launch_unique(const UniqueArgs& a, cudaStream_t s);
+
+// ---- K4: GPU column reduction (reduce.cu) ----------------------------------------------
+struct ReduceState {
+    uint32_t n;
+    uint64_t k;
+    const uint32_t* uv;      // sorted columns (u << 16 | v), filtration order
+    uint32_t* comp;          // [n] component label (root)
+    uint32_t* best;          // [2n]: per-root minimum candidate column | hook parent
+    uint32_t* cand[2];       // candidate column ids (capacity cap)
+    uint64_t cap;
+    uint32_t* surv;          // [n] survivor column ids (unordered)
+    uint32_t* counters;      // [8] device counters (see reduce.cu)
+    uint64_t* scan_status;   // look-back status for ordered compaction
+    uint32_t* scan_tile_counter;
+    uint32_t* pair_min;      // [kPairMax] sparse phase
+    uint8_t* cid;            // [n] compact component ids (sparse phase)
+    uint32_t* host_counters; // pinned host mirror [8]
+};
+struct ReduceStats {
+    uint32_t rounds = 0;
+    uint32_t iterations = 0;
+    uint64_t scanned = 0;     // columns streamed
+    uint32_t survivors = 0;
+    int launches = 0;
+};
+// Runs the full reduction; leaves survivor column ids (unordered) in st.surv.
+int run_reduction(ReduceState& st, cudaStream_t s, int num_sms, uint32_t& epoch,
+                  ReduceStats* stats);
+
+// ---- K5: barcode collect (collect.cu) --------------------------------------------------
+// cols_sorted: survivor column ids in filtration order (u64, from the keys-only sort).
+// Writes surv_sorted (u32), death_grade = 1 + lower_bound(D, length), death_length.
+int launch_collect_map(const uint64_t* cols_sorted, uint32_t m, const uint64_t* sorted_keys,
+                       const double* scale, const uint64_t* n_scale, uint32_t* surv_sorted,
+                       uint64_t* death_grade, double* death_length, cudaStream_t s);
+int launch_widen(const uint32_t* in, uint32_t m, uint64_t* out, cudaStream_t s);
+
+// Claimed lows (reduction.cpp:44-45) of survivors in filtration order: single-CTA union-find.
+int launch_claimed_lows(const uint32_t* surv_sorted, uint32_t m, const uint32_t* uv, uint32_t n,
+                        uint32_t* lows, cudaStream_t s);
+
+}  // namespace ph0b

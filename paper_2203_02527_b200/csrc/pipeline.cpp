@@ -1,0 +1,346 @@
+// Host orchestration of the B200 H0 pipeline: workspace management and the stage order of
+// proj/src/bench.cpp:45-59 (distances -> filtration -> matrix -> reduce -> barcode).
+#include "pipeline.h"
+
+#include <algorithm>
+#include <cstring>
+#include <map>
+#include <memory>
+
+#include "kernels.h"
+
+namespace ph0b {
+namespace {
+
+constexpr uint64_t kCandCap = 1ull << 25;  // reduction candidate buffer (columns)
+
+Status cuda_fail(cudaError_t e, const char* what) {
+    Status s;
+    s.code = (e == cudaErrorMemoryAllocation) ? PH0B_ERR_OUT_OF_MEMORY : PH0B_ERR_CUDA;
+    s.msg = std::string(what) + ": " + cudaGetErrorString(e);
+    return s;
+}
+
+#define PH0B_TRY(expr, what)                                         \
+    do {                                                             \
+        const cudaError_t e_ = (expr);                               \
+        if (e_ != cudaSuccess) return cuda_fail(e_, what);           \
+    } while (0)
+
+#define PH0B_CHECK_LAUNCH(what)                                      \
+    do {                                                             \
+        const cudaError_t e_ = cudaGetLastError();                   \
+        if (e_ != cudaSuccess) return cuda_fail(e_, what);           \
+    } while (0)
+
+inline uint32_t span_passes(uint64_t span, SortPlan* plan) {
+    const uint32_t bits = span ? 64u - (uint32_t)__builtin_clzll(span) : 0u;
+    plan->passes = (bits + 7) / 8;
+    for (uint32_t p = 0; p < plan->passes; ++p) plan->shift[p] = 8 * p;
+    return plan->passes;
+}
+
+}  // namespace
+
+Context::Context(int device) : device_(device) {}
+
+Context::~Context() {
+    cudaSetDevice(device_);
+    void* ps[] = {xin_,  xpad_, keys_[0], keys_[1], vals_[0], vals_[1], status_,
+                  grade_, comp_, best_, surv_, surv_sorted_, lows_, cand_[0], cand_[1],
+                  survkeys_[0], survkeys_[1], death_grade_, death_length_, hist_, counters_,
+                  small_};
+    for (void* p : ps)
+        if (p) cudaFree(p);
+    if (h_small_) cudaFreeHost(h_small_);
+    if (h_counters_) cudaFreeHost(h_counters_);
+    for (auto& e : ev_)
+        if (e) cudaEventDestroy(e);
+    if (stream_) cudaStreamDestroy(stream_);
+}
+
+Status Context::init() {
+    int count = 0;
+    if (cudaGetDeviceCount(&count) != cudaSuccess || count <= device_ || device_ < 0) {
+        cudaGetLastError();
+        return {PH0B_ERR_NO_DEVICE, "no CUDA device " + std::to_string(device_) + " visible"};
+    }
+    PH0B_TRY(cudaSetDevice(device_), "cudaSetDevice");
+    cudaDeviceProp prop;
+    PH0B_TRY(cudaGetDeviceProperties(&prop, device_), "cudaGetDeviceProperties");
+    if (prop.major != 10) {
+        return {PH0B_ERR_NO_DEVICE, std::string("device ") + prop.name +
+                                        " is not sm_100 (this build targets sm_100a only)"};
+    }
+    num_sms_ = prop.multiProcessorCount;
+    PH0B_TRY(cudaStreamCreateWithFlags(&stream_, cudaStreamNonBlocking), "cudaStreamCreate");
+    for (auto& e : ev_) PH0B_TRY(cudaEventCreate(&e), "cudaEventCreate");
+    PH0B_TRY(cudaMalloc(&hist_, sizeof(uint32_t) * 8 * 256), "cudaMalloc hist");
+    PH0B_TRY(cudaMalloc(&counters_, sizeof(uint32_t) * 64), "cudaMalloc counters");
+    PH0B_TRY(cudaMalloc(&small_, sizeof(uint64_t) * 8), "cudaMalloc small");
+    PH0B_TRY(cudaHostAlloc(&h_small_, sizeof(uint64_t) * 8, cudaHostAllocDefault), "cudaHostAlloc");
+    PH0B_TRY(cudaHostAlloc(&h_counters_, sizeof(uint32_t) * 64, cudaHostAllocDefault),
+             "cudaHostAlloc");
+    bytes_ += 8 * 256 * 4 + 64 * 4 + 64;
+    return Status::ok();
+}
+
+Status Context::grow(void** p, uint64_t* cap, uint64_t need) {
+    if (need <= *cap) return Status::ok();
+    if (*p) {
+        cudaFree(*p);
+        bytes_ -= *cap;
+        *p = nullptr;
+        *cap = 0;
+    }
+    need = (need + 255) & ~255ull;
+    const cudaError_t e = cudaMalloc(p, need);
+    if (e != cudaSuccess) {
+        cudaGetLastError();
+        Status s;
+        s.code = PH0B_ERR_OUT_OF_MEMORY;
+        s.msg = "device allocation of " + std::to_string(need) + " bytes failed (" +
+                cudaGetErrorString(e) + ")";
+        return s;
+    }
+    *cap = need;
+    bytes_ += need;
+    return Status::ok();
+}
+
+Status Context::reserve(uint64_t n, uint64_t d) {
+    PH0B_TRY(cudaSetDevice(device_), "cudaSetDevice");
+    const uint64_t k = n * (n - (n > 0)) / 2;
+    const uint64_t ldx = std::max<uint64_t>(128, (n + 127) / 128 * 128);
+    const uint64_t tiles = sort_tiles(std::max<uint64_t>(k, 1));
+    const uint64_t status_words = std::max<uint64_t>(tiles * 256, sort_tiles(n + 1) * 256);
+    const uint64_t cand = std::max<uint64_t>(1, std::min<uint64_t>(k, kCandCap));
+    Status s;
+#define G(ptr, cap, bytes)                                                    \
+    if (!(s = grow(reinterpret_cast<void**>(&(ptr)), &(cap), (bytes))).good()) return s;
+    G(xin_, xin_cap_, std::max<uint64_t>(8, n * d * 8));
+    G(xpad_, xpad_cap_, std::max<uint64_t>(8, d * ldx * 8));
+    for (int i = 0; i < 2; ++i) {
+        G(keys_[i], keys_cap_[i], std::max<uint64_t>(8, k * 8));
+        G(vals_[i], vals_cap_[i], std::max<uint64_t>(4, k * 4));
+        G(cand_[i], cand_cap_[i], cand * 4);
+        G(survkeys_[i], survkeys_cap_[i], std::max<uint64_t>(8, n * 8));
+    }
+    if (status_words * 8 > status_cap_) status_zeroed_ = false;
+    G(status_, status_cap_, status_words * 8);
+    G(comp_, comp_cap_, std::max<uint64_t>(4, n * 4));
+    G(best_, best_cap_, std::max<uint64_t>(8, 2 * n * 4));
+    G(surv_, surv_cap_, std::max<uint64_t>(4, n * 4));
+    G(surv_sorted_, surv_sorted_cap_, std::max<uint64_t>(4, n * 4));
+    G(lows_, lows_cap_, std::max<uint64_t>(4, n * 4));
+    G(death_grade_, death_grade_cap_, std::max<uint64_t>(8, n * 8));
+    G(death_length_, death_length_cap_, std::max<uint64_t>(8, n * 8));
+#undef G
+    if (!status_zeroed_) {
+        PH0B_TRY(cudaMemset(status_, 0, status_cap_), "cudaMemset status");
+        epoch_ = 1;
+        status_zeroed_ = true;
+    }
+    return Status::ok();
+}
+
+uint32_t Context::next_epochs(uint32_t count, cudaStream_t s) {
+    if (epoch_ + count >= (1u << 30) - 1) {
+        cudaMemsetAsync(status_, 0, status_cap_, s);
+        epoch_ = 1;
+    }
+    const uint32_t e = epoch_;
+    epoch_ += count;
+    return e;
+}
+
+Status Context::run_host_input(const double* X, uint64_t n, uint64_t d, uint32_t layout,
+                               cudaStream_t stream, StopAfter stop, bool want_grade,
+                               RunOutputs* out) {
+    Status s = reserve(n, d);
+    if (!s.good()) return s;
+    if (n * d)
+        PH0B_TRY(cudaMemcpyAsync(xin_, X, n * d * 8, cudaMemcpyHostToDevice, stream),
+                 "H2D point cloud");
+    return run(xin_, n, d, layout, stream, stop, want_grade, out);
+}
+
+Status Context::run(const double* dX, uint64_t n, uint64_t d, uint32_t layout,
+                    cudaStream_t stream, StopAfter stop, bool want_grade, RunOutputs* out) {
+    Status s = reserve(n, d);
+    if (!s.good()) return s;
+    cudaStream_t st = stream ? stream : stream_;
+    launches = 0;
+    const uint64_t k = n * (n - (n > 0)) / 2;
+    const uint64_t ldx = std::max<uint64_t>(128, (n + 127) / 128 * 128);
+    RunOutputs r;
+    r.k = k;
+    std::memset(&r.times, 0, sizeof(r.times));
+
+    PH0B_TRY(cudaEventRecord(ev_[0], st), "event");
+    // ---- K1: pack + distances ------------------------------------------------------------
+    PH0B_TRY(cudaMemsetAsync(small_, 0xFF, 8, st), "memset");        // min = ~0
+    PH0B_TRY(cudaMemsetAsync(small_ + 1, 0, 3 * 8, st), "memset");   // max, n_scale, flag
+    PH0B_TRY(cudaMemsetAsync(hist_, 0, 256 * 4, st), "memset");
+    launches += launch_pack_points(dX, layout, (uint32_t)n, (uint32_t)d, xpad_, ldx,
+                                   reinterpret_cast<uint32_t*>(small_ + 3), st);
+    PH0B_CHECK_LAUNCH("pack_points");
+    DistanceArgs da{xpad_, ldx, (uint32_t)n, (uint32_t)d, keys_[0], vals_[0], small_, hist_};
+    launches += launch_distance(da, st, num_sms_);
+    PH0B_CHECK_LAUNCH("distance kernel");
+    PH0B_TRY(cudaEventRecord(ev_[1], st), "event");
+    PH0B_TRY(cudaMemcpyAsync(h_small_, small_, 4 * 8, cudaMemcpyDeviceToHost, st), "D2H");
+    PH0B_TRY(cudaStreamSynchronize(st), "distance stage");
+    if (static_cast<uint32_t>(h_small_[3]) != 0)
+        return {PH0B_ERR_NONFINITE, "point cloud contains non-finite coordinates"};
+    const uint64_t kmin = h_small_[0], kmax = h_small_[1];
+    r.d_lengths_umajor = keys_[0];
+    if (stop == StopAfter::Distance || k == 0) {
+        r.essential = n;
+        PH0B_TRY(cudaEventRecord(ev_[5], st), "event");
+        PH0B_TRY(cudaEventSynchronize(ev_[5]), "sync");
+        cudaEventElapsedTime(&r.times.distance_ms, ev_[0], ev_[1]);
+        cudaEventElapsedTime(&r.times.total_ms, ev_[0], ev_[5]);
+        r.d_scale = reinterpret_cast<const double*>(keys_[1]);
+        r.d_uv_sorted = vals_[0];
+        r.d_grade = grade_;
+        if (out) *out = r;
+        return Status::ok();
+    }
+
+    // ---- K2: onesweep radix sort -----------------------------------------------------------
+    SortPlan plan{};
+    span_passes(kmax - kmin, &plan);
+    SortArgs sa{};
+    sa.count = k;
+    sa.kmin = kmin;
+    sa.keys[0] = keys_[0];
+    sa.keys[1] = keys_[1];
+    sa.vals[0] = vals_[0];
+    sa.vals[1] = vals_[1];
+    sa.status = status_;
+    sa.hist = hist_;
+    sa.tile_counter = counters_ + 32;
+    sa.epoch_base = next_epochs(plan.passes + 1, st);
+    sa.hist0_rot = (uint32_t)(kmin & 0xFFu);
+    int sl = 0;
+    const int cur = launch_sort_passes(sa, plan, st, num_sms_, &sl);
+    launches += sl;
+    PH0B_CHECK_LAUNCH("radix sort");
+    PH0B_TRY(cudaEventRecord(ev_[2], st), "event");
+    r.times.sort_passes = plan.passes;
+
+    // ---- K2c/K3: unique -> D (into the free key buffer), grades ---------------------------
+    double* scale = reinterpret_cast<double*>(keys_[cur ^ 1]);
+    if (want_grade) {
+        s = grow(reinterpret_cast<void**>(&grade_), &grade_cap_, std::max<uint64_t>(4, k * 4));
+        if (!s.good()) return s;
+    }
+    UniqueArgs ua{keys_[cur], k, scale, want_grade ? grade_ : nullptr, status_,
+                  counters_ + 40, small_ + 2, next_epochs(1, st)};
+    launches += launch_unique(ua, st);
+    PH0B_CHECK_LAUNCH("unique kernel");
+    PH0B_TRY(cudaEventRecord(ev_[3], st), "event");
+    r.d_uv_sorted = vals_[cur];
+    r.d_grade = want_grade ? grade_ : nullptr;
+    r.d_scale = scale;
+
+    if (stop == StopAfter::Barcode) {
+        // ---- K4: column reduction ----------------------------------------------------------
+        ReduceState rs{};
+        rs.n = (uint32_t)n;
+        rs.k = k;
+        rs.uv = vals_[cur];
+        rs.comp = comp_;
+        rs.best = best_;
+        rs.cand[0] = cand_[0];
+        rs.cand[1] = cand_[1];
+        rs.cap = cand_cap_[0] / 4;
+        rs.surv = surv_;
+        rs.counters = counters_;
+        rs.host_counters = h_counters_;
+        ReduceStats rst;
+        uint32_t ep = 0;
+        run_reduction(rs, st, num_sms_, ep, &rst);
+        launches += rst.launches;
+        PH0B_CHECK_LAUNCH("reduction");
+        PH0B_TRY(cudaEventRecord(ev_[4], st), "event");
+        r.times.reduce_rounds = rst.rounds;
+        r.times.columns_scanned = rst.scanned;
+        const uint32_t m = rst.survivors;
+        if (m != n - 1)
+            return {PH0B_ERR_CUDA, "internal error: reduction produced " + std::to_string(m) +
+                                       " surviving columns, expected " + std::to_string(n - 1)};
+
+        // ---- K5: collect: survivors in filtration order -> intervals ----------------------
+        launches += launch_widen(surv_, m, survkeys_[0], st);
+        SortPlan sp{};
+        span_passes(k - 1, &sp);
+        PH0B_TRY(cudaMemsetAsync(hist_, 0, 256 * 4, st), "memset");
+        launches += launch_digit_histogram(survkeys_[0], m, 0, 0, hist_, st, num_sms_);
+        SortArgs sv{};
+        sv.count = m;
+        sv.kmin = 0;
+        sv.keys[0] = survkeys_[0];
+        sv.keys[1] = survkeys_[1];
+        sv.status = status_;
+        sv.hist = hist_;
+        sv.tile_counter = counters_ + 48;
+        sv.epoch_base = next_epochs(sp.passes + 1, st);
+        sv.hist0_rot = 0;
+        int l2 = 0;
+        const int c2 = launch_sort_passes(sv, sp, st, num_sms_, &l2);
+        launches += l2;
+        launches += launch_collect_map(survkeys_[c2], m, keys_[cur], scale, small_ + 2,
+                                       surv_sorted_, death_grade_, death_length_, st);
+        PH0B_CHECK_LAUNCH("collect");
+        r.d_death_grade = death_grade_;
+        r.d_death_length = death_length_;
+        r.d_surv_sorted = surv_sorted_;
+        r.n_finite = m;
+        r.essential = n - m;
+    }
+    PH0B_TRY(cudaEventRecord(ev_[5], st), "event");
+    PH0B_TRY(cudaMemcpyAsync(h_small_ + 2, small_ + 2, 8, cudaMemcpyDeviceToHost, st), "D2H");
+    PH0B_TRY(cudaStreamSynchronize(st), "pipeline");
+    r.n_scale = h_small_[2];
+    cudaEventElapsedTime(&r.times.distance_ms, ev_[0], ev_[1]);
+    cudaEventElapsedTime(&r.times.sort_ms, ev_[1], ev_[2]);
+    cudaEventElapsedTime(&r.times.unique_ms, ev_[2], ev_[3]);
+    if (stop == StopAfter::Barcode) {
+        cudaEventElapsedTime(&r.times.reduce_ms, ev_[3], ev_[4]);
+        cudaEventElapsedTime(&r.times.collect_ms, ev_[4], ev_[5]);
+    }
+    cudaEventElapsedTime(&r.times.total_ms, ev_[0], ev_[5]);
+    if (out) *out = r;
+    return Status::ok();
+}
+
+Status Context::claimed_lows(const RunOutputs& r, uint32_t n, uint32_t* d_lows,
+                             cudaStream_t stream) {
+    cudaStream_t st = stream ? stream : stream_;
+    launches += launch_claimed_lows(r.d_surv_sorted, (uint32_t)r.n_finite, r.d_uv_sorted, n,
+                                    d_lows, st);
+    PH0B_CHECK_LAUNCH("claimed lows");
+    PH0B_TRY(cudaStreamSynchronize(st), "claimed lows");
+    return Status::ok();
+}
+
+Context* default_context(int device, Status* st) {
+    static std::mutex mu;
+    static std::map<int, std::unique_ptr<Context>> ctxs;
+    std::lock_guard<std::mutex> lk(mu);
+    auto it = ctxs.find(device);
+    if (it != ctxs.end()) return it->second.get();
+    auto c = std::make_unique<Context>(device);
+    Status s = c->init();
+    if (!s.good()) {
+        if (st) *st = s;
+        return nullptr;
+    }
+    Context* p = c.get();
+    ctxs[device] = std::move(c);
+    return p;
+}
+
+}  // namespace ph0b

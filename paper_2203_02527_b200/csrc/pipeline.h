@@ -1,0 +1,100 @@
+// Host-side pipeline context (device workspace, streams, orchestration).  Internal header.
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <cstdint>
+#include <mutex>
+#include <string>
+
+#include "../../include/ph0b.h"
+
+namespace ph0b {
+
+struct Status {
+    int code = PH0B_OK;
+    std::string msg;
+    static Status ok() { return {}; }
+    bool good() const { return code == PH0B_OK; }
+};
+
+enum class StopAfter { Distance, Filtration, Barcode };
+
+struct RunOutputs {
+    // device pointers into the workspace after a run
+    const uint64_t* d_lengths_umajor = nullptr;  // StopAfter::Distance (bits)
+    const uint32_t* d_uv_sorted = nullptr;       // >= Filtration
+    const uint32_t* d_grade = nullptr;           // Filtration with want_grade
+    const double* d_scale = nullptr;             // >= Filtration
+    const uint64_t* d_death_grade = nullptr;     // Barcode
+    const double* d_death_length = nullptr;
+    const uint32_t* d_surv_sorted = nullptr;
+    uint64_t k = 0;
+    uint64_t n_scale = 0;
+    uint64_t n_finite = 0;
+    uint64_t essential = 0;
+    ph0b_stage_times times{};
+};
+
+class Context {
+public:
+    explicit Context(int device);
+    ~Context();
+    Status init();
+    Status reserve(uint64_t n, uint64_t d);
+    uint64_t workspace_bytes() const { return bytes_; }
+
+    // Runs the pipeline on a device-resident cloud.
+    Status run(const double* dX, uint64_t n, uint64_t d, uint32_t layout, cudaStream_t stream,
+               StopAfter stop, bool want_grade, RunOutputs* out);
+    // Host cloud -> device staging buffer, then run().
+    Status run_host_input(const double* X, uint64_t n, uint64_t d, uint32_t layout,
+                          cudaStream_t stream, StopAfter stop, bool want_grade, RunOutputs* out);
+    Status claimed_lows(const RunOutputs& r, uint32_t n, uint32_t* d_lows, cudaStream_t stream);
+    uint32_t* lows_buffer() { return lows_; }
+
+    std::mutex mu;
+    int device() const { return device_; }
+    cudaStream_t own_stream() const { return stream_; }
+    uint64_t launches = 0;
+
+private:
+    Status grow(void** p, uint64_t* cap_bytes, uint64_t need_bytes);
+    uint32_t next_epochs(uint32_t count, cudaStream_t s);
+
+    int device_;
+    int num_sms_ = 148;
+    cudaStream_t stream_ = nullptr;
+    cudaEvent_t ev_[8] = {};
+    uint64_t bytes_ = 0;
+
+    // workspace (capacities in bytes)
+    double* xin_ = nullptr;        uint64_t xin_cap_ = 0;
+    double* xpad_ = nullptr;       uint64_t xpad_cap_ = 0;
+    uint64_t* keys_[2] = {};       uint64_t keys_cap_[2] = {};
+    uint32_t* vals_[2] = {};       uint64_t vals_cap_[2] = {};
+    uint64_t* status_ = nullptr;   uint64_t status_cap_ = 0;
+    uint32_t* grade_ = nullptr;    uint64_t grade_cap_ = 0;
+    uint32_t* comp_ = nullptr;     uint64_t comp_cap_ = 0;
+    uint32_t* best_ = nullptr;     uint64_t best_cap_ = 0;
+    uint32_t* surv_ = nullptr;     uint64_t surv_cap_ = 0;
+    uint32_t* surv_sorted_ = nullptr; uint64_t surv_sorted_cap_ = 0;
+    uint32_t* lows_ = nullptr;     uint64_t lows_cap_ = 0;
+    uint32_t* cand_[2] = {};       uint64_t cand_cap_[2] = {};
+    uint64_t* survkeys_[2] = {};   uint64_t survkeys_cap_[2] = {};
+    uint64_t* death_grade_ = nullptr; uint64_t death_grade_cap_ = 0;
+    double* death_length_ = nullptr;  uint64_t death_length_cap_ = 0;
+    // fixed small buffers
+    uint32_t* hist_ = nullptr;     // [8][256]
+    uint32_t* counters_ = nullptr; // [64]
+    uint64_t* small_ = nullptr;    // [0..1] minmax, [2] n_scale, [3] nonfinite flag (u32)
+    uint64_t* h_small_ = nullptr;  // pinned mirror of small_
+    uint32_t* h_counters_ = nullptr;  // pinned [64]
+    uint32_t epoch_ = 1;
+    bool status_zeroed_ = false;
+};
+
+// Default per-device contexts used by the stateless C entry points.
+Context* default_context(int device, Status* st);
+
+}  // namespace ph0b

@@ -1,0 +1,232 @@
+// K4 — GPU-parallel column reduction of the boundary matrix M over Z2 (replaces
+// ReduceEngine::run, /root/reference/proj/src/reduction.cpp:31-51, and its pivot table
+// claimed_by_, reduction.cpp:121).
+//
+// Why this is the reference's reduction, not an approximation of it:
+//  * Every column of M starts as {u, v} (boundary_matrix.cpp:22-24) and every addition XORs
+//    it with the unique earlier column owning its low (reduction.cpp:36-42), so supports stay
+//    2-sparse.  The claimed columns form a "pivot forest" (claimed row r -> the other row of
+//    its column, always < r), whose roots are the unclaimed rows = the minimum vertex of each
+//    tree.  Reducing column {u, v} walks both endpoints up that forest, XOR by XOR: it empties
+//    iff u and v are in the same tree, and otherwise claims max(root(u), root(v)).
+//  * So a column is a cycle (reduces to 0) exactly when label[u] == label[v] — this is the
+//    clearing filter below, applied in bulk and provably result-preserving — and the
+//    surviving columns are exactly the columns that join two trees, in filtration order:
+//    the minimum spanning forest under the strict column order (length, u, v).
+//
+// Parallel schedule (rounds over windows of the filtration):
+//   (i)   filter: stream the window's columns, drop those whose endpoints share a label
+//         (one 4-byte load + two label gathers per column), compact the rest;
+//   (ii)  resolve the candidates in parallel rounds: every live tree takes the minimum-index
+//         candidate column touching it (atomicMin into a per-tree pivot slot), each such
+//         column is a surviving column (cut property: it is the first column in filtration
+//         order leaving that tree), trees hook along it (mutual pairs keep the smaller root),
+//         labels are re-pointed by pointer jumping, candidates are re-filtered; repeat until
+//         no candidate joins two trees;
+//   (iii) early exit as soon as N-1 columns survived — every later column is provably a
+//         cycle (the reference still walks all K columns).
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cstdint>
+
+#include "common.cuh"
+#include "kernels.h"
+
+namespace ph0b {
+namespace {
+
+constexpr uint32_t kNone = 0xFFFFFFFFu;
+constexpr int kThreads = 256;
+
+// counters[] layout
+constexpr int kCntCand = 0;      // candidates written by the last filter
+constexpr int kCntSurv = 1;      // surviving columns found so far
+constexpr int kCntHooks = 2;     // hooks made by the last resolve round
+constexpr int kCntOverflow = 3;  // filter exceeded the candidate capacity
+
+__global__ void k4_init(uint32_t* comp, uint32_t* best, uint32_t* par, uint32_t n) {
+    for (uint32_t v = blockIdx.x * blockDim.x + threadIdx.x; v < n; v += gridDim.x * blockDim.x) {
+        comp[v] = v;
+        par[v] = v;
+        best[v] = kNone;
+    }
+}
+
+// Clearing filter over columns [begin, end) (list == nullptr) or over a candidate list.
+__global__ void __launch_bounds__(kThreads)
+    k4_filter(const uint32_t* __restrict__ uv, uint64_t begin, uint64_t end,
+              const uint32_t* __restrict__ list, uint32_t list_n,
+              const uint32_t* __restrict__ comp, uint32_t* __restrict__ out, uint64_t cap,
+              uint32_t* counters) {
+    const uint64_t total = list ? (uint64_t)list_n : end - begin;
+    const uint32_t lane = threadIdx.x & 31;
+    const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+    for (uint64_t base = (uint64_t)blockIdx.x * blockDim.x; base < total; base += stride) {
+        const uint64_t i = base + threadIdx.x;
+        bool keep = false;
+        uint32_t j = 0;
+        if (i < total) {
+            j = list ? list[i] : (uint32_t)(begin + i);
+            const uint32_t e = __ldg(uv + j);
+            keep = __ldg(comp + (e >> 16)) != __ldg(comp + (e & 0xFFFFu));
+        }
+        const uint32_t ballot = __ballot_sync(0xffffffffu, keep);
+        if (ballot) {
+            uint32_t slot = 0;
+            if (lane == 0) slot = atomicAdd(&counters[kCntCand], (uint32_t)__popc(ballot));
+            slot = __shfl_sync(0xffffffffu, slot, 0) + __popc(ballot & lanemask_lt());
+            if (keep) {
+                if (slot < cap)
+                    out[slot] = j;
+                else
+                    counters[kCntOverflow] = 1;
+            }
+        }
+    }
+}
+
+// Each live tree's minimum candidate column (its pivot candidate for this round).
+__global__ void __launch_bounds__(kThreads)
+    k4_min_edge(const uint32_t* __restrict__ cand, uint32_t ncand, const uint32_t* __restrict__ uv,
+                const uint32_t* __restrict__ comp, uint32_t* best) {
+    for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < ncand;
+         i += gridDim.x * blockDim.x) {
+        const uint32_t j = cand[i];
+        const uint32_t e = uv[j];
+        const uint32_t cu = comp[e >> 16], cv = comp[e & 0xFFFFu];
+        if (cu == cv) continue;
+        if (j < ld_cg_u32(best + cu)) atomicMin(best + cu, j);
+        if (j < ld_cg_u32(best + cv)) atomicMin(best + cv, j);
+    }
+}
+
+// Hook every tree along its minimum candidate column; record the surviving column.
+__global__ void k4_hook(uint32_t n, const uint32_t* __restrict__ uv,
+                        const uint32_t* __restrict__ comp, const uint32_t* __restrict__ best,
+                        uint32_t* par, uint32_t* surv, uint32_t* counters) {
+    for (uint32_t x = blockIdx.x * blockDim.x + threadIdx.x; x < n; x += gridDim.x * blockDim.x) {
+        if (comp[x] != x) continue;  // not a tree label
+        const uint32_t j = best[x];
+        if (j == kNone) continue;
+        const uint32_t e = uv[j];
+        const uint32_t cu = comp[e >> 16], cv = comp[e & 0xFFFFu];
+        const uint32_t other = (cu == x) ? cv : cu;
+        const bool mutual = best[other] == j;
+        if (mutual && x < other) continue;  // the larger label of a mutual pair hooks
+        par[x] = other;
+        surv[atomicAdd(&counters[kCntSurv], 1u)] = j;
+        counters[kCntHooks] = 1;
+    }
+}
+
+// Pointer jumping on the hooked labels (each label ends at the root of its hook tree).
+__global__ void k4_jump_roots(uint32_t n, const uint32_t* __restrict__ comp, uint32_t* par) {
+    for (uint32_t x = blockIdx.x * blockDim.x + threadIdx.x; x < n; x += gridDim.x * blockDim.x) {
+        if (comp[x] != x) continue;
+        uint32_t r = par[x];
+        if (r == x) continue;
+        uint32_t nx = par[r];
+        while (nx != r) {
+            r = nx;
+            nx = par[r];
+        }
+        // path compression: every pointer written is to the true root
+        uint32_t y = x;
+        while (par[y] != r) {
+            const uint32_t t = par[y];
+            par[y] = r;
+            y = t;
+        }
+    }
+}
+
+__global__ void k4_relabel(uint32_t n, uint32_t* comp, const uint32_t* __restrict__ par,
+                           uint32_t* best) {
+    for (uint32_t v = blockIdx.x * blockDim.x + threadIdx.x; v < n; v += gridDim.x * blockDim.x) {
+        comp[v] = par[comp[v]];
+        best[v] = kNone;
+    }
+}
+
+inline unsigned grid_for(uint64_t work, int num_sms, int per_sm = 8) {
+    uint64_t b = (work + kThreads - 1) / kThreads;
+    const uint64_t cap = (uint64_t)num_sms * per_sm;
+    if (b > cap) b = cap;
+    if (b == 0) b = 1;
+    return (unsigned)b;
+}
+
+}  // namespace
+
+int run_reduction(ReduceState& st, cudaStream_t s, int num_sms, uint32_t& epoch,
+                  ReduceStats* stats) {
+    (void)epoch;
+    ReduceStats local;
+    ReduceStats& S = stats ? *stats : local;
+    const uint32_t n = st.n;
+    if (n < 2 || st.k == 0) {
+        cudaMemsetAsync(st.counters, 0, sizeof(uint32_t) * 8, s);
+        return 0;
+    }
+    uint32_t* par = st.best + n;  // best buffer holds [best | par]
+    const unsigned gn = grid_for(n, num_sms, 4);
+    cudaMemsetAsync(st.counters, 0, sizeof(uint32_t) * 8, s);
+    k4_init<<<gn, kThreads, 0, s>>>(st.comp, st.best, par, n);
+    S.launches += 1;
+
+    uint32_t* h = st.host_counters;
+    auto pull = [&]() {
+        cudaMemcpyAsync(h, st.counters, sizeof(uint32_t) * 8, cudaMemcpyDeviceToHost, s);
+        cudaStreamSynchronize(s);
+    };
+
+    uint64_t pos = 0;
+    uint64_t window = std::min<uint64_t>(st.k, std::max<uint64_t>(8ull * n, 1u << 16));
+    uint32_t survivors = 0;
+    while (survivors < n - 1 && pos < st.k) {
+        uint64_t end = std::min<uint64_t>(st.k, pos + window);
+        // (i) clearing filter over the window
+        cudaMemsetAsync(st.counters + kCntCand, 0, sizeof(uint32_t), s);
+        cudaMemsetAsync(st.counters + kCntOverflow, 0, sizeof(uint32_t), s);
+        k4_filter<<<grid_for(end - pos, num_sms), kThreads, 0, s>>>(
+            st.uv, pos, end, nullptr, 0, st.comp, st.cand[0], st.cap, st.counters);
+        S.launches += 1;
+        pull();
+        if (h[kCntOverflow]) {  // too many live columns in this window: shrink and retry
+            window = std::max<uint64_t>(window / 4, 1024);
+            continue;
+        }
+        S.rounds += 1;
+        S.scanned += end - pos;
+        uint32_t ncand = h[kCntCand];
+        int cur = 0;
+        // (ii) parallel resolution rounds
+        while (ncand > 0) {
+            S.iterations += 1;
+            k4_min_edge<<<grid_for(ncand, num_sms), kThreads, 0, s>>>(st.cand[cur], ncand, st.uv,
+                                                                       st.comp, st.best);
+            cudaMemsetAsync(st.counters + kCntHooks, 0, sizeof(uint32_t), s);
+            k4_hook<<<gn, kThreads, 0, s>>>(n, st.uv, st.comp, st.best, par, st.surv,
+                                            st.counters);
+            k4_jump_roots<<<gn, kThreads, 0, s>>>(n, st.comp, par);
+            k4_relabel<<<gn, kThreads, 0, s>>>(n, st.comp, par, st.best);
+            cudaMemsetAsync(st.counters + kCntCand, 0, sizeof(uint32_t), s);
+            k4_filter<<<grid_for(ncand, num_sms), kThreads, 0, s>>>(
+                st.uv, 0, 0, st.cand[cur], ncand, st.comp, st.cand[cur ^ 1], st.cap,
+                st.counters);
+            S.launches += 5;
+            pull();
+            cur ^= 1;
+            ncand = h[kCntCand];
+            survivors = h[kCntSurv];
+        }
+        survivors = h[kCntSurv];
+        pos = end;
+        window = std::min<uint64_t>(window * 2, 1ull << 40);
+    }
+    S.survivors = survivors;
+    return 0;
+}
+
+}  // namespace ph0b

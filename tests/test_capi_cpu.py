@@ -1,0 +1,66 @@
+"""CPU: the C-ABI library loads, exports every symbol include/ph0b.h declares, and its
+host-side validation reproduces the reference's error behaviour (no GPU needed)."""
+import re
+
+import numpy as np
+import pytest
+
+import oracle_bridge as ob
+import paper_2203_02527_b200 as pkg
+from paper_2203_02527_b200 import ph0b
+
+HEADER = ob.ROOT / "include" / "ph0b.h"
+
+
+def declared_functions():
+    text = HEADER.read_text()
+    text = re.sub(r"/\*.*?\*/", "", text, flags=re.S)
+    return sorted(set(re.findall(r"\b(ph0b_[a-z0-9_]+)\s*\(", text)))
+
+
+def test_header_symbols_exported():
+    lib = pkg.lib()
+    names = declared_functions()
+    assert len(names) >= 15
+    for name in names:
+        assert hasattr(lib, name), name
+    assert set(names) == set(ph0b.EXPORTED_SYMBOLS)
+
+
+def test_abi_version():
+    assert pkg.lib().ph0b_abi_version() == 1
+
+
+def test_nonfinite_rejected_with_reference_message():  # point_cloud.cpp:15-18
+    X = np.array([[1.0, np.inf], [0.0, 0.0]])
+    with pytest.raises(ValueError, match="point cloud contains non-finite coordinates"):
+        pkg.h0_barcode(X)
+    X = np.array([[1.0, np.nan], [0.0, 0.0]])
+    with pytest.raises(ValueError, match="non-finite"):
+        pkg.pairwise_distances(X)
+
+
+def test_workers_zero_rejected():  # reduction.cpp:134
+    with pytest.raises(ValueError, match="worker count must be at least 1"):
+        pkg.h0_barcode(np.zeros((3, 2)), workers=0)
+
+
+def test_too_large_rejected():
+    X = np.zeros((65537, 1))
+    with pytest.raises(pkg.Ph0bError, match="too large"):
+        pkg.h0_barcode(X)
+
+
+def test_generate_uniform_cloud_matches_reference_generator():  # point_cloud.cpp:20-29
+    for n, d, seed in ((1, 2, 42), (17, 3, 9), (100, 1, 123)):
+        assert np.array_equal(pkg.generate_cloud(0, n, d, seed), ob.uniform_cloud(n, d, seed))
+    X = pkg.config_cloud("C4", 1)
+    assert X.shape == (1, 3)
+
+
+def test_config_clouds_deterministic():
+    for name in ("C1", "C2"):
+        a, b = pkg.config_cloud(name), pkg.config_cloud(name)
+        assert np.array_equal(a, b) and np.isfinite(a).all()
+    C5 = pkg.config_cloud("C5", 1000)
+    assert C5.shape == (1000, 8)
