@@ -1,0 +1,326 @@
+#!/usr/bin/env python
+"""Benchmark of the B200 H0 barcode pipeline (BASELINE.json metric: edges/s = K / wall).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--config C5] [--impl ours|reference]
+
+A step is one full pass of the hot path (pairwise distances -> sort -> unique/D -> boundary
+matrix -> column reduction -> barcode collect) over the workload's K = N(N-1)/2 edges.
+* value: device time with the cloud already resident in HBM and outputs left in HBM
+  (CUDA events on the pipeline stream, barrier + synchronize around the timed region,
+  max over ranks).  Inputs (keys/values: 25.8 GB at C5) are far larger than L2.
+* e2e:   the same metric through the public C ABI (ph0b_run_host) with host buffers: the
+  H2D copy of X from pinned memory and the D2H copy of the bars and of D (|D| doubles)
+  into pinned memory are inside the timed region.
+* --impl reference: the reference's own CPU implementation (oracle/_ref, the unmodified
+  /root/reference sources built here; else the C port in oracle/) on a bounded sample
+  of the same workload, rank 0 only.
+Prints ONE JSON line on rank 0.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+from pathlib import Path
+
+ROOT = Path(__file__).resolve().parent
+sys.path.insert(0, str(ROOT))
+
+METRIC = "end-to-end H0 barcode time (s) and edges/s vs N at 1/2/4/8 B200 vs CPU ref"
+UNIT = "edges/s"
+WORKLOADS = {
+    "C1": "N=500 d=2 two Gaussian clusters",
+    "C2": "N=2000 d=3 noisy circle + uniform background",
+    "C3": "N=8192 d=16 mixture of 10 Gaussians",
+    "C4": "N=32768 d=3 uniform cube (generate_uniform_cloud seed 4)",
+    "C5": "N=65536 d=8 mixture of 32 Gaussians",
+}
+REF_SAMPLE_N = 2048      # reference arm: first 2048 points of the workload cloud per step
+CPU_BASELINE_N = 3000    # cpu_baseline leg of our arm (~10 s of single-core work)
+
+
+def peaks():
+    p = ROOT / "MEASURED_PEAKS.json"
+    if p.exists():
+        j = json.loads(p.read_text())
+        return float(j.get("hbm_gbs", 6650.0)), "measured"
+    return 6650.0, "fallback"
+
+
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons sampled every 200 ms during the timed region."""
+
+    FIELDS = ("clocks.sm,clocks.max.sm,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.index = index
+        self.rows = []
+        self._stop = threading.Event()
+        self._t = None
+
+    def __enter__(self):
+        def run():
+            while not self._stop.is_set():
+                try:
+                    out = subprocess.run(
+                        ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.FIELDS}",
+                         "--format=csv,noheader,nounits"], capture_output=True, text=True,
+                        timeout=5).stdout.strip()
+                    if out:
+                        self.rows.append([x.strip() for x in out.split(",")])
+                except Exception:
+                    pass
+                self._stop.wait(0.2)
+
+        self._t = threading.Thread(target=run, daemon=True)
+        self._t.start()
+        return self
+
+    def __exit__(self, *a):
+        self._stop.set()
+        self._t.join(timeout=6)
+
+    def summary(self):
+        if not self.rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
+        sm = [float(r[0]) for r in self.rows if r[0].replace(".", "").isdigit()]
+        mx = [float(r[1]) for r in self.rows if r[1].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for r in self.rows for i in range(4)
+                          if len(r) > 3 + i and r[3 + i].lower() == "active"})
+        return {"sm_mhz": statistics.median(sm) if sm else None,
+                "sm_max_mhz": max(mx) if mx else None, "reasons": reasons,
+                "samples": len(self.rows)}
+
+
+def dist_env():
+    ws = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return ws, rank, local
+
+
+def cpu_reference_sample(X, n_sample: int):
+    """Run the reference's full CPU path on the first n_sample points; returns (seconds, K,
+    kind)."""
+    sys.path.insert(0, str(ROOT / "tests"))
+    import oracle_bridge as ob  # CPU checker / baseline only
+
+    Xs = X[:n_sample]
+    k = n_sample * (n_sample - 1) // 2
+    t0 = time.perf_counter()
+    if ob.ref_available():
+        ob.ref_h0(Xs, mode=0, want_scale=True)
+        kind = "reference"
+    else:
+        ob.oracle_filtration_and_bars(Xs, reduction_limit=1 << 30)
+        kind = "port"
+    return time.perf_counter() - t0, k, kind
+
+
+def run_reference_arm(args, cfg_name):
+    ws, rank, _ = dist_env()
+    if rank != 0:
+        return
+    import numpy as np  # noqa: F401
+
+    import paper_2203_02527_b200 as pkg  # host-side cloud generator only
+
+    X = pkg.config_cloud(cfg_name)
+    n = X.shape[0]
+    ns = min(REF_SAMPLE_N, n)
+    for _ in range(args.warmup):
+        cpu_reference_sample(X, ns)
+    secs = []
+    kind = "reference"
+    k = ns * (ns - 1) // 2
+    for _ in range(args.steps):
+        s, k, kind = cpu_reference_sample(X, ns)
+        secs.append(s)
+    total = sum(secs)
+    value = k * len(secs) / total
+    line = {
+        "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": ws,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * total / len(secs),
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic",
+        "config": {"workload": f"{cfg_name}: {WORKLOADS[cfg_name]}", "n": n, "d": X.shape[1],
+                   "sample": f"first {ns} points of the workload cloud per step",
+                   "parallelism": "cpu, 1 thread (reference path is single-threaded)"},
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": 1, "kind": kind,
+                         "sample": f"full reference path (pairwise_distances..extract_barcode) "
+                                   f"on the first {ns} points of {cfg_name}"},
+        "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+def load_traffic():
+    p = ROOT / "profiles" / "ncu_summary.json"
+    if p.exists():
+        try:
+            return json.loads(p.read_text())
+        except Exception:
+            return None
+    return None
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--config", default="C5", choices=sorted(WORKLOADS))
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--e2e-steps", type=int, default=None)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    args.warmup = max(args.warmup, 3)
+    cfg_name = args.config
+
+    if args.impl == "reference":
+        run_reference_arm(args, cfg_name)
+        return
+
+    import numpy as np
+    import torch
+
+    import paper_2203_02527_b200 as pkg
+
+    ws, rank, local = dist_env()
+    dist = None
+    if ws > 1:
+        import torch.distributed as dist
+        torch.cuda.set_device(local)
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    device = local if ws > 1 else 0
+    torch.cuda.set_device(device)
+
+    X = pkg.config_cloud(cfg_name)
+    n, d = X.shape
+    k = n * (n - 1) // 2
+    ctx = pkg.Context(device)
+    ctx.reserve(n, d)
+    stream = torch.cuda.Stream(device=device)
+    xdev = torch.from_numpy(np.asfortranarray(X).ravel(order="F").copy()).to(f"cuda:{device}")
+
+    def barrier():
+        torch.cuda.synchronize(device)
+        if dist is not None:
+            dist.barrier()
+
+    # ---- device-resident timing (value) ------------------------------------------------------
+    for _ in range(args.warmup):
+        ctx.run_device(xdev.data_ptr(), n, d, stream=stream.cuda_stream)
+    barrier()
+    launches = 0
+    stage_sums = {}
+    start, end = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with ClockSampler(device) as clk:
+        start.record(stream)
+        for _ in range(args.steps):
+            r = ctx.run_device(xdev.data_ptr(), n, d, stream=stream.cuda_stream)
+            launches += pkg.last_launch_count()
+            for f, _t in r.times._fields_:
+                stage_sums[f] = stage_sums.get(f, 0) + getattr(r.times, f)
+        end.record(stream)
+        barrier()
+    ms = start.elapsed_time(end)
+    ms_max = ms
+    if dist is not None:
+        t = torch.tensor([ms], device=f"cuda:{device}")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms_max = float(t.item())
+    value = ws * k * args.steps / (ms_max / 1e3)
+    n_scale = int(r.n_scale)
+    n_finite = int(r.n_finite)
+
+    # ---- end-to-end through the C ABI with host buffers (e2e) --------------------------------
+    e2e_steps = args.e2e_steps or max(1, min(args.steps, 5))
+    xin = pkg.PinnedArray(n * d)
+    xin.array[:] = np.asfortranarray(X).ravel(order="F")
+    Xh = xin.array.reshape(d, n).T  # (n, d) view of column-major pinned storage
+    dg = pkg.PinnedArray(n, np.uint64)
+    dl = pkg.PinnedArray(n, np.float64)
+    sc = pkg.PinnedArray(n_scale, np.float64)
+
+    def run_e2e():
+        return ctx.run_host(Xh, dg.array, dl.array, sc.array, stream=stream.cuda_stream)
+
+    run_e2e()
+    barrier()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    for _ in range(e2e_steps):
+        nf, ess, ns_, _t = run_e2e()
+    e1.record(stream)
+    barrier()
+    e2e_ms = e0.elapsed_time(e1)
+    if dist is not None:
+        t = torch.tensor([e2e_ms], device=f"cuda:{device}")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        e2e_ms = float(t.item())
+    e2e_value = ws * k * e2e_steps / (e2e_ms / 1e3)
+    h2d = n * d * 8
+    d2h = ns_ * 8 + nf * 16
+    for a in (xin, dg, dl, sc):
+        a.free()
+
+    # ---- roofline of the dominant kernel (onesweep digit pass) ------------------------------
+    peak, peak_kind = peaks()
+    passes = max(1, int(stage_sums.get("sort_passes", 0) / args.steps))
+    sort_ms = stage_sums.get("sort_ms", 0.0) / args.steps
+    pass_ms = sort_ms / passes
+    alg_bytes = 24 * k  # read key+value (12 B), write key+value (12 B) per edge per pass
+    achieved = alg_bytes / (pass_ms / 1e3) / 1e9
+    traffic = None
+    summ = load_traffic()
+    if summ and summ.get("config") == cfg_name:
+        traffic = summ.get("onesweep_dram_bytes_per_launch")
+    roofline = {"kernel": "k2_onesweep (LSD digit pass)", "bound": "hbm",
+                "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s",
+                "frac": round(achieved / peak, 4), "traffic": traffic,
+                "peak_source": f"{peak_kind} (MEASURED_PEAKS.json hbm_gbs)",
+                "alg_bytes_per_launch": alg_bytes, "avg_launch_ms": round(pass_ms, 4),
+                "passes": passes}
+
+    cpu = None
+    if rank == 0 and not args.no_cpu_baseline:
+        s, kk, kind = cpu_reference_sample(X, min(CPU_BASELINE_N, n))
+        cpu = {"value": kk / s, "unit": UNIT, "cores": 1, "kind": kind,
+               "sample": f"full reference path on the first {min(CPU_BASELINE_N, n)} points of "
+                         f"{cfg_name} ({kk} edges, {s:.1f} s)"}
+
+    if rank == 0:
+        stage_ms = {f: round(stage_sums[f] / args.steps, 3) for f in
+                    ("distance_ms", "sort_ms", "unique_ms", "reduce_ms", "collect_ms", "total_ms")}
+        line = {
+            "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": ws, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": ms_max / args.steps, "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": {"workload": f"{cfg_name}: {WORKLOADS[cfg_name]}", "n": n, "d": d,
+                       "edges": k, "parallelism": "replicas" if ws > 1 else "single",
+                       "l2": "inputs larger than L2 (keys+values 12 B/edge)",
+                       "n_scale": n_scale, "bars": n_finite},
+            "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": h2d,
+                    "d2h_bytes_per_step": d2h, "ms_per_step": e2e_ms / e2e_steps,
+                    "steps": e2e_steps, "api": "ph0b_run_host (pinned host X, D, bars)"},
+            "roofline": roofline, "cpu_baseline": cpu, "clocks": clk.summary(),
+            "gpu_launches": launches, "stage_ms": stage_ms,
+            "sort_passes": passes,
+        }
+        print(json.dumps(line), flush=True)
+    ctx.close()
+    if dist is not None:
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()
