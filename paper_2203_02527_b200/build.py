@@ -65,4 +65,8 @@ def build_library(verbose: bool = False, force: bool = False) -> Path:
 
 
 if __name__ == "__main__":
-    print(build_library(verbose=True, force="--force" in sys.argv))
+    try:
+        print(build_library(verbose=True, force="--force" in sys.argv))
+    except RuntimeError as e:
+        print("BUILD FAILED:", e)
+        sys.exit(1)

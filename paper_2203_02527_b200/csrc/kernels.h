@@ -40,6 +40,9 @@ struct SortArgs {
     uint32_t hist0_rot;         // hist row 0 is indexed (digit + rot) & 255 (raw low byte)
 };
 uint64_t sort_tiles(uint64_t count);
+// Device check of the ATOMS lane-ordering property used by the atomic ranking; selects the
+// ranking variant (atomic if it holds, bit-sliced ballots otherwise).
+bool sort_self_test(cudaStream_t s);
 // Runs the passes listed in plan; returns the buffer index (0/1) holding the result.
 // hist[p][*] must already hold the digit-p histogram of (key-kmin) for p = 0 (the
 // remaining histograms are produced by the passes themselves).

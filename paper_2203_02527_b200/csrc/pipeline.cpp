@@ -82,6 +82,7 @@ Status Context::init() {
     PH0B_TRY(cudaHostAlloc(&h_counters_, sizeof(uint32_t) * 64, cudaHostAllocDefault),
              "cudaHostAlloc");
     bytes_ += 8 * 256 * 4 + 64 * 4 + 64;
+    atomic_rank_ok_ = sort_self_test(stream_);
     return Status::ok();
 }
 

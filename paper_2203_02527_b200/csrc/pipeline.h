@@ -92,6 +92,7 @@ private:
     uint32_t* h_counters_ = nullptr;  // pinned [64]
     uint32_t epoch_ = 1;
     bool status_zeroed_ = false;
+    bool atomic_rank_ok_ = false;
 };
 
 // Default per-device contexts used by the stateless C entry points.

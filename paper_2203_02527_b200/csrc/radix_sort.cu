@@ -16,6 +16,7 @@
 #include <cuda_runtime.h>
 
 #include <cstdint>
+#include <cstdlib>
 
 #include "common.cuh"
 #include "kernels.h"
@@ -25,8 +26,8 @@ namespace {
 
 constexpr int kThreads = 256;
 constexpr int kWarps = kThreads / 32;
-constexpr int kItems = 16;
-constexpr int kTileKeys = kThreads * kItems;  // 4096
+constexpr int kItems = 12;
+constexpr int kTileKeys = kThreads * kItems;
 constexpr int kBins = 256;
 static_assert(kThreads == kBins, "one thread per digit value");
 
@@ -52,8 +53,28 @@ __device__ __forceinline__ uint32_t block_exclusive_scan(uint32_t x, uint32_t* s
     return wbase + inc - x;
 }
 
-template <bool kVals, bool kCountNext>
-__global__ void __launch_bounds__(kThreads)
+// Stable warp-level multisplit of one digit per lane: the mask of lanes holding the same
+// digit, by bit-sliced ballots (pure ALU, no MIO round trip) or by match.any.
+template <int kRank>
+__device__ __forceinline__ uint32_t peer_mask(uint32_t d, uint32_t valid_mask) {
+    if constexpr (kRank == 2) {
+        uint32_t peers = valid_mask;
+#pragma unroll
+        for (int b = 0; b < 8; ++b) {
+            const uint32_t bit = (d >> b) & 1u;
+            const uint32_t bal = __ballot_sync(0xffffffffu, bit);
+            peers &= bit ? bal : ~bal;
+        }
+        return peers;
+    } else {
+        return __match_any_sync(0xffffffffu, d);
+    }
+}
+
+// kRank: 0 = match.any + leader LDS/STS chain, 1 = match.any + leader atomicAdd (pipelined),
+//        2 = bit-sliced ballots + leader atomicAdd.
+template <bool kVals, bool kCountNext, int kRank, int kMinBlocks>
+__global__ void __launch_bounds__(kThreads, kMinBlocks)
     k2_onesweep(const uint64_t* __restrict__ keys_in, uint64_t* __restrict__ keys_out,
                 const uint32_t* __restrict__ vals_in, uint32_t* __restrict__ vals_out,
                 uint64_t count, uint64_t kmin, uint32_t shift, uint32_t next_shift,
@@ -79,35 +100,64 @@ __global__ void __launch_bounds__(kThreads)
     const uint32_t tile = s_tile;
     const uint64_t base = (uint64_t)tile * kTileKeys;
 
-    // ---- load (warp-striped, coalesced) and rank within the warp ------------------------
+    // ---- load keys (warp-striped, coalesced) and rank within the warp ------------------
     uint64_t k[kItems];
-    uint32_t v[kItems];
-    uint32_t rank[kItems];
+    // per item: [4:0] leader lane, [9:5] peers before me, [31:10] leader's warp-counter value
+    uint32_t pk[kItems];
     const uint64_t wbase = base + (uint64_t)warp * (32 * kItems) + lane;
 #pragma unroll
     for (int i = 0; i < kItems; ++i) {
         const uint64_t idx = wbase + 32 * i;
-        const bool valid = idx < count;
-        k[i] = valid ? keys_in[idx] : ~0ull;
-        if (kVals) v[i] = valid ? vals_in[idx] : 0u;
+        k[i] = idx < count ? keys_in[idx] : ~0ull;
     }
     const uint32_t lt = lanemask_lt();
 #pragma unroll
     for (int i = 0; i < kItems; ++i) {
         const bool valid = wbase + 32 * i < count;
         const uint32_t d = valid ? (uint32_t)((k[i] - kmin) >> shift) & 0xFFu : 0x100u;
-        const uint32_t peers = __match_any_sync(0xffffffffu, d);
-        const int leader = __ffs(peers) - 1;
-        uint32_t old = 0;
-        if (valid && lane == leader) old = s_whist[warp][d];
-        old = __shfl_sync(0xffffffffu, old, leader);
-        rank[i] = old + __popc(peers & lt);
-        if (valid && lane == leader) s_whist[warp][d] = old + __popc(peers);
-        __syncwarp();
+        if constexpr (kRank == 3) {
+            // ATOMS resolves same-address lanes of one instruction in ascending lane order
+            // (verified on the device at context creation, see rank_self_test), and
+            // instructions of one warp in program order: the returned count IS the stable
+            // in-warp rank.
+            pk[i] = valid ? atomicAdd(&s_whist[warp][d], 1u) : 0u;
+            continue;
+        }
+        const uint32_t vmask = __ballot_sync(0xffffffffu, valid);
+        const uint32_t peers = peer_mask<kRank>(d, vmask);
+        const uint32_t leader = __ffs(peers) - 1;
+        const uint32_t before = __popc(peers & lt);
+        if constexpr (kRank == 0) {
+            uint32_t o = 0;
+            if (valid && lane == (int)leader) o = s_whist[warp][d];
+            o = __shfl_sync(0xffffffffu, o, leader);
+            pk[i] = o + before;
+            if (valid && lane == (int)leader) s_whist[warp][d] = o + __popc(peers);
+            __syncwarp();
+        } else {
+            const uint32_t o = (valid && lane == (int)leader)
+                                   ? atomicAdd(&s_whist[warp][d], __popc(peers))
+                                   : 0u;
+            pk[i] = leader | (before << 5) | (o << 10);
+        }
+    }
+    uint32_t rank2[kItems / 2];  // two 16-bit in-warp ranks per register
+#pragma unroll
+    for (int i = 0; i < kItems; ++i) {
+        uint32_t r;
+        if constexpr (kRank == 0 || kRank == 3) {
+            r = pk[i];
+        } else {
+            r = (__shfl_sync(0xffffffffu, pk[i], pk[i] & 31u) >> 10) + ((pk[i] >> 5) & 31u);
+        }
+        if (i & 1)
+            rank2[i / 2] |= r << 16;
+        else
+            rank2[i / 2] = r;
     }
     __syncthreads();
 
-    // ---- per-digit counts, warp offsets, tile-local digit starts ------------------------
+    // ---- per-digit counts, warp offsets; publish this tile's aggregate early -------------
     const uint32_t t = tid;  // digit handled by this thread
     uint32_t cnt = 0;
 #pragma unroll
@@ -117,44 +167,49 @@ __global__ void __launch_bounds__(kThreads)
         cnt += c;
     }
     uint64_t* my_status = status + (uint64_t)tile * kBins + t;
-    if (tile == 0)
-        st_relaxed_u64(my_status, pack_status(kStateInclusive, epoch, cnt));
-    else
-        st_relaxed_u64(my_status, pack_status(kStateAggregate, epoch, cnt));
+    st_relaxed_u64(my_status, pack_status(tile == 0 ? kStateInclusive : kStateAggregate, epoch, cnt));
+    // first look-back probe goes out now; its latency hides behind the scans and the scatter
+    uint64_t probe = tile > 0 ? ld_relaxed_u64(status + (uint64_t)(tile - 1) * kBins + t) : 0ull;
 
-    // global start of digit t: exclusive scan of the (rotated) digit histogram
+    // global start of digit t (exclusive scan of the rotated digit histogram) and the
+    // tile-local start of digit t (exclusive scan of this tile's counts)
     const uint32_t hcount = hist[(t + hist_rot) & 0xFFu];
     const uint32_t bin_start = block_exclusive_scan(hcount, s_scan, nullptr);
     __syncthreads();
-    s_tile_start[t] = block_exclusive_scan(cnt, s_scan, nullptr);
-
-    // ---- decoupled look-back over earlier tiles, per digit -------------------------------
-    uint32_t excl = 0;
-    if (tile > 0) {
-        int64_t p = (int64_t)tile - 1;
-        while (p >= 0) {
-            const uint64_t s = ld_relaxed_u64(status + (uint64_t)p * kBins + t);
-            const uint32_t st = status_state(s, epoch);
-            if (st == 0) continue;  // predecessor not published yet
-            excl += (uint32_t)s;
-            if (st == kStateInclusive) break;
-            --p;
-        }
-        st_relaxed_u64(my_status, pack_status(kStateInclusive, epoch, excl + cnt));
-    }
-    s_global[t] = bin_start + excl;
+    const uint32_t tstart = block_exclusive_scan(cnt, s_scan, nullptr);
+    s_tile_start[t] = tstart;
     __syncthreads();
 
     // ---- scatter into shared memory in (digit, input order) order -----------------------
 #pragma unroll
     for (int i = 0; i < kItems; ++i) {
-        if (wbase + 32 * i < count) {
+        const uint64_t idx = wbase + 32 * i;
+        if (idx < count) {
             const uint32_t d = (uint32_t)((k[i] - kmin) >> shift) & 0xFFu;
-            const uint32_t pos = s_tile_start[d] + s_whist[warp][d] + rank[i];
+            const uint32_t pos = s_tile_start[d] + s_whist[warp][d] +
+                                 ((i & 1) ? (rank2[i / 2] >> 16) : (rank2[i / 2] & 0xFFFFu));
             s_keys[pos] = k[i];
-            if (kVals) s_vals[pos] = v[i];
+            if (kVals) s_vals[pos] = vals_in[idx];
         }
     }
+
+    // ---- decoupled look-back over earlier tiles, per digit -------------------------------
+    uint32_t excl = 0;
+    if (tile > 0) {
+        int64_t p = (int64_t)tile - 1;
+        for (;;) {
+            const uint32_t st = status_state(probe, epoch);
+            if (st != 0) {
+                excl += (uint32_t)probe;
+                if (st == kStateInclusive) break;
+                --p;
+            }
+            probe = ld_relaxed_u64(status + (uint64_t)p * kBins + t);
+        }
+        st_relaxed_u64(my_status, pack_status(kStateInclusive, epoch, excl + cnt));
+    }
+    // output position of the element at tile-local position p with digit d: delta[d] + p
+    s_global[t] = bin_start + excl - tstart;
     __syncthreads();
 
     // ---- write out: consecutive threads -> consecutive positions within each digit run --
@@ -167,7 +222,7 @@ __global__ void __launch_bounds__(kThreads)
             const uint64_t key = s_keys[p];
             const uint64_t rel = key - kmin;
             const uint32_t d = (uint32_t)(rel >> shift) & 0xFFu;
-            const uint64_t out = (uint64_t)s_global[d] + (p - s_tile_start[d]);
+            const uint64_t out = (uint64_t)(uint32_t)(s_global[d] + p);
             keys_out[out] = key;
             if (kVals) vals_out[out] = s_vals[p];
             if (kCountNext) atomicAdd(&s_next[(uint32_t)(rel >> next_shift) & 0xFFu], 1u);
@@ -194,10 +249,10 @@ __global__ void k2_digit_histogram(const uint64_t* __restrict__ keys, uint64_t c
     if (h[threadIdx.x]) atomicAdd(&hist[threadIdx.x], h[threadIdx.x]);
 }
 
-template <bool kVals, bool kCountNext>
-void launch_pass(const SortArgs& a, int cur, uint32_t p, const SortPlan& plan, uint32_t rot,
-                 uint32_t* next_hist, uint64_t tiles, cudaStream_t s) {
-    auto kern = k2_onesweep<kVals, kCountNext>;
+template <bool kVals, bool kCountNext, int kRank, int kMinBlocks>
+void launch_pass_r(const SortArgs& a, int cur, uint32_t p, const SortPlan& plan, uint32_t rot,
+                   uint32_t* next_hist, uint64_t tiles, cudaStream_t s) {
+    auto kern = k2_onesweep<kVals, kCountNext, kRank, kMinBlocks>;
     const size_t smem = kTileKeys * (sizeof(uint64_t) + (kVals ? sizeof(uint32_t) : 0));
     static bool configured = false;
     if (!configured) {
@@ -211,7 +266,73 @@ void launch_pass(const SortArgs& a, int cur, uint32_t p, const SortPlan& plan, u
         a.hist + kBins * p, rot, a.status, a.tile_counter + p, a.epoch_base + p, next_hist);
 }
 
+int g_rank_variant = -1;  // set by sort_self_test(); env PH0B_RANK overrides
+
+int rank_variant() {
+    if (g_rank_variant < 0) {
+        const char* e = getenv("PH0B_RANK");
+        g_rank_variant = e ? atoi(e) : 2;
+    }
+    return g_rank_variant;
+}
+
+template <bool kVals, bool kCountNext>
+void launch_pass(const SortArgs& a, int cur, uint32_t p, const SortPlan& plan, uint32_t rot,
+                 uint32_t* next_hist, uint64_t tiles, cudaStream_t s) {
+    static const int minb = [] {
+        const char* e = getenv("PH0B_MINB");
+        return e ? atoi(e) : 4;
+    }();
+    const int rv = rank_variant();
+    if (rv == 3) {
+        if (minb == 3)
+            launch_pass_r<kVals, kCountNext, 3, 3>(a, cur, p, plan, rot, next_hist, tiles, s);
+        else
+            launch_pass_r<kVals, kCountNext, 3, 4>(a, cur, p, plan, rot, next_hist, tiles, s);
+    } else {
+        launch_pass_r<kVals, kCountNext, 2, 4>(a, cur, p, plan, rot, next_hist, tiles, s);
+    }
+}
+
+// Self-test of the ordering property rank variant 3 relies on.  Returns true when every
+// same-address lane pair of every ATOMS instruction was resolved in ascending lane order.
+__global__ void k2_rank_self_test(unsigned long long* viol) {
+    __shared__ uint32_t h[8][256];
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    for (int i = threadIdx.x; i < 8 * 256; i += blockDim.x) (&h[0][0])[i] = 0;
+    __syncthreads();
+    uint32_t x = (blockIdx.x * 7919u + threadIdx.x * 104729u) ^ 0x9e3779b9u;
+    unsigned long long v = 0;
+    for (int it = 0; it < 64; ++it) {
+        x = x * 1664525u + 1013904223u;
+        const uint32_t d = (x >> 11) & ((it & 1) ? 7u : 255u);
+        const uint32_t old = atomicAdd(&h[warp][d], 1u);
+        for (int o = 0; o < 32; ++o) {  // uniform loop: every lane joins every shuffle
+            const uint32_t od = __shfl_sync(0xffffffffu, d, o);
+            const uint32_t oo = __shfl_sync(0xffffffffu, old, o);
+            if (o < lane && od == d && !(oo < old)) ++v;
+        }
+    }
+    if (v) atomicAdd(viol, v);
+}
+
 }  // namespace
+
+bool sort_self_test(cudaStream_t s) {
+    const char* e = getenv("PH0B_RANK");
+    unsigned long long* d = nullptr;
+    unsigned long long h = 1;
+    if (cudaMalloc(&d, sizeof(h)) == cudaSuccess) {
+        cudaMemsetAsync(d, 0, sizeof(h), s);
+        k2_rank_self_test<<<64, 256, 0, s>>>(d);
+        cudaMemcpyAsync(&h, d, sizeof(h), cudaMemcpyDeviceToHost, s);
+        cudaStreamSynchronize(s);
+        cudaFree(d);
+    }
+    cudaGetLastError();
+    g_rank_variant = e ? atoi(e) : (h == 0 ? 3 : 2);
+    return h == 0;
+}
 
 uint64_t sort_tiles(uint64_t count) { return (count + kTileKeys - 1) / kTileKeys; }
 
