@@ -20,6 +20,7 @@
 
 #include "common.cuh"
 #include "kernels.h"
+#include "tma.cuh"
 
 namespace ph0b {
 namespace {
@@ -29,48 +30,6 @@ constexpr int kThreads = 256;   // 8 warps
 constexpr int kWarps = kThreads / 32;
 constexpr int kRV = kTile / 32; // v columns per lane
 constexpr int kMaxTmaDim = 32;  // TMA/smem path for d <= 32
-
-__device__ __forceinline__ uint32_t smem_u32(const void* p) {
-    return static_cast<uint32_t>(__cvta_generic_to_shared(p));
-}
-__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
-    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count));
-}
-__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
-    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)),
-                 "r"(bytes)
-                 : "memory");
-}
-__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
-    asm volatile(
-        "{\n\t.reg .pred p;\n"
-        "WAIT_%=:\n\t"
-        "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
-        "@!p bra WAIT_%=;\n}" ::"r"(smem_u32(bar)),
-        "r"(parity)
-        : "memory");
-}
-__device__ __forceinline__ void tma_load_2d(void* dst, const CUtensorMap* map, uint64_t* bar,
-                                            int c0, int c1) {
-    asm volatile(
-        "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes"
-        " [%0], [%1, {%3, %4}], [%2];" ::"r"(smem_u32(dst)),
-        "l"(reinterpret_cast<uint64_t>(map)), "r"(smem_u32(bar)), "r"(c0), "r"(c1)
-        : "memory");
-}
-
-// Tile t of the row-major upper triangle of an nb x nb tile grid -> (bu, bv), bu <= bv.
-__device__ __forceinline__ void tile_coords(uint32_t t, uint32_t nb, uint32_t& bu, uint32_t& bv) {
-    // rowstart(b) = b*nb - b*(b-1)/2
-    const double B = 2.0 * nb + 1.0;
-    int b = (int)((B - sqrt(B * B - 8.0 * (double)t)) * 0.5);
-    if (b < 0) b = 0;
-    auto rs = [nb](int x) { return (int64_t)x * nb - (int64_t)x * (x - 1) / 2; };
-    while (b > 0 && rs(b) > (int64_t)t) --b;
-    while (rs(b + 1) <= (int64_t)t) ++b;
-    bu = (uint32_t)b;
-    bv = (uint32_t)(b + ((int64_t)t - rs(b)));
-}
 
 // One CTA-tile of edges. XS: source of coordinates, laid out [k][stride] with the tile's
 // first point at offset 0 (smem tile or global pointer).
@@ -275,12 +234,14 @@ __global__ void k0_pack_points(const double* __restrict__ x, uint32_t layout, ui
     }
 }
 
+}  // namespace
+
 using EncodeTiledFn = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*,
                                    const cuuint64_t*, const cuuint64_t*, const cuuint32_t*,
                                    const cuuint32_t*, CUtensorMapInterleave, CUtensorMapSwizzle,
                                    CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
 
-EncodeTiledFn get_encode_fn() {
+static EncodeTiledFn get_encode_fn() {
     static EncodeTiledFn fn = nullptr;
     if (!fn) {
         void* p = nullptr;
@@ -292,6 +253,21 @@ EncodeTiledFn get_encode_fn() {
     }
     return fn;
 }
+
+bool make_point_tmap(const double* xpad, uint64_t ldx, uint32_t d, CUtensorMap* map) {
+    if (d < 1 || d > 256) return false;
+    EncodeTiledFn enc = get_encode_fn();
+    if (!enc) return false;
+    const cuuint64_t dims[2] = {ldx, d};
+    const cuuint64_t strides[1] = {ldx * sizeof(double)};
+    const cuuint32_t box[2] = {128u, d};
+    const cuuint32_t estr[2] = {1, 1};
+    return enc(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 2, const_cast<double*>(xpad), dims, strides,
+               box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+               CU_TENSOR_MAP_L2_PROMOTION_NONE, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
+namespace {
 
 template <int D>
 int launch_tma(const DistanceArgs& a, const CUtensorMap& map, uint32_t nb, uint32_t total,
@@ -326,30 +302,16 @@ int launch_distance(const DistanceArgs& a, cudaStream_t s, int num_sms) {
     if (a.n < 2) return 0;
     const uint32_t nb = (a.n + kTile - 1) / kTile;
     const uint32_t total = nb * (nb + 1) / 2;
-    if (a.d >= 1 && a.d <= (uint32_t)kMaxTmaDim) {
-        EncodeTiledFn enc = get_encode_fn();
-        if (enc) {
-            CUtensorMap map;
-            const cuuint64_t dims[2] = {a.ldx, a.d};
-            const cuuint64_t strides[1] = {a.ldx * sizeof(double)};
-            const cuuint32_t box[2] = {(cuuint32_t)kTile, a.d};
-            const cuuint32_t estr[2] = {1, 1};
-            const CUresult r = enc(&map, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 2,
-                                   const_cast<double*>(a.xpad), dims, strides, box, estr,
-                                   CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
-                                   CU_TENSOR_MAP_L2_PROMOTION_NONE,
-                                   CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
-            if (r == CUDA_SUCCESS) {
-                switch (a.d) {
-                    case 1: return launch_tma<1>(a, map, nb, total, s, num_sms);
-                    case 2: return launch_tma<2>(a, map, nb, total, s, num_sms);
-                    case 3: return launch_tma<3>(a, map, nb, total, s, num_sms);
-                    case 4: return launch_tma<4>(a, map, nb, total, s, num_sms);
-                    case 8: return launch_tma<8>(a, map, nb, total, s, num_sms);
-                    case 16: return launch_tma<16>(a, map, nb, total, s, num_sms);
-                    default: return launch_tma<0>(a, map, nb, total, s, num_sms);
-                }
-            }
+    CUtensorMap map;
+    if (a.d >= 1 && a.d <= (uint32_t)kMaxTmaDim && make_point_tmap(a.xpad, a.ldx, a.d, &map)) {
+        switch (a.d) {
+            case 1: return launch_tma<1>(a, map, nb, total, s, num_sms);
+            case 2: return launch_tma<2>(a, map, nb, total, s, num_sms);
+            case 3: return launch_tma<3>(a, map, nb, total, s, num_sms);
+            case 4: return launch_tma<4>(a, map, nb, total, s, num_sms);
+            case 8: return launch_tma<8>(a, map, nb, total, s, num_sms);
+            case 16: return launch_tma<16>(a, map, nb, total, s, num_sms);
+            default: return launch_tma<0>(a, map, nb, total, s, num_sms);
         }
     }
     uint32_t grid = (uint32_t)num_sms * 4;

@@ -2,6 +2,7 @@
 #pragma once
 
 #include <cstdint>
+#include <cuda.h>
 #include <cuda_runtime.h>
 
 namespace ph0b {
@@ -18,6 +19,9 @@ struct DistanceArgs {
 };
 // Returns number of kernel launches issued (0 on error; check cudaGetLastError).
 int launch_distance(const DistanceArgs& a, cudaStream_t s, int num_sms);
+
+// TMA descriptor of the padded coordinate-major cloud, box {128 points, d coords}.
+bool make_point_tmap(const double* xpad, uint64_t ldx, uint32_t d, CUtensorMap* map);
 
 // Reorders a host-provided cloud into the padded coordinate-major layout.
 int launch_pack_points(const double* x, uint32_t layout, uint32_t n, uint32_t d, double* xpad,
@@ -54,14 +58,18 @@ int launch_digit_histogram(const uint64_t* keys, uint64_t count, uint64_t kmin, 
 
 // ---- K2c/K3: flag-and-scan unique -> D, and boundary matrix grades (unique.cu) ----------
 struct UniqueArgs {
-    const uint64_t* keys;   // sorted raw keys (f64 length bits)
+    uint64_t* keys;         // sorted raw keys (f64 length bits); runs fixed up in place
+    uint32_t* vals;         // columns (u << 16 | v), permuted with the keys
     uint64_t count;
+    uint64_t kmin;
+    uint32_t low_bits;      // keys are sorted by (key - kmin) >> low_bits only (0 = fully)
     double* scale;          // out: D
     uint32_t* grade;        // out (optional): 1-based grade per column
     uint64_t* status;       // look-back status [tiles]
     uint32_t* tile_counter;
     uint64_t* n_scale;      // out: |D| (device)
     uint32_t epoch;
+    uint32_t* redo;         // out: set when a run exceeded the in-place fix-up limit
 };
 int launch_unique(const UniqueArgs& a, cudaStream_t s);
 

@@ -40,6 +40,29 @@ inline uint32_t span_passes(uint64_t span, SortPlan* plan) {
     return plan->passes;
 }
 
+// Radix plan over the top 8*max_passes bits of the key span; returns the number of low
+// bits left unsorted (fixed up per equal-prefix run by the unique kernel).
+inline uint32_t truncated_plan(uint64_t span, uint32_t max_passes, SortPlan* plan) {
+    const uint32_t bits = span ? 64u - (uint32_t)__builtin_clzll(span) : 0u;
+    uint32_t passes = (bits + 7) / 8, low = 0;
+    if (passes > max_passes) {
+        passes = max_passes;
+        low = bits - 8 * passes;
+    }
+    plan->passes = passes;
+    for (uint32_t p = 0; p < passes; ++p) plan->shift[p] = low + 8 * p;
+    return low;
+}
+
+uint32_t max_sort_passes() {
+    static const uint32_t v = [] {
+        const char* e = getenv("PH0B_MAX_PASSES");
+        const int x = e ? atoi(e) : 5;
+        return (uint32_t)(x < 1 ? 1 : (x > 8 ? 8 : x));
+    }();
+    return v;
+}
+
 }  // namespace
 
 Context::Context(int device) : device_(device) {}
@@ -209,38 +232,64 @@ Status Context::run(const double* dX, uint64_t n, uint64_t d, uint32_t layout,
         return Status::ok();
     }
 
-    // ---- K2: onesweep radix sort -----------------------------------------------------------
-    SortPlan plan{};
-    span_passes(kmax - kmin, &plan);
-    SortArgs sa{};
-    sa.count = k;
-    sa.kmin = kmin;
-    sa.keys[0] = keys_[0];
-    sa.keys[1] = keys_[1];
-    sa.vals[0] = vals_[0];
-    sa.vals[1] = vals_[1];
-    sa.status = status_;
-    sa.hist = hist_;
-    sa.tile_counter = counters_ + 32;
-    sa.epoch_base = next_epochs(plan.passes + 1, st);
-    sa.hist0_rot = (uint32_t)(kmin & 0xFFu);
-    int sl = 0;
-    const int cur = launch_sort_passes(sa, plan, st, num_sms_, &sl);
-    launches += sl;
-    PH0B_CHECK_LAUNCH("radix sort");
-    PH0B_TRY(cudaEventRecord(ev_[2], st), "event");
-    r.times.sort_passes = plan.passes;
-
-    // ---- K2c/K3: unique -> D (into the free key buffer), grades ---------------------------
-    double* scale = reinterpret_cast<double*>(keys_[cur ^ 1]);
+    // ---- K2: onesweep radix sort over the top bits of the span, then K2c/K3 unique --------
     if (want_grade) {
         s = grow(reinterpret_cast<void**>(&grade_), &grade_cap_, std::max<uint64_t>(4, k * 4));
         if (!s.good()) return s;
     }
-    UniqueArgs ua{keys_[cur], k, scale, want_grade ? grade_ : nullptr, status_,
-                  counters_ + 40, small_ + 2, next_epochs(1, st)};
-    launches += launch_unique(ua, st);
-    PH0B_CHECK_LAUNCH("unique kernel");
+    int cur = 0;
+    double* scale = nullptr;
+    for (int attempt = 0;; ++attempt) {
+        SortPlan plan{};
+        const uint32_t low_bits =
+            truncated_plan(kmax - kmin, attempt == 0 ? max_sort_passes() : 8u, &plan);
+        if (attempt > 0) {
+            // an equal-prefix run was too long to fix up in place: regenerate the u-major
+            // edges and sort every digit (rare: only for heavily clumped lengths)
+            PH0B_TRY(cudaMemsetAsync(hist_, 0, 256 * 4, st), "memset");
+            launches += launch_distance(da, st, num_sms_);
+            PH0B_CHECK_LAUNCH("distance kernel (redo)");
+        }
+        SortArgs sa{};
+        sa.count = k;
+        sa.kmin = kmin;
+        sa.keys[0] = keys_[0];
+        sa.keys[1] = keys_[1];
+        sa.vals[0] = vals_[0];
+        sa.vals[1] = vals_[1];
+        sa.status = status_;
+        sa.hist = hist_;
+        sa.tile_counter = counters_ + 32;
+        sa.epoch_base = next_epochs(plan.passes + 1, st);
+        if (plan.passes > 0 && plan.shift[0] != 0) {
+            // first digit is not the raw low byte: count it over (key - kmin)
+            PH0B_TRY(cudaMemsetAsync(hist_, 0, 256 * 4, st), "memset");
+            launches += launch_digit_histogram(keys_[0], k, kmin, plan.shift[0], hist_, st,
+                                               num_sms_);
+            sa.hist0_rot = 0;
+        } else {
+            sa.hist0_rot = (uint32_t)(kmin & 0xFFu);  // distance kernel's raw low-byte histogram
+        }
+        int sl = 0;
+        cur = launch_sort_passes(sa, plan, st, num_sms_, &sl);
+        launches += sl;
+        PH0B_CHECK_LAUNCH("radix sort");
+        PH0B_TRY(cudaEventRecord(ev_[2], st), "event");
+        r.times.sort_passes += plan.passes;
+
+        scale = reinterpret_cast<double*>(keys_[cur ^ 1]);
+        uint32_t* redo = reinterpret_cast<uint32_t*>(small_ + 4);
+        PH0B_TRY(cudaMemsetAsync(redo, 0, 4, st), "memset");
+        UniqueArgs ua{keys_[cur], vals_[cur], k, kmin, low_bits, scale,
+                      want_grade ? grade_ : nullptr, status_, counters_ + 40, small_ + 2,
+                      next_epochs(1, st), redo};
+        launches += launch_unique(ua, st);
+        PH0B_CHECK_LAUNCH("unique kernel");
+        if (low_bits == 0) break;
+        PH0B_TRY(cudaMemcpyAsync(h_small_ + 4, small_ + 4, 8, cudaMemcpyDeviceToHost, st), "D2H");
+        PH0B_TRY(cudaStreamSynchronize(st), "unique");
+        if (static_cast<uint32_t>(h_small_[4]) == 0) break;
+    }
     PH0B_TRY(cudaEventRecord(ev_[3], st), "event");
     r.d_uv_sorted = vals_[cur];
     r.d_grade = want_grade ? grade_ : nullptr;
