@@ -145,8 +145,9 @@ Status Context::reserve(uint64_t n, uint64_t d) {
     G(xin_, xin_cap_, std::max<uint64_t>(8, n * d * 8));
     G(xpad_, xpad_cap_, std::max<uint64_t>(8, d * ldx * 8));
     for (int i = 0; i < 2; ++i) {
-        G(keys_[i], keys_cap_[i], std::max<uint64_t>(8, k * 8));
-        G(vals_[i], vals_cap_[i], std::max<uint64_t>(4, k * 4));
+        // +256 B: the TMA bulk prefetch of the last sort tile rounds its size up to 16 B
+        G(keys_[i], keys_cap_[i], k * 8 + 256);
+        G(vals_[i], vals_cap_[i], k * 4 + 256);
         G(cand_[i], cand_cap_[i], cand * 4);
         G(survkeys_[i], survkeys_cap_[i], std::max<uint64_t>(8, n * 8));
     }

@@ -235,6 +235,189 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks)
     }
 }
 
+// ---- persistent onesweep with TMA bulk prefetch -------------------------------------------
+// Static tile assignment (tile = blockIdx.x + r * gridDim.x, all CTAs co-resident), so a
+// CTA can prefetch its next tile with cp.async.bulk (TMA, mbarrier completion) while it is
+// still in the look-back and write-out phases of the current one; the look-back chain only
+// ever waits on tiles of the same or an earlier round, which are being processed by
+// co-resident CTAs (deadlock-free).
+constexpr int kPTile = 4096;
+constexpr int kPItems = kPTile / kThreads;  // 16
+
+__device__ __forceinline__ uint32_t smem_addr(const void* p) {
+    return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes,
+                                         uint64_t* bar) {
+    asm volatile(
+        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
+        ::"r"(smem_addr(dst)), "l"(src), "r"(bytes), "r"(smem_addr(bar))
+        : "memory");
+}
+__device__ __forceinline__ void mbar_arrive_tx(uint64_t* bar, uint32_t bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_addr(bar)),
+                 "r"(bytes)
+                 : "memory");
+}
+__device__ __forceinline__ void mbar_wait_parity(uint64_t* bar, uint32_t parity) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n"
+        "WAITP_%=:\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
+        "@!p bra WAITP_%=;\n}" ::"r"(smem_addr(bar)),
+        "r"(parity)
+        : "memory");
+}
+
+template <bool kVals, bool kCountNext>
+__global__ void __launch_bounds__(kThreads, 2)
+    k2_onesweep_p(const uint64_t* __restrict__ keys_in, uint64_t* __restrict__ keys_out,
+                  const uint32_t* __restrict__ vals_in, uint32_t* __restrict__ vals_out,
+                  uint64_t count, uint64_t kmin, uint32_t shift, uint32_t next_shift,
+                  const uint32_t* __restrict__ hist, uint32_t hist_rot,
+                  uint64_t* __restrict__ status, uint32_t epoch,
+                  uint32_t* __restrict__ next_hist, uint32_t num_tiles) {
+    extern __shared__ __align__(128) uint64_t p_dyn[];
+    uint64_t* st_k = p_dyn;                                                    // stage keys
+    uint32_t* st_v = reinterpret_cast<uint32_t*>(p_dyn + kPTile);              // stage vals
+    uint64_t* so_k = p_dyn + kPTile + kPTile / 2;                              // sorted keys
+    uint32_t* so_v = reinterpret_cast<uint32_t*>(so_k + kPTile);               // sorted vals
+    __shared__ uint32_t s_whist[kWarps][kBins];
+    __shared__ uint32_t s_tile_start[kBins];
+    __shared__ uint32_t s_global[kBins];
+    __shared__ uint32_t s_bin_start[kBins];
+    __shared__ uint32_t s_next[kCountNext ? kBins : 1];
+    __shared__ uint32_t s_scan[kWarps];
+    __shared__ __align__(8) uint64_t s_bar;
+
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const uint32_t t = tid;  // digit handled by this thread in the per-digit phases
+    if (tid == 0) {
+        asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_addr(&s_bar)));
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    if (kCountNext) s_next[tid] = 0;
+    {
+        const uint32_t hcount = hist[(t + hist_rot) & 0xFFu];
+        s_bin_start[t] = block_exclusive_scan(hcount, s_scan, nullptr);
+    }
+    __syncthreads();
+
+    auto issue = [&](uint32_t tl) {
+        const uint64_t b0 = (uint64_t)tl * kPTile;
+        const uint64_t n = count - b0 < (uint64_t)kPTile ? count - b0 : (uint64_t)kPTile;
+        const uint32_t bk = (uint32_t)((n * 8 + 15) & ~15ull);
+        const uint32_t bv = kVals ? (uint32_t)((n * 4 + 15) & ~15ull) : 0u;
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+        mbar_arrive_tx(&s_bar, bk + bv);
+        bulk_g2s(st_k, keys_in + b0, bk, &s_bar);
+        if (kVals) bulk_g2s(st_v, vals_in + b0, bv, &s_bar);
+    };
+    uint32_t tile = blockIdx.x;
+    if (tid == 0 && tile < num_tiles) issue(tile);
+    uint32_t parity = 0;
+    const uint32_t lt = lanemask_lt();
+
+    for (; tile < num_tiles; tile += gridDim.x) {
+        const uint64_t base = (uint64_t)tile * kPTile;
+        const uint64_t rem = count - base;
+        const uint32_t tile_n = rem < (uint64_t)kPTile ? (uint32_t)rem : (uint32_t)kPTile;
+#pragma unroll
+        for (int w = 0; w < kWarps; ++w) s_whist[w][tid] = 0;
+        __syncthreads();
+        mbar_wait_parity(&s_bar, parity);
+        parity ^= 1u;
+
+        // ---- rank within the warp (keys from the staged tile) --------------------------
+        uint64_t k[kPItems];
+        uint32_t rank2[kPItems / 2];
+        const uint32_t wofs = warp * (32 * kPItems) + lane;
+#pragma unroll
+        for (int i = 0; i < kPItems; ++i) {
+            const uint32_t pos = wofs + 32 * i;
+            const bool valid = pos < tile_n;
+            k[i] = valid ? st_k[pos] : ~0ull;
+            const uint32_t d = valid ? (uint32_t)((k[i] - kmin) >> shift) & 0xFFu : 0x100u;
+            const uint32_t r = valid ? atomicAdd(&s_whist[warp][d], 1u) : 0u;
+            if (i & 1)
+                rank2[i / 2] |= r << 16;
+            else
+                rank2[i / 2] = r;
+        }
+        (void)lt;
+        __syncthreads();
+
+        uint32_t cnt = 0;
+#pragma unroll
+        for (int w = 0; w < kWarps; ++w) {
+            const uint32_t c = s_whist[w][t];
+            s_whist[w][t] = cnt;
+            cnt += c;
+        }
+        uint64_t* my_status = status + (uint64_t)tile * kBins + t;
+        st_relaxed_u64(my_status,
+                       pack_status(tile == 0 ? kStateInclusive : kStateAggregate, epoch, cnt));
+        uint64_t probe = tile > 0 ? ld_relaxed_u64(status + (uint64_t)(tile - 1) * kBins + t) : 0ull;
+        const uint32_t tstart = block_exclusive_scan(cnt, s_scan, nullptr);
+        s_tile_start[t] = tstart;
+        __syncthreads();
+
+        // ---- scatter the staged tile into the sorted buffer (shared -> shared) ----------
+#pragma unroll
+        for (int i = 0; i < kPItems; ++i) {
+            const uint32_t pos = wofs + 32 * i;
+            if (pos < tile_n) {
+                const uint32_t d = (uint32_t)((k[i] - kmin) >> shift) & 0xFFu;
+                const uint32_t dst = s_tile_start[d] + s_whist[warp][d] +
+                                     ((i & 1) ? (rank2[i / 2] >> 16) : (rank2[i / 2] & 0xFFFFu));
+                so_k[dst] = k[i];
+                if (kVals) so_v[dst] = st_v[pos];
+            }
+        }
+        __syncthreads();  // the stage buffer is free: prefetch the next tile now
+        const uint32_t next = tile + gridDim.x;
+        if (tid == 0 && next < num_tiles) issue(next);
+
+        // ---- decoupled look-back, per digit ----------------------------------------------
+        uint32_t excl = 0;
+        if (tile > 0) {
+            int64_t p = (int64_t)tile - 1;
+            for (;;) {
+                const uint32_t st = status_state(probe, epoch);
+                if (st != 0) {
+                    excl += (uint32_t)probe;
+                    if (st == kStateInclusive) break;
+                    --p;
+                }
+                probe = ld_relaxed_u64(status + (uint64_t)p * kBins + t);
+            }
+            st_relaxed_u64(my_status, pack_status(kStateInclusive, epoch, excl + cnt));
+        }
+        s_global[t] = s_bin_start[t] + excl - tstart;
+        __syncthreads();
+
+        // ---- write out: consecutive threads -> consecutive positions of each digit run ---
+#pragma unroll 4
+        for (int j = 0; j < kPItems; ++j) {
+            const uint32_t p = j * kThreads + tid;
+            if (p < tile_n) {
+                const uint64_t key = so_k[p];
+                const uint64_t rel = key - kmin;
+                const uint32_t d = (uint32_t)(rel >> shift) & 0xFFu;
+                const uint64_t out = (uint64_t)(uint32_t)(s_global[d] + p);
+                keys_out[out] = key;
+                if (kVals) vals_out[out] = so_v[p];
+                if (kCountNext) atomicAdd(&s_next[(uint32_t)(rel >> next_shift) & 0xFFu], 1u);
+            }
+        }
+    }
+    if (kCountNext) {
+        __syncthreads();
+        const uint32_t c = s_next[tid];
+        if (c) atomicAdd(&next_hist[tid], c);
+    }
+}
+
 // Histogram of one digit of (key - kmin) (used only when the distance kernel's raw
 // low-byte histogram does not apply, e.g. for the survivor sort).
 __global__ void k2_digit_histogram(const uint64_t* __restrict__ keys, uint64_t count,
@@ -274,6 +457,35 @@ int rank_variant() {
         g_rank_variant = e ? atoi(e) : 2;
     }
     return g_rank_variant;
+}
+
+template <bool kVals, bool kCountNext>
+void launch_pass_p(const SortArgs& a, int cur, uint32_t p, const SortPlan& plan, uint32_t rot,
+                   uint32_t* next_hist, cudaStream_t s, int num_sms) {
+    auto kern = k2_onesweep_p<kVals, kCountNext>;
+    const size_t smem = (size_t)kPTile * 8 * 2 + (size_t)kPTile * 4 * 2;
+    static int grid_per_sm = 0;
+    if (!grid_per_sm) {
+        cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&grid_per_sm, kern, kThreads, smem);
+        if (grid_per_sm < 1) grid_per_sm = 1;
+    }
+    const uint64_t tiles = (a.count + kPTile - 1) / kPTile;
+    uint64_t grid = (uint64_t)num_sms * grid_per_sm;
+    if (grid > tiles) grid = tiles;
+    const uint32_t next_shift = kCountNext ? plan.shift[p + 1] : 0u;
+    kern<<<(unsigned)grid, kThreads, smem, s>>>(
+        a.keys[cur], a.keys[cur ^ 1], kVals ? a.vals[cur] : nullptr,
+        kVals ? a.vals[cur ^ 1] : nullptr, a.count, a.kmin, plan.shift[p], next_shift,
+        a.hist + kBins * p, rot, a.status, a.epoch_base + p, next_hist, (uint32_t)tiles);
+}
+
+bool use_persistent() {
+    static const bool v = [] {
+        const char* e = getenv("PH0B_SORT_KERNEL");
+        return !(e && e[0] == 'o');  // 'o' = original dynamic-tile onesweep
+    }();
+    return v;
 }
 
 template <bool kVals, bool kCountNext>
@@ -348,7 +560,6 @@ int launch_digit_histogram(const uint64_t* keys, uint64_t count, uint64_t kmin, 
 
 int launch_sort_passes(const SortArgs& a, const SortPlan& plan, cudaStream_t s, int num_sms,
                        int* launches) {
-    (void)num_sms;
     int cur = 0;
     const uint64_t tiles = sort_tiles(a.count);
     if (a.count == 0 || plan.passes == 0) return 0;
@@ -360,7 +571,19 @@ int launch_sort_passes(const SortArgs& a, const SortPlan& plan, cudaStream_t s, 
         const bool last = p + 1 == plan.passes;
         uint32_t* next_hist = last ? nullptr : a.hist + kBins * (p + 1);
         const uint32_t rot = (p == 0) ? a.hist0_rot : 0u;
-        if (a.vals[0]) {
+        if (use_persistent() && rank_variant() == 3) {
+            if (a.vals[0]) {
+                if (last)
+                    launch_pass_p<true, false>(a, cur, p, plan, rot, next_hist, s, num_sms);
+                else
+                    launch_pass_p<true, true>(a, cur, p, plan, rot, next_hist, s, num_sms);
+            } else {
+                if (last)
+                    launch_pass_p<false, false>(a, cur, p, plan, rot, next_hist, s, num_sms);
+                else
+                    launch_pass_p<false, true>(a, cur, p, plan, rot, next_hist, s, num_sms);
+            }
+        } else if (a.vals[0]) {
             if (last)
                 launch_pass<true, false>(a, cur, p, plan, rot, next_hist, tiles, s);
             else

@@ -21,7 +21,7 @@
 namespace ph0b {
 namespace {
 
-constexpr int kThreads = 256;
+constexpr int kThreads = 512;
 constexpr int kWarps = kThreads / 32;
 constexpr int kItems = 16;
 constexpr int kTileKeys = kThreads * kItems;
@@ -52,7 +52,7 @@ __device__ void fix_run(uint64_t* keys, uint32_t* vals, uint64_t a, uint32_t len
 // owns exactly the runs that start in it (its first elements may continue the previous
 // tile's run; its last run may extend past its end).  Runs longer than kMaxRun raise
 // *redo and the caller re-sorts with the full digit plan.
-__global__ void __launch_bounds__(kThreads)
+__global__ void __launch_bounds__(kThreads, 2)
     k3_unique(uint64_t* __restrict__ keys, uint32_t* __restrict__ vals, uint64_t count,
               uint64_t kmin, uint32_t low_bits, double* __restrict__ scale,
               uint32_t* __restrict__ grade, uint64_t* __restrict__ status,
@@ -62,8 +62,12 @@ __global__ void __launch_bounds__(kThreads)
     __shared__ uint32_t s_prefix;
     __shared__ uint64_t s_own[2];
     __shared__ uint32_t s_ext_tot;
+    __shared__ int s_fixed;
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-    if (tid == 0) s_tile = atomicAdd(tile_counter, 1u);
+    if (tid == 0) {
+        s_tile = atomicAdd(tile_counter, 1u);
+        s_fixed = 0;
+    }
     __syncthreads();
     const uint32_t tile = s_tile;
     const uint64_t tile_start = (uint64_t)tile * kTileKeys;
@@ -71,16 +75,27 @@ __global__ void __launch_bounds__(kThreads)
     const uint64_t wbase = tile_start + (uint64_t)warp * (32 * kItems) + lane;
     auto pre = [&](uint64_t kk) { return (kk - kmin) >> low_bits; };
 
+    uint64_t k[kItems];
+#pragma unroll
+    for (int i = 0; i < kItems; ++i) {
+        const uint64_t idx = wbase + 32 * i;
+        k[i] = idx < tile_end ? keys[idx] : 0ull;
+    }
+
     uint64_t own_start = tile_start, own_end = tile_end;
     if (low_bits) {
-        // ---- phase A: sort the runs that start in this tile ---------------------------
-#pragma unroll 1
+        // ---- phase A: sort the equal-prefix runs that start in this tile ----------------
+        bool fixed = false;
+#pragma unroll
         for (int i = 0; i < kItems; ++i) {
             const uint64_t idx = wbase + 32 * i;
+            uint64_t prev = __shfl_up_sync(0xffffffffu, k[i], 1);
+            uint64_t next = __shfl_down_sync(0xffffffffu, k[i], 1);
+            if (lane == 0 && idx > 0 && idx < tile_end) prev = keys[idx - 1];
+            if (lane == 31 && idx + 1 < count && idx < tile_end) next = keys[idx + 1];
             if (idx + 1 >= count || idx >= tile_end) continue;
-            const uint64_t p = pre(keys[idx]);
-            if (pre(keys[idx + 1]) != p) continue;
-            if (idx > 0 && pre(keys[idx - 1]) == p) continue;  // not a run start
+            const uint64_t p = pre(k[i]);
+            if (pre(next) != p || (idx > 0 && pre(prev) == p)) continue;  // not a run start
             uint32_t len = 2;
             while (idx + len < count && len <= kMaxRun && pre(keys[idx + len]) == p) ++len;
             if (len > kMaxRun) {
@@ -88,26 +103,32 @@ __global__ void __launch_bounds__(kThreads)
                 continue;
             }
             fix_run(keys, vals, idx, len);
+            fixed = true;
         }
-        __syncthreads();  // block-wide visibility of the fixed runs (global memory)
+        if (__syncthreads_or(fixed)) {
+#pragma unroll
+            for (int i = 0; i < kItems; ++i) {  // re-read the (partly) re-ordered tile
+                const uint64_t idx = wbase + 32 * i;
+                k[i] = idx < tile_end ? keys[idx] : 0ull;
+            }
+        }
         if (tid == 0) {
             // skip the continuation of a run owned by an earlier tile
-            uint64_t s = tile_start;
-            if (s > 0) {
-                const uint64_t p0 = pre(keys[s - 1]);
-                while (s < count && s < tile_start + kMaxRun + 1 && pre(keys[s]) == p0) ++s;
+            uint64_t st = tile_start;
+            if (st > 0) {
+                const uint64_t p0 = pre(keys[st - 1]);
+                while (st < tile_end && st < tile_start + kMaxRun + 1 && pre(keys[st]) == p0) ++st;
             }
             // extend through the run that crosses the tile end
             uint64_t e = tile_end;
-            if (e < count && e > s) {
+            if (e < count && e > st) {
                 const uint64_t pl = pre(keys[e - 1]);
                 while (e < count && e < tile_end + kMaxRun + 1 && pre(keys[e]) == pl) ++e;
             }
-            if (s >= tile_end) s = e = tile_end;  // the whole tile continues an earlier run
-            s_own[0] = s;
+            if (st >= tile_end) st = e = tile_end;  // the whole tile continues an earlier run
+            s_own[0] = st;
             s_own[1] = e;
-            // distinct values in the extension [tile_end, e)
-            uint32_t ext = 0;
+            uint32_t ext = 0;  // distinct values in the extension [tile_end, e)
             for (uint64_t g = tile_end; g < e; ++g) ext += keys[g] != keys[g - 1] ? 1u : 0u;
             s_ext_tot = ext;
         }
@@ -117,14 +138,12 @@ __global__ void __launch_bounds__(kThreads)
     }
 
     // ---- phase B: flags, counts, look-back, D -------------------------------------------
-    uint64_t k[kItems];
     uint32_t ball[kItems];
     uint32_t total = 0;
 #pragma unroll
     for (int i = 0; i < kItems; ++i) {
         const uint64_t idx = wbase + 32 * i;
         const bool valid = idx < tile_end;
-        k[i] = valid ? keys[idx] : 0ull;
         uint64_t prev = __shfl_up_sync(0xffffffffu, k[i], 1);
         if (lane == 0 && valid && idx > 0) prev = keys[idx - 1];
         const bool owned = valid && idx >= own_start && idx < own_end;
@@ -150,13 +169,15 @@ __global__ void __launch_bounds__(kThreads)
         } else {
             st_relaxed_u64(my, pack_status(kStateAggregate, epoch, tile_tot));
             int64_t p = (int64_t)tile - 1;
-            while (p >= 0) {
-                const uint64_t s = ld_relaxed_u64(status + p);
-                const uint32_t st = status_state(s, epoch);
-                if (st == 0) continue;
-                excl += (uint32_t)s;
-                if (st == kStateInclusive) break;
-                --p;
+            uint64_t probe = ld_relaxed_u64(status + p);
+            for (;;) {
+                const uint32_t st = status_state(probe, epoch);
+                if (st != 0) {
+                    excl += (uint32_t)probe;
+                    if (st == kStateInclusive) break;
+                    --p;
+                }
+                probe = ld_relaxed_u64(status + p);
             }
             st_relaxed_u64(my, pack_status(kStateInclusive, epoch, excl + tile_tot));
         }
