@@ -54,6 +54,38 @@ __device__ __forceinline__ uint32_t status_state(uint64_t s, uint32_t epoch) {
     return ((uint32_t)(s >> 32) & 0x3FFFFFFFu) == (epoch & 0x3FFFFFFFu) ? (uint32_t)(s >> 62) : 0u;
 }
 
+// Decoupled look-back for one prefix column: sums the counts of tiles tile-1, tile-2, ...
+// down to the nearest INCLUSIVE entry.  `stride` is the distance in words between the
+// status entries of consecutive tiles for this column.  Instead of one L2 round trip per
+// predecessor, a window of W predecessors is read per round trip.
+template <int W>
+__device__ __forceinline__ uint32_t lookback_window(const uint64_t* status, uint64_t stride,
+                                                    uint32_t tile, uint32_t epoch) {
+    uint32_t excl = 0;
+    int64_t p = (int64_t)tile - 1;
+    while (p >= 0) {
+        uint64_t s[W];
+#pragma unroll
+        for (int j = 0; j < W; ++j)
+            s[j] = (p - j >= 0) ? ld_relaxed_u64(status + (uint64_t)(p - j) * stride) : 0ull;
+        int consumed = 0;
+        bool done = false;
+#pragma unroll
+        for (int j = 0; j < W; ++j) {
+            if (done || consumed != j) break;
+            if (p - j < 0) break;
+            const uint32_t st = status_state(s[j], epoch);
+            if (st == 0) break;  // not yet published: poll again from here
+            excl += (uint32_t)s[j];
+            ++consumed;
+            if (st == kStateInclusive) done = true;
+        }
+        if (done) break;
+        p -= consumed;
+    }
+    return excl;
+}
+
 // Upper-triangle edge indexing in the reference's u-major order (filtration.cpp:14-15):
 // e(u, v) = u*(2N-u-1)/2 + (v-u-1) for u < v.
 __host__ __device__ __forceinline__ uint64_t row_base(uint64_t u, uint64_t n) {

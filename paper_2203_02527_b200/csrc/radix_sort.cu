@@ -381,16 +381,11 @@ __global__ void __launch_bounds__(kThreads, 2)
         // ---- decoupled look-back, per digit ----------------------------------------------
         uint32_t excl = 0;
         if (tile > 0) {
-            int64_t p = (int64_t)tile - 1;
-            for (;;) {
-                const uint32_t st = status_state(probe, epoch);
-                if (st != 0) {
-                    excl += (uint32_t)probe;
-                    if (st == kStateInclusive) break;
-                    --p;
-                }
-                probe = ld_relaxed_u64(status + (uint64_t)p * kBins + t);
-            }
+            const uint32_t st0 = status_state(probe, epoch);
+            if (st0 == kStateInclusive)
+                excl = (uint32_t)probe;  // common case: the early probe already has it
+            else
+                excl = lookback_window<8>(status + t, kBins, tile, epoch);
             st_relaxed_u64(my_status, pack_status(kStateInclusive, epoch, excl + cnt));
         }
         s_global[t] = s_bin_start[t] + excl - tstart;

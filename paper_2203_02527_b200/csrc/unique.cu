@@ -168,17 +168,7 @@ __global__ void __launch_bounds__(kThreads, 2)
             st_relaxed_u64(my, pack_status(kStateInclusive, epoch, tile_tot));
         } else {
             st_relaxed_u64(my, pack_status(kStateAggregate, epoch, tile_tot));
-            int64_t p = (int64_t)tile - 1;
-            uint64_t probe = ld_relaxed_u64(status + p);
-            for (;;) {
-                const uint32_t st = status_state(probe, epoch);
-                if (st != 0) {
-                    excl += (uint32_t)probe;
-                    if (st == kStateInclusive) break;
-                    --p;
-                }
-                probe = ld_relaxed_u64(status + p);
-            }
+            excl = lookback_window<8>(status, 1, tile, epoch);
             st_relaxed_u64(my, pack_status(kStateInclusive, epoch, excl + tile_tot));
         }
         s_prefix = excl;
