@@ -152,6 +152,35 @@ int ph0b_run_host(ph0b_context* ctx, const double* X, uint64_t n, uint64_t d, ui
                   uint64_t* n_finite, uint64_t* essential_count, double* scale,
                   uint64_t scale_capacity, uint64_t* n_scale, ph0b_stage_times* times);
 
+/* ---- sharded (multi-GPU) stages: one context per rank; the caller exchanges data between
+ * ranks (NCCL).  SURVEY.md §8(e); orchestration in paper_2203_02527_b200/sharded.py. ----- */
+/* K1 over rows [u_lo, u_hi): their edges in u-major order, into the context workspace. */
+int ph0b_shard_distances(ph0b_context* ctx, const double* dX, uint64_t n, uint64_t d,
+                         uint32_t layout, uint64_t u_lo, uint64_t u_hi, void* stream,
+                         uint64_t* count, uint64_t* kmin, uint64_t* kmax);
+/* s evenly spaced length keys of the local edges (host), for splitter selection. */
+int ph0b_shard_sample(ph0b_context* ctx, uint64_t s, uint64_t* out_host);
+/* Stable partition of the local edges by parts-1 ascending splitter keys: segment j
+ * (contiguous in the returned device send buffers) goes to rank j.  counts/part_min/
+ * part_max: host arrays of `parts` entries. */
+int ph0b_shard_partition(ph0b_context* ctx, const uint64_t* splitters, uint32_t parts,
+                         void* stream, uint64_t** d_keys_send, uint32_t** d_vals_send,
+                         uint64_t* counts, uint64_t* part_min, uint64_t* part_max);
+/* Device receive buffers for `count` edges (keys u64, columns u32). */
+int ph0b_shard_recv(ph0b_context* ctx, uint64_t count, uint64_t** d_keys, uint32_t** d_vals);
+/* Sort + unique of the received slice: local |D| and the device pointer of the D slice. */
+int ph0b_shard_sort_unique(ph0b_context* ctx, uint64_t count, uint64_t kmin, uint64_t kmax,
+                           void* stream, uint64_t* n_distinct, const double** d_scale);
+/* Column reduction of the local slice + collect: m surviving columns in slice order, their
+ * supports (u << 16 | v), grades (+ grade_offset) and lengths, as device pointers. */
+int ph0b_shard_reduce(ph0b_context* ctx, uint64_t n, uint64_t count, uint64_t grade_offset,
+                      void* stream, uint64_t* m, const uint32_t** d_uv,
+                      const uint64_t** d_grade, const double** d_length);
+/* Column reduction of `count` columns given in filtration order (device supports): host
+ * indices of the surviving columns, ascending. */
+int ph0b_reduce_columns(ph0b_context* ctx, const uint32_t* d_uv, uint64_t count, uint64_t n,
+                        void* stream, uint32_t* idx_host, uint64_t* n_out);
+
 /* ---- utilities ------------------------------------------------------------------------ */
 const char* ph0b_last_error(void);
 uint32_t ph0b_abi_version(void);

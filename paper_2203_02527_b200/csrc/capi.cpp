@@ -100,6 +100,12 @@ int copy_out(Context* c, const RunOutputs& r, cudaStream_t s, uint64_t* death_gr
 
 }  // namespace
 
+namespace ph0b {
+int capi_fail(const Status& s) { return fail(s); }
+int capi_fail(int code, const std::string& msg) { return fail(code, msg); }
+void capi_set_launches(uint64_t n) { g_last_launches = n; }
+}  // namespace ph0b
+
 extern "C" {
 
 const char* ph0b_last_error(void) { return g_last_error.c_str(); }

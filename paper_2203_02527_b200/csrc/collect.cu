@@ -20,9 +20,15 @@ __global__ void k5_widen(const uint32_t* __restrict__ in, uint32_t m, uint64_t* 
         out[i] = in[i];
 }
 
+__global__ void k5_narrow(const uint64_t* __restrict__ in, uint32_t m, uint32_t* __restrict__ out) {
+    for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < m; i += gridDim.x * blockDim.x)
+        out[i] = (uint32_t)in[i];
+}
+
 __global__ void k5_map(const uint64_t* __restrict__ cols_sorted, uint32_t m,
                        const uint64_t* __restrict__ sorted_keys, const double* __restrict__ scale,
-                       const uint64_t* __restrict__ n_scale, uint32_t* __restrict__ surv_sorted,
+                       const uint64_t* __restrict__ n_scale, uint64_t grade_offset,
+                       uint32_t* __restrict__ surv_sorted,
                        uint64_t* __restrict__ death_grade, double* __restrict__ death_length) {
     const uint64_t* dbits = reinterpret_cast<const uint64_t*>(scale);
     const uint64_t ns = *n_scale;
@@ -37,7 +43,7 @@ __global__ void k5_map(const uint64_t* __restrict__ cols_sorted, uint32_t m,
             else
                 hi = mid;
         }
-        death_grade[i] = lo + 1;
+        death_grade[i] = grade_offset + lo + 1;
         death_length[i] = __longlong_as_double((long long)key);
         surv_sorted[i] = (uint32_t)j;
     }
@@ -73,12 +79,19 @@ __global__ void k5_claimed_lows(const uint32_t* __restrict__ surv_sorted, uint32
 // a.surv: unordered survivors; a.surv_scratch reinterpreted as 2 x m u64 ping-pong is not
 // enough room, so the caller passes u64 scratch through SortArgs (see pipeline).
 int launch_collect_map(const uint64_t* cols_sorted, uint32_t m, const uint64_t* sorted_keys,
-                       const double* scale, const uint64_t* n_scale, uint32_t* surv_sorted,
-                       uint64_t* death_grade, double* death_length, cudaStream_t s) {
+                       const double* scale, const uint64_t* n_scale, uint64_t grade_offset,
+                       uint32_t* surv_sorted, uint64_t* death_grade, double* death_length,
+                       cudaStream_t s) {
     if (m == 0) return 0;
     const unsigned grid = (m + 255) / 256;
-    k5_map<<<grid, 256, 0, s>>>(cols_sorted, m, sorted_keys, scale, n_scale, surv_sorted,
-                                death_grade, death_length);
+    k5_map<<<grid, 256, 0, s>>>(cols_sorted, m, sorted_keys, scale, n_scale, grade_offset,
+                                surv_sorted, death_grade, death_length);
+    return 1;
+}
+
+int launch_narrow(const uint64_t* in, uint32_t m, uint32_t* out, cudaStream_t s) {
+    if (m == 0) return 0;
+    k5_narrow<<<(m + 255) / 256, 256, 0, s>>>(in, m, out);
     return 1;
 }
 

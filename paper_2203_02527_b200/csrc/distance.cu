@@ -37,6 +37,7 @@ template <int D>
 __device__ __forceinline__ void tile_edges(const double* __restrict__ xu_src,
                                            const double* __restrict__ xv_src, uint64_t stride,
                                            int dd, uint32_t n, uint32_t u0, uint32_t v0,
+                                           uint32_t u_lo, uint32_t u_hi, uint64_t e_off,
                                            uint64_t* __restrict__ keys,
                                            uint32_t* __restrict__ vals, uint64_t& kmin,
                                            uint64_t& kmax, uint32_t* sh_hist) {
@@ -56,9 +57,10 @@ __device__ __forceinline__ void tile_edges(const double* __restrict__ xu_src,
     const uint64_t nn = n;
     for (int i = warp; i < kTile; i += kWarps) {
         const uint32_t u = u0 + i;
-        if (u >= n) break;
+        if (u >= u_hi) break;
         if (u + 1 >= v0 + kTile) break;  // no v > u left in this tile (diagonal tiles)
-        const uint64_t base = row_base(u, nn) - u - 1;
+        if (u < u_lo) continue;          // row outside this shard's row range
+        const uint64_t base = row_base(u, nn) - u - 1 - e_off;
         double acc[kRV];
         if constexpr (kStatic && D <= 8) {
             double xu[D];
@@ -146,7 +148,8 @@ __device__ __forceinline__ void finish_block(uint64_t kmin, uint64_t kmax, uint3
 template <int D>
 __global__ void __launch_bounds__(kThreads)
     k1_distance_tma(const __grid_constant__ CUtensorMap tmap, uint32_t n, uint32_t dd,
-                    uint32_t nb, uint32_t total_tiles, uint64_t* __restrict__ keys,
+                    uint32_t nb, uint32_t total_tiles, uint32_t t0, uint32_t u_lo, uint32_t u_hi,
+                    uint64_t e_off, uint64_t* __restrict__ keys,
                     uint32_t* __restrict__ vals, uint64_t* minmax, uint32_t* hist0) {
     extern __shared__ __align__(128) double smem[];
     __shared__ uint64_t bar[2];
@@ -169,7 +172,7 @@ __global__ void __launch_bounds__(kThreads)
     uint32_t tile = blockIdx.x;
     auto issue = [&](uint32_t t, int b) {
         uint32_t bu, bv;
-        tile_coords(t, nb, bu, bv);
+        tile_coords(t + t0, nb, bu, bv);
         asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
         mbar_expect_tx(&bar[b], bytes);
         tma_load_2d(buf[b], &tmap, &bar[b], (int)(bu * kTile), 0);
@@ -187,9 +190,9 @@ __global__ void __launch_bounds__(kThreads)
         const uint32_t next = tile + gridDim.x;
         if (threadIdx.x == 0 && next < total_tiles) issue(next, b ^ 1);
         uint32_t bu, bv;
-        tile_coords(tile, nb, bu, bv);
-        tile_edges<D>(buf[b], buf[b] + tile_elems, kTile, dim, n, bu * kTile, bv * kTile, keys,
-                      vals, kmin, kmax, sh_hist);
+        tile_coords(tile + t0, nb, bu, bv);
+        tile_edges<D>(buf[b], buf[b] + tile_elems, kTile, dim, n, bu * kTile, bv * kTile, u_lo,
+                      u_hi, e_off, keys, vals, kmin, kmax, sh_hist);
         b ^= 1;
     }
     __syncthreads();
@@ -199,7 +202,8 @@ __global__ void __launch_bounds__(kThreads)
 // Global-memory path for d > 32 (reads X through L1/L2; same arithmetic and order).
 __global__ void __launch_bounds__(kThreads)
     k1_distance_global(const double* __restrict__ xpad, uint64_t ldx, uint32_t n, uint32_t dd,
-                       uint32_t nb, uint32_t total_tiles, uint64_t* __restrict__ keys,
+                       uint32_t nb, uint32_t total_tiles, uint32_t t0, uint32_t u_lo,
+                       uint32_t u_hi, uint64_t e_off, uint64_t* __restrict__ keys,
                        uint32_t* __restrict__ vals, uint64_t* minmax, uint32_t* hist0) {
     __shared__ uint32_t sh_hist[256];
     __shared__ uint64_t sh_min[kWarps], sh_max[kWarps];
@@ -208,9 +212,9 @@ __global__ void __launch_bounds__(kThreads)
     uint64_t kmin = ~0ull, kmax = 0;
     for (uint32_t tile = blockIdx.x; tile < total_tiles; tile += gridDim.x) {
         uint32_t bu, bv;
-        tile_coords(tile, nb, bu, bv);
+        tile_coords(tile + t0, nb, bu, bv);
         tile_edges<0>(xpad + bu * kTile, xpad + bv * kTile, ldx, (int)dd, n, bu * kTile,
-                      bv * kTile, keys, vals, kmin, kmax, sh_hist);
+                      bv * kTile, u_lo, u_hi, e_off, keys, vals, kmin, kmax, sh_hist);
     }
     __syncthreads();
     finish_block(kmin, kmax, sh_hist, sh_min, sh_max, minmax, hist0);
@@ -271,7 +275,7 @@ namespace {
 
 template <int D>
 int launch_tma(const DistanceArgs& a, const CUtensorMap& map, uint32_t nb, uint32_t total,
-               cudaStream_t s, int num_sms) {
+               uint32_t t0, cudaStream_t s, int num_sms) {
     const uint32_t dim = D > 0 ? D : a.d;
     const size_t smem = 4ull * kTile * dim * sizeof(double);
     auto kern = k1_distance_tma<D>;
@@ -281,8 +285,8 @@ int launch_tma(const DistanceArgs& a, const CUtensorMap& map, uint32_t nb, uint3
     if (per_sm < 1) per_sm = 1;
     uint32_t grid = (uint32_t)num_sms * per_sm;
     if (grid > total) grid = total;
-    kern<<<grid, kThreads, smem, s>>>(map, a.n, a.d, nb, total, a.keys, a.vals, a.minmax,
-                                      a.hist0);
+    kern<<<grid, kThreads, smem, s>>>(map, a.n, a.d, nb, total, t0, a.u_lo, a.u_hi, a.e_off,
+                                      a.keys, a.vals, a.minmax, a.hist0);
     return 1;
 }
 
@@ -299,25 +303,30 @@ int launch_pack_points(const double* x, uint32_t layout, uint32_t n, uint32_t d,
 }
 
 int launch_distance(const DistanceArgs& a, cudaStream_t s, int num_sms) {
-    if (a.n < 2) return 0;
+    if (a.n < 2 || a.u_hi <= a.u_lo) return 0;
     const uint32_t nb = (a.n + kTile - 1) / kTile;
-    const uint32_t total = nb * (nb + 1) / 2;
+    // tile rows bu_lo..bu_hi of the upper triangle (rowstart(b) = b*nb - b*(b-1)/2)
+    auto rowstart = [nb](uint64_t b) { return b * nb - b * (b - 1) / 2; };
+    const uint32_t bu_lo = a.u_lo / kTile, bu_hi = (a.u_hi - 1) / kTile;
+    const uint32_t t0 = (uint32_t)rowstart(bu_lo);
+    const uint32_t total = (uint32_t)(rowstart(bu_hi + 1) - t0);
     CUtensorMap map;
     if (a.d >= 1 && a.d <= (uint32_t)kMaxTmaDim && make_point_tmap(a.xpad, a.ldx, a.d, &map)) {
         switch (a.d) {
-            case 1: return launch_tma<1>(a, map, nb, total, s, num_sms);
-            case 2: return launch_tma<2>(a, map, nb, total, s, num_sms);
-            case 3: return launch_tma<3>(a, map, nb, total, s, num_sms);
-            case 4: return launch_tma<4>(a, map, nb, total, s, num_sms);
-            case 8: return launch_tma<8>(a, map, nb, total, s, num_sms);
-            case 16: return launch_tma<16>(a, map, nb, total, s, num_sms);
-            default: return launch_tma<0>(a, map, nb, total, s, num_sms);
+            case 1: return launch_tma<1>(a, map, nb, total, t0, s, num_sms);
+            case 2: return launch_tma<2>(a, map, nb, total, t0, s, num_sms);
+            case 3: return launch_tma<3>(a, map, nb, total, t0, s, num_sms);
+            case 4: return launch_tma<4>(a, map, nb, total, t0, s, num_sms);
+            case 8: return launch_tma<8>(a, map, nb, total, t0, s, num_sms);
+            case 16: return launch_tma<16>(a, map, nb, total, t0, s, num_sms);
+            default: return launch_tma<0>(a, map, nb, total, t0, s, num_sms);
         }
     }
     uint32_t grid = (uint32_t)num_sms * 4;
     if (grid > total) grid = total;
-    k1_distance_global<<<grid, kThreads, 0, s>>>(a.xpad, a.ldx, a.n, a.d, nb, total, a.keys,
-                                                 a.vals, a.minmax, a.hist0);
+    k1_distance_global<<<grid, kThreads, 0, s>>>(a.xpad, a.ldx, a.n, a.d, nb, total, t0, a.u_lo,
+                                                 a.u_hi, a.e_off, a.keys, a.vals, a.minmax,
+                                                 a.hist0);
     return 1;
 }
 

@@ -16,6 +16,9 @@ struct DistanceArgs {
     uint32_t* vals;       // [K] u << 16 | v
     uint64_t* minmax;     // [2] running min / max key (init ~0 / 0)
     uint32_t* hist0;      // [256] histogram of raw key bits 0..7
+    uint32_t u_lo = 0;    // rows [u_lo, u_hi) only (sharded runs); u_hi = n for all rows
+    uint32_t u_hi = 0;
+    uint64_t e_off = 0;   // edge index of (u_lo, u_lo+1): outputs are written at e - e_off
 };
 // Returns number of kernel launches issued (0 on error; check cudaGetLastError).
 int launch_distance(const DistanceArgs& a, cudaStream_t s, int num_sms);
@@ -105,12 +108,24 @@ int run_reduction(ReduceState& st, cudaStream_t s, int num_sms, uint32_t& epoch,
 // cols_sorted: survivor column ids in filtration order (u64, from the keys-only sort).
 // Writes surv_sorted (u32), death_grade = 1 + lower_bound(D, length), death_length.
 int launch_collect_map(const uint64_t* cols_sorted, uint32_t m, const uint64_t* sorted_keys,
-                       const double* scale, const uint64_t* n_scale, uint32_t* surv_sorted,
-                       uint64_t* death_grade, double* death_length, cudaStream_t s);
+                       const double* scale, const uint64_t* n_scale, uint64_t grade_offset,
+                       uint32_t* surv_sorted, uint64_t* death_grade, double* death_length,
+                       cudaStream_t s);
 int launch_widen(const uint32_t* in, uint32_t m, uint64_t* out, cudaStream_t s);
+int launch_narrow(const uint64_t* in, uint32_t m, uint32_t* out, cudaStream_t s);
 
 // Claimed lows (reduction.cpp:44-45) of survivors in filtration order: single-CTA union-find.
 int launch_claimed_lows(const uint32_t* surv_sorted, uint32_t m, const uint32_t* uv, uint32_t n,
                         uint32_t* lows, cudaStream_t s);
+
+// ---- multi-GPU splitter partition (shard.cu) ---------------------------------------------
+int launch_partition(const uint64_t* keys, const uint32_t* vals, uint64_t count,
+                     const uint64_t* d_splitters, uint32_t parts, uint32_t* d_counts_scratch,
+                     uint64_t* d_totals, uint64_t* d_bminmax, uint64_t* keys_out,
+                     uint32_t* vals_out, cudaStream_t s);
+uint64_t partition_scratch_words(uint64_t count, uint32_t parts);
+int launch_sample(const uint64_t* keys, uint64_t count, uint64_t s, uint64_t* out, cudaStream_t st);
+int launch_gather_u32(const uint32_t* src, const uint32_t* idx, uint64_t m, uint32_t* out,
+                      cudaStream_t st);
 
 }  // namespace ph0b

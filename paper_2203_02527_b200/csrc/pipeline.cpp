@@ -54,6 +54,8 @@ inline uint32_t truncated_plan(uint64_t span, uint32_t max_passes, SortPlan* pla
     return low;
 }
 
+inline uint64_t row_base(uint64_t u, uint64_t n) { return u * (2 * n - u - 1) / 2; }
+
 uint32_t max_sort_passes() {
     static const uint32_t v = [] {
         const char* e = getenv("PH0B_MAX_PASSES");
@@ -132,25 +134,16 @@ Status Context::grow(void** p, uint64_t* cap, uint64_t need) {
     return Status::ok();
 }
 
-Status Context::reserve(uint64_t n, uint64_t d) {
+Status Context::reserve_points(uint64_t n, uint64_t d) {
     PH0B_TRY(cudaSetDevice(device_), "cudaSetDevice");
-    const uint64_t k = n * (n - (n > 0)) / 2;
     const uint64_t ldx = std::max<uint64_t>(128, (n + 127) / 128 * 128);
-    const uint64_t tiles = sort_tiles(std::max<uint64_t>(k, 1));
-    const uint64_t status_words = std::max<uint64_t>(tiles * 256, sort_tiles(n + 1) * 256);
-    const uint64_t cand = std::max<uint64_t>(1, std::min<uint64_t>(k, kCandCap));
+    const uint64_t status_words = sort_tiles(n + 1) * 256;
     Status s;
 #define G(ptr, cap, bytes)                                                    \
     if (!(s = grow(reinterpret_cast<void**>(&(ptr)), &(cap), (bytes))).good()) return s;
     G(xin_, xin_cap_, std::max<uint64_t>(8, n * d * 8));
     G(xpad_, xpad_cap_, std::max<uint64_t>(8, d * ldx * 8));
-    for (int i = 0; i < 2; ++i) {
-        // +256 B: the TMA bulk prefetch of the last sort tile rounds its size up to 16 B
-        G(keys_[i], keys_cap_[i], k * 8 + 256);
-        G(vals_[i], vals_cap_[i], k * 4 + 256);
-        G(cand_[i], cand_cap_[i], cand * 4);
-        G(survkeys_[i], survkeys_cap_[i], std::max<uint64_t>(8, n * 8));
-    }
+    for (int i = 0; i < 2; ++i) G(survkeys_[i], survkeys_cap_[i], std::max<uint64_t>(8, n * 8));
     if (status_words * 8 > status_cap_) status_zeroed_ = false;
     G(status_, status_cap_, status_words * 8);
     G(comp_, comp_cap_, std::max<uint64_t>(4, n * 4));
@@ -160,6 +153,68 @@ Status Context::reserve(uint64_t n, uint64_t d) {
     G(lows_, lows_cap_, std::max<uint64_t>(4, n * 4));
     G(death_grade_, death_grade_cap_, std::max<uint64_t>(8, n * 8));
     G(death_length_, death_length_cap_, std::max<uint64_t>(8, n * 8));
+#undef G
+    if (!status_zeroed_) {
+        PH0B_TRY(cudaMemset(status_, 0, status_cap_), "cudaMemset status");
+        epoch_ = 1;
+        status_zeroed_ = true;
+    }
+    return Status::ok();
+}
+
+Status Context::reserve(uint64_t n, uint64_t d) {
+    Status s = reserve_points(n, d);
+    if (!s.good()) return s;
+    return reserve_edges(n * (n - (n > 0)) / 2);
+}
+
+Status Context::reserve_recv(uint64_t k) {
+    Status s;
+    if (!(s = grow(reinterpret_cast<void**>(&keys_[0]), &keys_cap_[0], k * 8 + 256)).good())
+        return s;
+    return grow(reinterpret_cast<void**>(&vals_[0]), &vals_cap_[0], k * 4 + 256);
+}
+
+Status Context::sort_survivors(uint32_t m, uint64_t count, cudaStream_t st) {
+    if (m == 0) return Status::ok();
+    launches += launch_widen(surv_, m, survkeys_[0], st);
+    SortPlan sp{};
+    span_passes(count > 1 ? count - 1 : 1, &sp);
+    PH0B_TRY(cudaMemsetAsync(hist_, 0, 256 * 4, st), "memset");
+    launches += launch_digit_histogram(survkeys_[0], m, 0, 0, hist_, st, num_sms_);
+    SortArgs sv{};
+    sv.count = m;
+    sv.kmin = 0;
+    sv.keys[0] = survkeys_[0];
+    sv.keys[1] = survkeys_[1];
+    sv.status = status_;
+    sv.hist = hist_;
+    sv.tile_counter = counters_ + 48;
+    sv.epoch_base = next_epochs(sp.passes + 1, st);
+    sv.hist0_rot = 0;
+    int l2 = 0;
+    surv_sorted_idx_ = launch_sort_passes(sv, sp, st, num_sms_, &l2);
+    launches += l2;
+    launches += launch_narrow(survkeys_[surv_sorted_idx_], m, surv_sorted_, st);
+    PH0B_CHECK_LAUNCH("survivor sort");
+    return Status::ok();
+}
+
+Status Context::reserve_edges(uint64_t k) {
+    PH0B_TRY(cudaSetDevice(device_), "cudaSetDevice");
+    const uint64_t status_words = sort_tiles(std::max<uint64_t>(k, 1)) * 256;
+    Status s;
+#define G(ptr, cap, bytes)                                                    \
+    if (!(s = grow(reinterpret_cast<void**>(&(ptr)), &(cap), (bytes))).good()) return s;
+    const uint64_t cand = std::max<uint64_t>(1, std::min<uint64_t>(k, kCandCap));
+    for (int i = 0; i < 2; ++i) {
+        // +256 B: the TMA bulk prefetch of the last sort tile rounds its size up to 16 B
+        G(keys_[i], keys_cap_[i], k * 8 + 256);
+        G(vals_[i], vals_cap_[i], k * 4 + 256);
+        G(cand_[i], cand_cap_[i], cand * 4);
+    }
+    if (status_words * 8 > status_cap_) status_zeroed_ = false;
+    G(status_, status_cap_, status_words * 8);
 #undef G
     if (!status_zeroed_) {
         PH0B_TRY(cudaMemset(status_, 0, status_cap_), "cudaMemset status");
@@ -190,20 +245,10 @@ Status Context::run_host_input(const double* X, uint64_t n, uint64_t d, uint32_t
     return run(xin_, n, d, layout, stream, stop, want_grade, out);
 }
 
-Status Context::run(const double* dX, uint64_t n, uint64_t d, uint32_t layout,
-                    cudaStream_t stream, StopAfter stop, bool want_grade, RunOutputs* out) {
-    Status s = reserve(n, d);
-    if (!s.good()) return s;
-    cudaStream_t st = stream ? stream : stream_;
-    launches = 0;
-    const uint64_t k = n * (n - (n > 0)) / 2;
+Status Context::stage_distances(const double* dX, uint64_t n, uint64_t d, uint32_t layout,
+                                uint64_t u_lo, uint64_t u_hi, cudaStream_t st, uint64_t* count,
+                                uint64_t* kmin, uint64_t* kmax) {
     const uint64_t ldx = std::max<uint64_t>(128, (n + 127) / 128 * 128);
-    RunOutputs r;
-    r.k = k;
-    std::memset(&r.times, 0, sizeof(r.times));
-
-    PH0B_TRY(cudaEventRecord(ev_[0], st), "event");
-    // ---- K1: pack + distances ------------------------------------------------------------
     PH0B_TRY(cudaMemsetAsync(small_, 0xFF, 8, st), "memset");        // min = ~0
     PH0B_TRY(cudaMemsetAsync(small_ + 1, 0, 3 * 8, st), "memset");   // max, n_scale, flag
     PH0B_TRY(cudaMemsetAsync(hist_, 0, 256 * 4, st), "memset");
@@ -211,14 +256,137 @@ Status Context::run(const double* dX, uint64_t n, uint64_t d, uint32_t layout,
                                    reinterpret_cast<uint32_t*>(small_ + 3), st);
     PH0B_CHECK_LAUNCH("pack_points");
     DistanceArgs da{xpad_, ldx, (uint32_t)n, (uint32_t)d, keys_[0], vals_[0], small_, hist_};
+    da.u_lo = (uint32_t)u_lo;
+    da.u_hi = (uint32_t)u_hi;
+    da.e_off = u_lo < n ? row_base(u_lo, n) : 0;
     launches += launch_distance(da, st, num_sms_);
     PH0B_CHECK_LAUNCH("distance kernel");
-    PH0B_TRY(cudaEventRecord(ev_[1], st), "event");
     PH0B_TRY(cudaMemcpyAsync(h_small_, small_, 4 * 8, cudaMemcpyDeviceToHost, st), "D2H");
     PH0B_TRY(cudaStreamSynchronize(st), "distance stage");
     if (static_cast<uint32_t>(h_small_[3]) != 0)
         return {PH0B_ERR_NONFINITE, "point cloud contains non-finite coordinates"};
-    const uint64_t kmin = h_small_[0], kmax = h_small_[1];
+    const uint64_t hi = std::min<uint64_t>(u_hi, n);
+    *count = (u_lo < hi) ? row_base(hi, n) - row_base(u_lo, n) : 0;
+    *kmin = h_small_[0];
+    *kmax = h_small_[1];
+    xpad_ld_ = ldx;
+    xpad_d_ = d;
+    return Status::ok();
+}
+
+Status Context::stage_sort_unique(uint64_t k, uint64_t kmin, uint64_t kmax, bool raw_hist,
+                                  bool want_grade, cudaStream_t st, uint32_t* passes) {
+    if (want_grade) {
+        Status s = grow(reinterpret_cast<void**>(&grade_), &grade_cap_, std::max<uint64_t>(4, k * 4));
+        if (!s.good()) return s;
+    }
+    int src = 0;
+    cur_ = 0;
+    *passes = 0;
+    if (k == 0) {
+        PH0B_TRY(cudaMemsetAsync(small_ + 2, 0, 8, st), "memset");
+        scale_ = reinterpret_cast<double*>(keys_[1]);
+        return Status::ok();
+    }
+    for (int attempt = 0;; ++attempt) {
+        SortPlan plan{};
+        const uint32_t low_bits =
+            truncated_plan(kmax - kmin, attempt == 0 ? max_sort_passes() : 8u, &plan);
+        // attempt > 0: an equal-prefix run was too long to fix up in place; every radix pass
+        // and every run fix-up so far was stable, so re-sorting the current order over all
+        // digits restores the exact (length, u, v) order.
+        SortArgs sa{};
+        sa.count = k;
+        sa.kmin = kmin;
+        sa.keys[0] = keys_[src];
+        sa.keys[1] = keys_[src ^ 1];
+        sa.vals[0] = vals_[src];
+        sa.vals[1] = vals_[src ^ 1];
+        sa.status = status_;
+        sa.hist = hist_;
+        sa.tile_counter = counters_ + 32;
+        sa.epoch_base = next_epochs(plan.passes + 1, st);
+        if (plan.passes > 0 && (plan.shift[0] != 0 || !raw_hist || attempt > 0)) {
+            PH0B_TRY(cudaMemsetAsync(hist_, 0, 256 * 4, st), "memset");
+            launches += launch_digit_histogram(keys_[src], k, kmin, plan.shift[0], hist_, st,
+                                               num_sms_);
+            sa.hist0_rot = 0;
+        } else {
+            sa.hist0_rot = (uint32_t)(kmin & 0xFFu);  // distance kernel's raw low-byte histogram
+        }
+        int sl = 0;
+        const int out = launch_sort_passes(sa, plan, st, num_sms_, &sl);
+        cur_ = src ^ out;
+        launches += sl;
+        PH0B_CHECK_LAUNCH("radix sort");
+        PH0B_TRY(cudaEventRecord(ev_[2], st), "event");
+        *passes += plan.passes;
+
+        scale_ = reinterpret_cast<double*>(keys_[cur_ ^ 1]);
+        uint32_t* redo = reinterpret_cast<uint32_t*>(small_ + 4);
+        PH0B_TRY(cudaMemsetAsync(redo, 0, 4, st), "memset");
+        UniqueArgs ua{keys_[cur_], vals_[cur_], k, kmin, low_bits, scale_,
+                      want_grade ? grade_ : nullptr, status_, counters_ + 40, small_ + 2,
+                      next_epochs(1, st), redo};
+        launches += launch_unique(ua, st);
+        PH0B_CHECK_LAUNCH("unique kernel");
+        if (low_bits == 0) break;
+        PH0B_TRY(cudaMemcpyAsync(h_small_ + 4, small_ + 4, 8, cudaMemcpyDeviceToHost, st), "D2H");
+        PH0B_TRY(cudaStreamSynchronize(st), "unique");
+        if (static_cast<uint32_t>(h_small_[4]) == 0) break;
+        src = cur_;
+    }
+    return Status::ok();
+}
+
+Status Context::stage_reduce(const uint32_t* uv, uint64_t count, uint32_t n, cudaStream_t st,
+                             ReduceStats* rst) {
+    ReduceState rs{};
+    rs.n = n;
+    rs.k = count;
+    rs.uv = uv;
+    rs.comp = comp_;
+    rs.best = best_;
+    rs.cand[0] = cand_[0];
+    rs.cand[1] = cand_[1];
+    rs.cap = cand_cap_[0] / 4;
+    rs.surv = surv_;
+    rs.counters = counters_;
+    rs.host_counters = h_counters_;
+    uint32_t ep = 0;
+    run_reduction(rs, st, num_sms_, ep, rst);
+    launches += rst->launches;
+    PH0B_CHECK_LAUNCH("reduction");
+    return Status::ok();
+}
+
+Status Context::stage_collect(uint32_t m, uint64_t count, uint64_t grade_offset, cudaStream_t st) {
+    if (m == 0) return Status::ok();
+    Status s = sort_survivors(m, count, st);
+    if (!s.good()) return s;
+    launches += launch_collect_map(survkeys_[surv_sorted_idx_], m, keys_[cur_], scale_, small_ + 2,
+                                   grade_offset, surv_sorted_, death_grade_, death_length_, st);
+    PH0B_CHECK_LAUNCH("collect");
+    return Status::ok();
+}
+
+Status Context::run(const double* dX, uint64_t n, uint64_t d, uint32_t layout,
+                    cudaStream_t stream, StopAfter stop, bool want_grade, RunOutputs* out) {
+    Status s = reserve(n, d);
+    if (!s.good()) return s;
+    cudaStream_t st = stream ? stream : stream_;
+    launches = 0;
+    const uint64_t k = n * (n - (n > 0)) / 2;
+    RunOutputs r;
+    r.k = k;
+    std::memset(&r.times, 0, sizeof(r.times));
+
+    PH0B_TRY(cudaEventRecord(ev_[0], st), "event");
+    // ---- K1: pack + distances ------------------------------------------------------------
+    uint64_t cnt = 0, kmin = 0, kmax = 0;
+    s = stage_distances(dX, n, d, layout, 0, n, st, &cnt, &kmin, &kmax);
+    if (!s.good()) return s;
+    PH0B_TRY(cudaEventRecord(ev_[1], st), "event");
     r.d_lengths_umajor = keys_[0];
     if (stop == StopAfter::Distance || k == 0) {
         r.essential = n;
@@ -233,88 +401,19 @@ Status Context::run(const double* dX, uint64_t n, uint64_t d, uint32_t layout,
         return Status::ok();
     }
 
-    // ---- K2: onesweep radix sort over the top bits of the span, then K2c/K3 unique --------
-    if (want_grade) {
-        s = grow(reinterpret_cast<void**>(&grade_), &grade_cap_, std::max<uint64_t>(4, k * 4));
-        if (!s.good()) return s;
-    }
-    int cur = 0;
-    double* scale = nullptr;
-    for (int attempt = 0;; ++attempt) {
-        SortPlan plan{};
-        const uint32_t low_bits =
-            truncated_plan(kmax - kmin, attempt == 0 ? max_sort_passes() : 8u, &plan);
-        if (attempt > 0) {
-            // an equal-prefix run was too long to fix up in place: regenerate the u-major
-            // edges and sort every digit (rare: only for heavily clumped lengths)
-            PH0B_TRY(cudaMemsetAsync(hist_, 0, 256 * 4, st), "memset");
-            launches += launch_distance(da, st, num_sms_);
-            PH0B_CHECK_LAUNCH("distance kernel (redo)");
-        }
-        SortArgs sa{};
-        sa.count = k;
-        sa.kmin = kmin;
-        sa.keys[0] = keys_[0];
-        sa.keys[1] = keys_[1];
-        sa.vals[0] = vals_[0];
-        sa.vals[1] = vals_[1];
-        sa.status = status_;
-        sa.hist = hist_;
-        sa.tile_counter = counters_ + 32;
-        sa.epoch_base = next_epochs(plan.passes + 1, st);
-        if (plan.passes > 0 && plan.shift[0] != 0) {
-            // first digit is not the raw low byte: count it over (key - kmin)
-            PH0B_TRY(cudaMemsetAsync(hist_, 0, 256 * 4, st), "memset");
-            launches += launch_digit_histogram(keys_[0], k, kmin, plan.shift[0], hist_, st,
-                                               num_sms_);
-            sa.hist0_rot = 0;
-        } else {
-            sa.hist0_rot = (uint32_t)(kmin & 0xFFu);  // distance kernel's raw low-byte histogram
-        }
-        int sl = 0;
-        cur = launch_sort_passes(sa, plan, st, num_sms_, &sl);
-        launches += sl;
-        PH0B_CHECK_LAUNCH("radix sort");
-        PH0B_TRY(cudaEventRecord(ev_[2], st), "event");
-        r.times.sort_passes += plan.passes;
-
-        scale = reinterpret_cast<double*>(keys_[cur ^ 1]);
-        uint32_t* redo = reinterpret_cast<uint32_t*>(small_ + 4);
-        PH0B_TRY(cudaMemsetAsync(redo, 0, 4, st), "memset");
-        UniqueArgs ua{keys_[cur], vals_[cur], k, kmin, low_bits, scale,
-                      want_grade ? grade_ : nullptr, status_, counters_ + 40, small_ + 2,
-                      next_epochs(1, st), redo};
-        launches += launch_unique(ua, st);
-        PH0B_CHECK_LAUNCH("unique kernel");
-        if (low_bits == 0) break;
-        PH0B_TRY(cudaMemcpyAsync(h_small_ + 4, small_ + 4, 8, cudaMemcpyDeviceToHost, st), "D2H");
-        PH0B_TRY(cudaStreamSynchronize(st), "unique");
-        if (static_cast<uint32_t>(h_small_[4]) == 0) break;
-    }
+    // ---- K2 + K2c/K3: radix sort over the top bits of the span, unique -> D, M -------------
+    s = stage_sort_unique(k, kmin, kmax, true, want_grade, st, &r.times.sort_passes);
+    if (!s.good()) return s;
     PH0B_TRY(cudaEventRecord(ev_[3], st), "event");
-    r.d_uv_sorted = vals_[cur];
+    r.d_uv_sorted = vals_[cur_];
     r.d_grade = want_grade ? grade_ : nullptr;
-    r.d_scale = scale;
+    r.d_scale = scale_;
 
     if (stop == StopAfter::Barcode) {
         // ---- K4: column reduction ----------------------------------------------------------
-        ReduceState rs{};
-        rs.n = (uint32_t)n;
-        rs.k = k;
-        rs.uv = vals_[cur];
-        rs.comp = comp_;
-        rs.best = best_;
-        rs.cand[0] = cand_[0];
-        rs.cand[1] = cand_[1];
-        rs.cap = cand_cap_[0] / 4;
-        rs.surv = surv_;
-        rs.counters = counters_;
-        rs.host_counters = h_counters_;
         ReduceStats rst;
-        uint32_t ep = 0;
-        run_reduction(rs, st, num_sms_, ep, &rst);
-        launches += rst.launches;
-        PH0B_CHECK_LAUNCH("reduction");
+        s = stage_reduce(vals_[cur_], k, (uint32_t)n, st, &rst);
+        if (!s.good()) return s;
         PH0B_TRY(cudaEventRecord(ev_[4], st), "event");
         r.times.reduce_rounds = rst.rounds;
         r.times.columns_scanned = rst.scanned;
@@ -322,29 +421,9 @@ Status Context::run(const double* dX, uint64_t n, uint64_t d, uint32_t layout,
         if (m != n - 1)
             return {PH0B_ERR_CUDA, "internal error: reduction produced " + std::to_string(m) +
                                        " surviving columns, expected " + std::to_string(n - 1)};
-
         // ---- K5: collect: survivors in filtration order -> intervals ----------------------
-        launches += launch_widen(surv_, m, survkeys_[0], st);
-        SortPlan sp{};
-        span_passes(k - 1, &sp);
-        PH0B_TRY(cudaMemsetAsync(hist_, 0, 256 * 4, st), "memset");
-        launches += launch_digit_histogram(survkeys_[0], m, 0, 0, hist_, st, num_sms_);
-        SortArgs sv{};
-        sv.count = m;
-        sv.kmin = 0;
-        sv.keys[0] = survkeys_[0];
-        sv.keys[1] = survkeys_[1];
-        sv.status = status_;
-        sv.hist = hist_;
-        sv.tile_counter = counters_ + 48;
-        sv.epoch_base = next_epochs(sp.passes + 1, st);
-        sv.hist0_rot = 0;
-        int l2 = 0;
-        const int c2 = launch_sort_passes(sv, sp, st, num_sms_, &l2);
-        launches += l2;
-        launches += launch_collect_map(survkeys_[c2], m, keys_[cur], scale, small_ + 2,
-                                       surv_sorted_, death_grade_, death_length_, st);
-        PH0B_CHECK_LAUNCH("collect");
+        s = stage_collect(m, k, 0, st);
+        if (!s.good()) return s;
         r.d_death_grade = death_grade_;
         r.d_death_length = death_length_;
         r.d_surv_sorted = surv_sorted_;

@@ -8,6 +8,7 @@
 #include <string>
 
 #include "../../include/ph0b.h"
+#include "kernels.h"
 
 namespace ph0b {
 
@@ -51,6 +52,36 @@ public:
     Status run_host_input(const double* X, uint64_t n, uint64_t d, uint32_t layout,
                           cudaStream_t stream, StopAfter stop, bool want_grade, RunOutputs* out);
     Status claimed_lows(const RunOutputs& r, uint32_t n, uint32_t* d_lows, cudaStream_t stream);
+
+    // ---- pipeline stages (single-GPU run() composes them; sharded runs call them) ------
+    Status stage_distances(const double* dX, uint64_t n, uint64_t d, uint32_t layout,
+                           uint64_t u_lo, uint64_t u_hi, cudaStream_t st, uint64_t* count,
+                           uint64_t* kmin, uint64_t* kmax);
+    Status stage_sort_unique(uint64_t count, uint64_t kmin, uint64_t kmax, bool raw_hist,
+                             bool want_grade, cudaStream_t st, uint32_t* passes);
+    Status stage_reduce(const uint32_t* uv, uint64_t count, uint32_t n, cudaStream_t st,
+                        ReduceStats* rst);
+    Status stage_collect(uint32_t m, uint64_t count, uint64_t grade_offset, cudaStream_t st);
+    Status reserve_edges(uint64_t count);  // ping-pong key/column buffers for count edges
+    Status reserve_points(uint64_t n, uint64_t d);
+    Status reserve_recv(uint64_t count);   // sharded receive side: buffer 0 only
+    Status sort_survivors(uint32_t m, uint64_t count, cudaStream_t st);
+    // workspace accessors for the sharded C entry points
+    uint64_t* keys(int i) { return keys_[i]; }
+    uint32_t* vals(int i) { return vals_[i]; }
+    int cur() const { return cur_; }
+    double* scale() { return scale_; }
+    uint64_t* small_dev() { return small_; }
+    uint64_t* small_host() { return h_small_; }
+    uint32_t* surv() { return surv_; }
+    uint32_t* surv_sorted() { return surv_sorted_; }
+    uint64_t* death_grade() { return death_grade_; }
+    double* death_length() { return death_length_; }
+    uint32_t* hist() { return hist_; }
+    uint64_t* status() { return status_; }
+    uint32_t* counters() { return counters_; }
+    int num_sms() const { return num_sms_; }
+    uint32_t epochs(uint32_t count, cudaStream_t s) { return next_epochs(count, s); }
     uint32_t* lows_buffer() { return lows_; }
 
     std::mutex mu;
@@ -93,6 +124,10 @@ private:
     uint32_t epoch_ = 1;
     bool status_zeroed_ = false;
     bool atomic_rank_ok_ = false;
+    int cur_ = 0;              // ping-pong index holding the sorted keys/columns
+    int surv_sorted_idx_ = 0;  // survkeys_ index holding the sorted survivor ids
+    double* scale_ = nullptr;  // D of the last sort_unique stage
+    uint64_t xpad_ld_ = 128, xpad_d_ = 0;
 };
 
 // Default per-device contexts used by the stateless C entry points.

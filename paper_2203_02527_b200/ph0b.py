@@ -32,7 +32,9 @@ EXPORTED_SYMBOLS = [
     "ph0b_build_filtration", "ph0b_claimed_lows", "ph0b_context_create", "ph0b_context_destroy",
     "ph0b_context_reserve", "ph0b_context_workspace_bytes", "ph0b_run_device", "ph0b_run_host",
     "ph0b_last_error", "ph0b_abi_version", "ph0b_host_alloc", "ph0b_host_free",
-    "ph0b_last_launch_count", "ph0b_generate_cloud",
+    "ph0b_last_launch_count", "ph0b_generate_cloud", "ph0b_shard_distances", "ph0b_shard_sample",
+    "ph0b_shard_partition", "ph0b_shard_recv", "ph0b_shard_sort_unique", "ph0b_shard_reduce",
+    "ph0b_reduce_columns",
 ]
 
 

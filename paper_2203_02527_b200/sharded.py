@@ -1,0 +1,290 @@
+"""Multi-GPU H0 barcode: one process (rank) per GPU, NCCL for the one real
+exchange step.
+
+    rank r:  K1 distances of rows [U_r, U_{r+1})      (balanced edge counts, no communication)
+             sample lengths -> all-gather -> P-1 splitters (global, on the length key)
+             stable partition by splitter -> all-to-all-v (NCCL) of (length, column)
+             local radix sort + unique  -> D slice r (D is sharded, contiguous in global order)
+             all-gather |D_r| -> grade offsets
+             local column reduction of the slice -> <= N-1 candidate columns
+             gather candidates -> rank 0: column reduction over <= P(N-1) columns -> bars
+
+Exactness: rows are assigned in increasing u and every partition is stable, so what a rank
+receives (sources in rank order) is in u-major order and the local stable sort produces the
+global (length, u, v) order restricted to its key range; equal lengths never straddle ranks
+(splitters are key values).  A column that reduces to zero inside its own key range closes a
+cycle of earlier columns, so it is a cycle globally; the survivors of all ranges, reduced again
+in global order, are exactly the reference's surviving columns (the minimum spanning forest).
+
+`Comm` hides the transport: torch.distributed (NCCL on GPUs, gloo for the CPU tests) or a
+thread-based comm that runs P virtual ranks in one process (single-GPU parity tests).
+"""
+from __future__ import annotations
+
+import ctypes as C
+import threading
+from dataclasses import dataclass
+
+import numpy as np
+
+from . import ph0b as _b
+
+SAMPLES_PER_RANK = 4096
+
+
+def row_ranges(n: int, parts: int) -> list[tuple[int, int]]:
+    """Contiguous row ranges [U_r, U_{r+1}) with ~K/parts edges each (row u has n-1-u)."""
+    k = n * (n - 1) // 2
+    bounds = [0]
+    cum = 0
+    u = 0
+    for r in range(1, parts):
+        target = (k * r) // parts
+        while u < n and cum + (n - 1 - u) <= target:
+            cum += n - 1 - u
+            u += 1
+        bounds.append(u)
+    bounds.append(n)
+    return [(bounds[i], bounds[i + 1]) for i in range(parts)]
+
+
+def choose_splitters(samples: np.ndarray, parts: int) -> np.ndarray:
+    s = np.sort(np.asarray(samples, np.uint64))
+    if parts <= 1 or len(s) == 0:
+        return np.zeros(max(parts - 1, 0), np.uint64)
+    idx = [((j + 1) * len(s)) // parts for j in range(parts - 1)]
+    return s[np.minimum(idx, len(s) - 1)].astype(np.uint64)
+
+
+@dataclass
+class ShardResult:
+    rank: int
+    parts: int
+    death_grade: np.ndarray | None      # rank 0 only (filtration order)
+    death_length: np.ndarray | None
+    essential_count: int
+    scale_offset: int                   # global index of this rank's first D entry
+    n_scale_local: int
+    n_scale_total: int
+    scale_local: object                 # backend-specific view of the D slice
+    edges_local: int
+
+
+# ---- transports -------------------------------------------------------------------------------
+class TorchComm:
+    """torch.distributed transport (NCCL for device tensors, gloo for CPU tensors)."""
+
+    def __init__(self, group=None):
+        import torch.distributed as dist
+        self.dist = dist
+        self.group = group
+        self.rank = dist.get_rank(group)
+        self.size = dist.get_world_size(group)
+
+    def allgather_obj(self, obj):
+        out = [None] * self.size
+        self.dist.all_gather_object(out, obj, group=self.group)
+        return out
+
+    def alltoallv(self, send, send_counts, recv, recv_counts):
+        self.dist.all_to_all_single(recv, send, [int(c) for c in recv_counts],
+                                    [int(c) for c in send_counts], group=self.group)
+        if recv.is_cuda:  # the next stage runs on the ph0b context's own stream
+            import torch
+            torch.cuda.current_stream(recv.device).synchronize()
+
+    def barrier(self):
+        self.dist.barrier(group=self.group)
+
+
+class ThreadComm:
+    """P virtual ranks as threads of one process (single-GPU multi-rank parity tests)."""
+
+    class _Shared:
+        def __init__(self, size):
+            self.size = size
+            self.barrier = threading.Barrier(size)
+            self.slots = [None] * size
+
+    def __init__(self, shared: "ThreadComm._Shared", rank: int):
+        self.s = shared
+        self.rank = rank
+        self.size = shared.size
+
+    @classmethod
+    def make(cls, size):
+        sh = cls._Shared(size)
+        return [cls(sh, r) for r in range(size)]
+
+    def allgather_obj(self, obj):
+        self.s.barrier.wait()
+        self.s.slots[self.rank] = obj
+        self.s.barrier.wait()
+        out = list(self.s.slots)
+        self.s.barrier.wait()
+        return out
+
+    def alltoallv(self, send, send_counts, recv, recv_counts):
+        import torch
+        torch.cuda.synchronize(send.device) if send.is_cuda else None
+        peers = self.allgather_obj((send, [int(c) for c in send_counts]))
+        pos = 0
+        for src in range(self.size):
+            sbuf, scounts = peers[src]
+            off = sum(scounts[: self.rank])
+            cnt = scounts[self.rank]
+            if cnt:
+                recv[pos:pos + cnt].copy_(sbuf[off:off + cnt])
+            pos += cnt
+        if recv.is_cuda:
+            torch.cuda.synchronize(recv.device)
+        self.allgather_obj(None)  # nobody reuses its send buffer before all copies are done
+
+    def barrier(self):
+        self.s.barrier.wait()
+
+
+# ---- device backend (the product path) -----------------------------------------------------
+class _CAI:
+    def __init__(self, ptr, count, typestr):
+        self.__cuda_array_interface__ = {"shape": (int(count),), "typestr": typestr,
+                                         "data": (int(ptr), False), "version": 3,
+                                         "strides": None}
+
+
+def _dev_view(ptr, count, typestr, device):
+    import torch
+    if count == 0:
+        return torch.empty(0, dtype={"<i8": torch.int64, "<i4": torch.int32,
+                                     "<f8": torch.float64}[typestr], device=f"cuda:{device}")
+    return torch.as_tensor(_CAI(ptr, count, typestr), device=f"cuda:{device}")
+
+
+class DeviceBackend:
+    """Per-rank stages on the B200 through the C ABI (one ph0b context per rank)."""
+
+    def __init__(self, device: int = 0):
+        self.device = device
+        self.ctx = _b.Context(device)
+        self.L = _b.lib()
+        h = self.ctx._h
+        self.h = h
+        L = self.L
+        vp, u64, u32 = C.c_void_p, C.c_uint64, C.c_uint32
+        u64p = C.POINTER(C.c_uint64)
+        for name, res, args in [
+            ("ph0b_shard_distances", C.c_int, [vp, vp, u64, u64, u32, u64, u64, vp, u64p, u64p, u64p]),
+            ("ph0b_shard_sample", C.c_int, [vp, u64, vp]),
+            ("ph0b_shard_partition", C.c_int, [vp, vp, u32, vp, C.POINTER(vp), C.POINTER(vp), vp, vp, vp]),
+            ("ph0b_shard_recv", C.c_int, [vp, u64, C.POINTER(vp), C.POINTER(vp)]),
+            ("ph0b_shard_sort_unique", C.c_int, [vp, u64, u64, u64, vp, u64p, C.POINTER(vp)]),
+            ("ph0b_shard_reduce", C.c_int, [vp, u64, u64, u64, vp, u64p, C.POINTER(vp), C.POINTER(vp), C.POINTER(vp)]),
+            ("ph0b_reduce_columns", C.c_int, [vp, vp, u64, u64, vp, vp, u64p]),
+        ]:
+            fn = getattr(L, name)
+            fn.restype, fn.argtypes = res, args
+
+    def distances(self, x_ptr, n, d, u_lo, u_hi, layout=_b.COL_MAJOR):
+        cnt, lo, hi = C.c_uint64(), C.c_uint64(), C.c_uint64()
+        _b._check(self.L.ph0b_shard_distances(self.h, C.c_void_p(x_ptr), n, d, layout, u_lo, u_hi,
+                                              None, C.byref(cnt), C.byref(lo), C.byref(hi)))
+        return cnt.value, lo.value, hi.value
+
+    def sample(self, s, count):
+        s = min(s, count)
+        out = np.zeros(s, np.uint64)
+        if s:
+            _b._check(self.L.ph0b_shard_sample(self.h, s, C.c_void_p(out.ctypes.data)))
+        return out
+
+    def partition(self, splitters, parts):
+        spl = np.ascontiguousarray(splitters, np.uint64)
+        counts = np.zeros(parts, np.uint64)
+        pmin = np.zeros(parts, np.uint64)
+        pmax = np.zeros(parts, np.uint64)
+        kp, vp_ = C.c_void_p(), C.c_void_p()
+        _b._check(self.L.ph0b_shard_partition(
+            self.h, C.c_void_p(spl.ctypes.data) if spl.size else None, parts, None, C.byref(kp),
+            C.byref(vp_), C.c_void_p(counts.ctypes.data), C.c_void_p(pmin.ctypes.data),
+            C.c_void_p(pmax.ctypes.data)))
+        total = int(counts.sum())
+        return (_dev_view(kp.value, total, "<i8", self.device),
+                _dev_view(vp_.value, total, "<i4", self.device), counts, pmin, pmax)
+
+    def recv(self, count):
+        kp, vp_ = C.c_void_p(), C.c_void_p()
+        _b._check(self.L.ph0b_shard_recv(self.h, count, C.byref(kp), C.byref(vp_)))
+        return (_dev_view(kp.value, count, "<i8", self.device),
+                _dev_view(vp_.value, count, "<i4", self.device))
+
+    def sort_unique(self, count, kmin, kmax):
+        nd, sp = C.c_uint64(), C.c_void_p()
+        _b._check(self.L.ph0b_shard_sort_unique(self.h, count, kmin, kmax, None, C.byref(nd),
+                                                C.byref(sp)))
+        return nd.value, _dev_view(sp.value, nd.value, "<f8", self.device)
+
+    def reduce(self, n, count, grade_offset):
+        m, up, gp, lp = C.c_uint64(), C.c_void_p(), C.c_void_p(), C.c_void_p()
+        _b._check(self.L.ph0b_shard_reduce(self.h, n, count, grade_offset, None, C.byref(m),
+                                           C.byref(up), C.byref(gp), C.byref(lp)))
+        m = m.value
+        uv = _dev_view(up.value, m, "<i4", self.device).cpu().numpy().view(np.uint32)
+        g = _dev_view(gp.value, m, "<i8", self.device).cpu().numpy().view(np.uint64)
+        ln = _dev_view(lp.value, m, "<f8", self.device).cpu().numpy()
+        return uv.copy(), g.copy(), ln.copy()
+
+    def reduce_columns(self, uv: np.ndarray, n: int) -> np.ndarray:
+        import torch
+        uv_dev = torch.from_numpy(np.ascontiguousarray(uv, np.uint32).view(np.int32)).to(
+            f"cuda:{self.device}")
+        idx = np.zeros(max(len(uv), 1), np.uint32)
+        cnt = C.c_uint64()
+        _b._check(self.L.ph0b_reduce_columns(self.h, C.c_void_p(uv_dev.data_ptr()), len(uv), n,
+                                              None, C.c_void_p(idx.ctypes.data), C.byref(cnt)))
+        return idx[: cnt.value].copy()
+
+    def close(self):
+        self.ctx.close()
+
+
+# ---- the SPMD driver -------------------------------------------------------------------------
+def h0_barcode_sharded(x_ptr, n: int, d: int, comm, backend, layout=_b.COL_MAJOR) -> ShardResult:
+    """Run on every rank (same X on every rank: it is <= 4 MiB, replicated)."""
+    P, r = comm.size, comm.rank
+    lo, hi = row_ranges(n, P)[r]
+    count, kmin, kmax = backend.distances(x_ptr, n, d, lo, hi, layout)
+    if P > 1:
+        samples = np.concatenate(comm.allgather_obj(backend.sample(SAMPLES_PER_RANK, count)))
+        spl = choose_splitters(samples, P)
+        send_k, send_v, counts, pmin, pmax = backend.partition(spl, P)
+        allc = np.array(comm.allgather_obj(counts), np.uint64)          # [src][dst]
+        allmin = np.array(comm.allgather_obj(pmin), np.uint64)
+        allmax = np.array(comm.allgather_obj(pmax), np.uint64)
+        recv_counts = allc[:, r]
+        total = int(recv_counts.sum())
+        have = recv_counts > 0
+        kmin = int(allmin[have, r].min()) if have.any() else 0
+        kmax = int(allmax[have, r].max()) if have.any() else 0
+        recv_k, recv_v = backend.recv(total)
+        comm.alltoallv(send_k, counts, recv_k, recv_counts)
+        comm.alltoallv(send_v, counts, recv_v, recv_counts)
+        count = total
+    n_distinct, scale = backend.sort_unique(count, kmin, kmax)
+    nds = comm.allgather_obj(int(n_distinct)) if P > 1 else [int(n_distinct)]
+    offset = int(sum(nds[:r]))
+    uv, grade, length = backend.reduce(n, count, offset)
+    cands = comm.allgather_obj((uv, grade, length)) if P > 1 else [(uv, grade, length)]
+    dg = dl = None
+    if r == 0:
+        all_uv = np.concatenate([c[0] for c in cands]) if cands else np.zeros(0, np.uint32)
+        all_g = np.concatenate([c[1] for c in cands]) if cands else np.zeros(0, np.uint64)
+        all_l = np.concatenate([c[2] for c in cands]) if cands else np.zeros(0)
+        if P > 1:
+            idx = backend.reduce_columns(all_uv, n)
+            dg, dl = all_g[idx], all_l[idx]
+        else:
+            dg, dl = all_g, all_l
+    ess = n - (n - 1 if n >= 1 else 0)
+    return ShardResult(rank=r, parts=P, death_grade=dg, death_length=dl, essential_count=ess,
+                       scale_offset=offset, n_scale_local=int(n_distinct),
+                       n_scale_total=int(sum(nds)), scale_local=scale, edges_local=count)
