@@ -172,6 +172,113 @@ def load_traffic():
     return None
 
 
+def run_sharded(args, cfg_name):
+    """N > 1 (torchrun, one rank per GPU): the sharded pipeline of sharded.py — rows split
+    across ranks, splitter partition + one NCCL all-to-all-v, D sharded, local + final column
+    reductions.  Total work fixed as N grows (strong scaling of the C5 problem)."""
+    import numpy as np
+    import torch
+    import torch.distributed as dist
+
+    import paper_2203_02527_b200 as pkg
+    from paper_2203_02527_b200.sharded import DeviceBackend, TorchComm, h0_barcode_sharded
+
+    ws, rank, local = dist_env()
+    torch.cuda.set_device(local)
+    dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    comm = TorchComm()
+    X = pkg.config_cloud(cfg_name)
+    n, d = X.shape
+    k = n * (n - 1) // 2
+    be = DeviceBackend(local)
+    xcm = np.asfortranarray(X).ravel(order="F").copy()
+    xdev = torch.from_numpy(xcm).to(f"cuda:{local}")
+
+    def sync_all():
+        torch.cuda.synchronize(local)
+        dist.barrier()
+
+    def timed(fn, steps):
+        sync_all()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        out = None
+        for _ in range(steps):
+            out = fn()
+        torch.cuda.synchronize(local)  # all streams (ph0b contexts, NCCL) drained
+        e1.record()
+        e1.synchronize()
+        ms = e0.elapsed_time(e1)
+        t = torch.tensor([ms], device=f"cuda:{local}")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return float(t.item()), out
+
+    step = lambda: h0_barcode_sharded(xdev.data_ptr(), n, d, comm, be)  # noqa: E731
+    for _ in range(args.warmup):
+        step()
+    l0 = be.launches
+    with ClockSampler(local) as clk:
+        ms, res = timed(step, args.steps)
+    launches0 = be.launches - l0
+    value = k * args.steps / (ms / 1e3)
+    sort_s, passes, sort_edges = be.last_sort
+
+    # e2e: pinned host X -> device, sharded pipeline, D slice + bars back to pinned host memory
+    xin = pkg.PinnedArray(n * d)
+    xin.array[:] = xcm
+    dpin = pkg.PinnedArray(max(res.n_scale_local, 1) * 2, np.float64)
+    bars = pkg.PinnedArray(2 * n, np.float64)
+    xbuf = torch.empty(n * d, dtype=torch.float64, device=f"cuda:{local}")
+
+    def e2e_step():
+        xbuf.copy_(torch.from_numpy(xin.array), non_blocking=True)
+        r = h0_barcode_sharded(xbuf.data_ptr(), n, d, comm, be)
+        host_d = torch.from_numpy(dpin.array[: r.n_scale_local])
+        host_d.copy_(r.scale_local)
+        if r.death_grade is not None:
+            bars.array[: len(r.death_length)] = r.death_length
+        return r
+
+    e2e_steps = args.e2e_steps or max(1, min(args.steps, 5))
+    e2e_step()
+    e2e_ms, r2 = timed(e2e_step, e2e_steps)
+    d2h = r2.n_scale_local * 8 + (16 * (n - 1) if rank == 0 else 0)
+    peak, peak_kind = peaks()
+    alg = (24 * max(passes, 1) + 16) * sort_edges
+    achieved = alg / sort_s / 1e9
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": ws, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": ms / args.steps, "higher_is_better": True,
+            "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": {"workload": f"{cfg_name}: {WORKLOADS[cfg_name]}", "n": n, "d": d,
+                       "edges": k, "parallelism": f"dp{ws} (row shards + splitter all-to-all)",
+                       "l2": "inputs larger than L2", "n_scale": res.n_scale_total,
+                       "bars": int(len(res.death_grade))},
+            "e2e": {"value": k * e2e_steps / (e2e_ms / 1e3), "unit": UNIT,
+                    "h2d_bytes_per_step": n * d * 8, "d2h_bytes_per_step": d2h,
+                    "ms_per_step": e2e_ms / e2e_steps, "steps": e2e_steps,
+                    "api": "sharded.h0_barcode_sharded (pinned host X; D slice per rank to pinned host)"},
+            "roofline": {"kernel": "shard sort+unique (rank 0: onesweep passes + unique)",
+                         "bound": "hbm", "achieved": round(achieved, 1), "peak": peak,
+                         "unit": "GB/s", "frac": round(achieved / peak, 4), "traffic": None,
+                         "peak_source": f"{peak_kind} (MEASURED_PEAKS.json hbm_gbs)",
+                         "alg_bytes_per_launch": alg, "passes": passes},
+            "cpu_baseline": None, "clocks": clk.summary(), "gpu_launches": launches0 or None,
+        }
+        if not args.no_cpu_baseline:
+            s_, kk, kind = cpu_reference_sample(X, min(CPU_BASELINE_N, n))
+            line["cpu_baseline"] = {"value": kk / s_, "unit": UNIT, "cores": 1, "kind": kind,
+                                    "sample": f"full reference path on the first "
+                                              f"{min(CPU_BASELINE_N, n)} points of {cfg_name}"}
+        print(json.dumps(line), flush=True)
+    for a in (xin, dpin, bars):
+        a.free()
+    be.close()
+    dist.barrier()
+    dist.destroy_process_group()
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -181,6 +288,10 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--e2e-steps", type=int, default=None)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--sharded", action="store_true",
+                    help="use the sharded multi-GPU pipeline even at N=1 (torchrun)")
+    ap.add_argument("--replicas", action="store_true",
+                    help="N>1: run N independent single-GPU replicas instead of the sharded path")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
     cfg_name = args.config
@@ -195,6 +306,9 @@ def main():
     import paper_2203_02527_b200 as pkg
 
     ws, rank, local = dist_env()
+    if (ws > 1 and not args.replicas) or args.sharded:
+        run_sharded(args, cfg_name)
+        return
     dist = None
     if ws > 1:
         import torch.distributed as dist

@@ -170,7 +170,8 @@ int ph0b_shard_partition(ph0b_context* ctx, const uint64_t* splitters, uint32_t 
 int ph0b_shard_recv(ph0b_context* ctx, uint64_t count, uint64_t** d_keys, uint32_t** d_vals);
 /* Sort + unique of the received slice: local |D| and the device pointer of the D slice. */
 int ph0b_shard_sort_unique(ph0b_context* ctx, uint64_t count, uint64_t kmin, uint64_t kmax,
-                           void* stream, uint64_t* n_distinct, const double** d_scale);
+                           void* stream, uint64_t* n_distinct, const double** d_scale,
+                           uint32_t* passes);
 /* Column reduction of the local slice + collect: m surviving columns in slice order, their
  * supports (u << 16 | v), grades (+ grade_offset) and lengths, as device pointers. */
 int ph0b_shard_reduce(ph0b_context* ctx, uint64_t n, uint64_t count, uint64_t grade_offset,

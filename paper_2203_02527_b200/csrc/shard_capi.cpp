@@ -163,7 +163,8 @@ int ph0b_shard_recv(ph0b_context* ctx, uint64_t count, uint64_t** d_keys, uint32
 }
 
 int ph0b_shard_sort_unique(ph0b_context* ctx, uint64_t count, uint64_t kmin, uint64_t kmax,
-                           void* stream, uint64_t* n_distinct, const double** d_scale) {
+                           void* stream, uint64_t* n_distinct, const double** d_scale,
+                           uint32_t* passes_out) {
     Context* c = reinterpret_cast<Context*>(ctx);
     std::lock_guard<std::mutex> lk(c->mu);
     Status s = c->reserve_edges(count);  // the send buffer is free now: grow the ping-pong
@@ -180,6 +181,7 @@ int ph0b_shard_sort_unique(ph0b_context* ctx, uint64_t count, uint64_t kmin, uin
         return ph0b::capi_fail(PH0B_ERR_CUDA, "shard sort");
     if (n_distinct) *n_distinct = c->small_host()[2];
     if (d_scale) *d_scale = c->scale();
+    if (passes_out) *passes_out = passes;
     return PH0B_OK;
 }
 

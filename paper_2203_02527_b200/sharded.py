@@ -165,6 +165,7 @@ class DeviceBackend:
 
     def __init__(self, device: int = 0):
         self.device = device
+        self.launches = 0  # kernel launches issued through this backend (evidence counter)
         self.ctx = _b.Context(device)
         self.L = _b.lib()
         h = self.ctx._h
@@ -177,17 +178,22 @@ class DeviceBackend:
             ("ph0b_shard_sample", C.c_int, [vp, u64, vp]),
             ("ph0b_shard_partition", C.c_int, [vp, vp, u32, vp, C.POINTER(vp), C.POINTER(vp), vp, vp, vp]),
             ("ph0b_shard_recv", C.c_int, [vp, u64, C.POINTER(vp), C.POINTER(vp)]),
-            ("ph0b_shard_sort_unique", C.c_int, [vp, u64, u64, u64, vp, u64p, C.POINTER(vp)]),
+            ("ph0b_shard_sort_unique", C.c_int, [vp, u64, u64, u64, vp, u64p, C.POINTER(vp),
+                                                 C.POINTER(C.c_uint32)]),
             ("ph0b_shard_reduce", C.c_int, [vp, u64, u64, u64, vp, u64p, C.POINTER(vp), C.POINTER(vp), C.POINTER(vp)]),
             ("ph0b_reduce_columns", C.c_int, [vp, vp, u64, u64, vp, vp, u64p]),
         ]:
             fn = getattr(L, name)
             fn.restype, fn.argtypes = res, args
 
+    def _count(self):
+        self.launches += int(self.L.ph0b_last_launch_count())
+
     def distances(self, x_ptr, n, d, u_lo, u_hi, layout=_b.COL_MAJOR):
         cnt, lo, hi = C.c_uint64(), C.c_uint64(), C.c_uint64()
         _b._check(self.L.ph0b_shard_distances(self.h, C.c_void_p(x_ptr), n, d, layout, u_lo, u_hi,
                                               None, C.byref(cnt), C.byref(lo), C.byref(hi)))
+        self._count()
         return cnt.value, lo.value, hi.value
 
     def sample(self, s, count):
@@ -207,6 +213,7 @@ class DeviceBackend:
             self.h, C.c_void_p(spl.ctypes.data) if spl.size else None, parts, None, C.byref(kp),
             C.byref(vp_), C.c_void_p(counts.ctypes.data), C.c_void_p(pmin.ctypes.data),
             C.c_void_p(pmax.ctypes.data)))
+        self._count()
         total = int(counts.sum())
         return (_dev_view(kp.value, total, "<i8", self.device),
                 _dev_view(vp_.value, total, "<i4", self.device), counts, pmin, pmax)
@@ -218,15 +225,20 @@ class DeviceBackend:
                 _dev_view(vp_.value, count, "<i4", self.device))
 
     def sort_unique(self, count, kmin, kmax):
-        nd, sp = C.c_uint64(), C.c_void_p()
+        import time
+        nd, sp, ps = C.c_uint64(), C.c_void_p(), C.c_uint32()
+        t0 = time.perf_counter()
         _b._check(self.L.ph0b_shard_sort_unique(self.h, count, kmin, kmax, None, C.byref(nd),
-                                                C.byref(sp)))
+                                                C.byref(sp), C.byref(ps)))
+        self.last_sort = (time.perf_counter() - t0, int(ps.value), int(count))
+        self._count()
         return nd.value, _dev_view(sp.value, nd.value, "<f8", self.device)
 
     def reduce(self, n, count, grade_offset):
         m, up, gp, lp = C.c_uint64(), C.c_void_p(), C.c_void_p(), C.c_void_p()
         _b._check(self.L.ph0b_shard_reduce(self.h, n, count, grade_offset, None, C.byref(m),
                                            C.byref(up), C.byref(gp), C.byref(lp)))
+        self._count()
         m = m.value
         uv = _dev_view(up.value, m, "<i4", self.device).cpu().numpy().view(np.uint32)
         g = _dev_view(gp.value, m, "<i8", self.device).cpu().numpy().view(np.uint64)
@@ -241,6 +253,7 @@ class DeviceBackend:
         cnt = C.c_uint64()
         _b._check(self.L.ph0b_reduce_columns(self.h, C.c_void_p(uv_dev.data_ptr()), len(uv), n,
                                               None, C.c_void_p(idx.ctypes.data), C.byref(cnt)))
+        self._count()
         return idx[: cnt.value].copy()
 
     def close(self):
