@@ -73,8 +73,10 @@ struct UniqueArgs {
     uint64_t* n_scale;      // out: |D| (device)
     uint32_t epoch;
     uint32_t* redo;         // out: set when a run exceeded the in-place fix-up limit
+    uint64_t* scratch;      // unique_scratch_words(count) words
 };
 int launch_unique(const UniqueArgs& a, cudaStream_t s);
+uint64_t unique_scratch_words(uint64_t count);
 
 // ---- K4: GPU column reduction (reduce.cu) ----------------------------------------------
 struct ReduceState {

@@ -74,7 +74,7 @@ Context::~Context() {
     void* ps[] = {xin_,  xpad_, keys_[0], keys_[1], vals_[0], vals_[1], status_,
                   grade_, comp_, best_, surv_, surv_sorted_, lows_, cand_[0], cand_[1],
                   survkeys_[0], survkeys_[1], death_grade_, death_length_, hist_, counters_,
-                  small_};
+                  small_, uscratch_};
     for (void* p : ps)
         if (p) cudaFree(p);
     if (h_small_) cudaFreeHost(h_small_);
@@ -325,9 +325,12 @@ Status Context::stage_sort_unique(uint64_t k, uint64_t kmin, uint64_t kmax, bool
         scale_ = reinterpret_cast<double*>(keys_[cur_ ^ 1]);
         uint32_t* redo = reinterpret_cast<uint32_t*>(small_ + 4);
         PH0B_TRY(cudaMemsetAsync(redo, 0, 4, st), "memset");
+        Status gs = grow(reinterpret_cast<void**>(&uscratch_), &uscratch_cap_,
+                         unique_scratch_words(k) * 8);
+        if (!gs.good()) return gs;
         UniqueArgs ua{keys_[cur_], vals_[cur_], k, kmin, low_bits, scale_,
                       want_grade ? grade_ : nullptr, status_, counters_ + 40, small_ + 2,
-                      next_epochs(1, st), redo};
+                      next_epochs(1, st), redo, uscratch_};
         launches += launch_unique(ua, st);
         PH0B_CHECK_LAUNCH("unique kernel");
         if (low_bits == 0) break;

@@ -115,6 +115,7 @@ private:
     uint64_t* survkeys_[2] = {};   uint64_t survkeys_cap_[2] = {};
     uint64_t* death_grade_ = nullptr; uint64_t death_grade_cap_ = 0;
     double* death_length_ = nullptr;  uint64_t death_length_cap_ = 0;
+    uint64_t* uscratch_ = nullptr; uint64_t uscratch_cap_ = 0;
     // fixed small buffers
     uint32_t* hist_ = nullptr;     // [8][256]
     uint32_t* counters_ = nullptr; // [64]

@@ -14,6 +14,7 @@
 #include <cuda_runtime.h>
 
 #include <cstdint>
+#include <cstdlib>
 
 #include "common.cuh"
 #include "kernels.h"
@@ -23,195 +24,493 @@ namespace {
 
 constexpr int kThreads = 512;
 constexpr int kWarps = kThreads / 32;
-constexpr int kItems = 16;
+constexpr int kItems = 8;
 constexpr int kTileKeys = kThreads * kItems;
 
 constexpr uint32_t kMaxRun = 64;  // longest equal-prefix run fixed up in place
 
-// Stable insertion sort of the run [a, a+len) by full key, in global memory (runs are short:
-// the radix passes ordered by the top 40 bits of the span, so a run is a handful of lengths
-// within one 2^low_bits-ULP cell, already in (u, v) order among themselves).
-__device__ void fix_run(uint64_t* keys, uint32_t* vals, uint64_t a, uint32_t len) {
-    for (uint32_t i = 1; i < len; ++i) {
-        const uint64_t k = keys[a + i];
-        const uint32_t v = vals[a + i];
-        uint32_t j = i;
-        while (j > 0 && keys[a + j - 1] > k) {
-            keys[a + j] = keys[a + j - 1];
-            vals[a + j] = vals[a + j - 1];
-            --j;
-        }
-        keys[a + j] = k;
-        vals[a + j] = v;
-    }
+// Three kernels, no look-back: count the distinct lengths of every tile (fixing the
+// equal-prefix runs of a truncated radix plan in shared memory first), scan the tile counts,
+// then write D and the grades.  Keys are read twice (8 B + 8 B) and D written once (8 B);
+// no CTA ever waits on another.
+constexpr int kExt = (int)kMaxRun + 1;  // extension past the tile end (runs crossing it)
+
+__device__ __forceinline__ bool is_run_start(uint64_t p, uint64_t pprev, uint64_t pnext,
+                                             bool has_prev, bool has_next) {
+    return has_next && pnext == p && !(has_prev && pprev == p);
 }
 
-// low_bits == 0: keys are fully sorted; flag-and-scan unique over the tile.
-// low_bits  > 0: keys are sorted by prefix = (key - kmin) >> low_bits only.  Every run of
-// equal prefix is first sorted by full key (stably) by the tile in which it starts; a tile
-// owns exactly the runs that start in it (its first elements may continue the previous
-// tile's run; its last run may extend past its end).  Runs longer than kMaxRun raise
-// *redo and the caller re-sorts with the full digit plan.
-__global__ void __launch_bounds__(kThreads, 2)
-    k3_unique(uint64_t* __restrict__ keys, uint32_t* __restrict__ vals, uint64_t count,
-              uint64_t kmin, uint32_t low_bits, double* __restrict__ scale,
-              uint32_t* __restrict__ grade, uint64_t* __restrict__ status,
-              uint32_t* tile_counter, uint32_t epoch, uint64_t* n_scale, uint32_t* redo) {
-    __shared__ uint32_t s_tile;
+__global__ void __launch_bounds__(kThreads)
+    k3_count(uint64_t* __restrict__ keys, uint32_t* __restrict__ vals, uint64_t count,
+             uint64_t kmin, uint32_t low_bits, uint32_t* __restrict__ counts,
+             int2* __restrict__ own, uint32_t* redo) {
+    extern __shared__ __align__(16) uint64_t u_dyn[];
+    uint64_t* s_k = u_dyn;                                              // [kTileKeys + kExt]
     __shared__ uint32_t s_warp_tot[kWarps];
-    __shared__ uint32_t s_prefix;
-    __shared__ uint64_t s_own[2];
-    __shared__ uint32_t s_ext_tot;
-    __shared__ int s_fixed;
+    __shared__ int s_own[2];
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-    if (tid == 0) {
-        s_tile = atomicAdd(tile_counter, 1u);
-        s_fixed = 0;
-    }
-    __syncthreads();
-    const uint32_t tile = s_tile;
-    const uint64_t tile_start = (uint64_t)tile * kTileKeys;
+    const uint64_t tile_start = (uint64_t)blockIdx.x * kTileKeys;
     const uint64_t tile_end = tile_start + kTileKeys < count ? tile_start + kTileKeys : count;
     const uint64_t wbase = tile_start + (uint64_t)warp * (32 * kItems) + lane;
     auto pre = [&](uint64_t kk) { return (kk - kmin) >> low_bits; };
 
-    uint64_t k[kItems];
+    if (low_bits == 0) {
+        uint64_t k[kItems];
 #pragma unroll
-    for (int i = 0; i < kItems; ++i) {
-        const uint64_t idx = wbase + 32 * i;
-        k[i] = idx < tile_end ? keys[idx] : 0ull;
-    }
-
-    uint64_t own_start = tile_start, own_end = tile_end;
-    if (low_bits) {
-        // ---- phase A: sort the equal-prefix runs that start in this tile ----------------
-        bool fixed = false;
+        for (int i = 0; i < kItems; ++i) {  // all loads in flight before any use
+            const uint64_t idx = wbase + 32 * i;
+            k[i] = idx < tile_end ? keys[idx] : 0ull;
+        }
+        const uint64_t k_before = (lane == 0 && wbase > 0) ? keys[wbase - 1] : 0ull;
+        uint32_t total = 0;
 #pragma unroll
         for (int i = 0; i < kItems; ++i) {
             const uint64_t idx = wbase + 32 * i;
             uint64_t prev = __shfl_up_sync(0xffffffffu, k[i], 1);
-            uint64_t next = __shfl_down_sync(0xffffffffu, k[i], 1);
-            if (lane == 0 && idx > 0 && idx < tile_end) prev = keys[idx - 1];
-            if (lane == 31 && idx + 1 < count && idx < tile_end) next = keys[idx + 1];
-            if (idx + 1 >= count || idx >= tile_end) continue;
-            const uint64_t p = pre(k[i]);
-            if (pre(next) != p || (idx > 0 && pre(prev) == p)) continue;  // not a run start
-            uint32_t len = 2;
-            while (idx + len < count && len <= kMaxRun && pre(keys[idx + len]) == p) ++len;
-            if (len > kMaxRun) {
-                atomicOr(redo, 1u);
-                continue;
-            }
-            fix_run(keys, vals, idx, len);
-            fixed = true;
+            const uint64_t last = __shfl_sync(0xffffffffu, i ? k[i - 1] : 0ull, 31);
+            if (lane == 0) prev = i ? last : k_before;
+            total += __popc(__ballot_sync(0xffffffffu, idx < tile_end && (idx == 0 || k[i] != prev)));
         }
-        if (__syncthreads_or(fixed)) {
-#pragma unroll
-            for (int i = 0; i < kItems; ++i) {  // re-read the (partly) re-ordered tile
-                const uint64_t idx = wbase + 32 * i;
-                k[i] = idx < tile_end ? keys[idx] : 0ull;
-            }
-        }
-        if (tid == 0) {
-            // skip the continuation of a run owned by an earlier tile
-            uint64_t st = tile_start;
-            if (st > 0) {
-                const uint64_t p0 = pre(keys[st - 1]);
-                while (st < tile_end && st < tile_start + kMaxRun + 1 && pre(keys[st]) == p0) ++st;
-            }
-            // extend through the run that crosses the tile end
-            uint64_t e = tile_end;
-            if (e < count && e > st) {
-                const uint64_t pl = pre(keys[e - 1]);
-                while (e < count && e < tile_end + kMaxRun + 1 && pre(keys[e]) == pl) ++e;
-            }
-            if (st >= tile_end) st = e = tile_end;  // the whole tile continues an earlier run
-            s_own[0] = st;
-            s_own[1] = e;
-            uint32_t ext = 0;  // distinct values in the extension [tile_end, e)
-            for (uint64_t g = tile_end; g < e; ++g) ext += keys[g] != keys[g - 1] ? 1u : 0u;
-            s_ext_tot = ext;
-        }
+        if (lane == 0) s_warp_tot[warp] = total;
         __syncthreads();
-        own_start = s_own[0];
-        own_end = s_own[1];
+        if (tid == 0) {
+            uint32_t t = 0;
+            for (int w = 0; w < kWarps; ++w) t += s_warp_tot[w];
+            counts[blockIdx.x] = t;
+            own[blockIdx.x] = make_int2(0, (int)(tile_end - tile_start));
+        }
+        return;
     }
 
-    // ---- phase B: flags, counts, look-back, D -------------------------------------------
+    // ---- stage the tile (+ extension) in shared memory ------------------------------------
+    const uint64_t ext_end = tile_end + kExt < count ? tile_end + kExt : count;
+    const uint32_t staged = (uint32_t)(ext_end - tile_start);
+    {
+        uint64_t t[kItems];
+#pragma unroll
+        for (int i = 0; i < kItems; ++i) {  // all loads in flight before any store
+            const uint32_t j = i * kThreads + tid;
+            t[i] = j < staged ? keys[tile_start + j] : 0ull;
+        }
+#pragma unroll
+        for (int i = 0; i < kItems; ++i) {
+            const uint32_t j = i * kThreads + tid;
+            if (j < staged) s_k[j] = t[i];
+        }
+        if (tid < kExt && kTileKeys + tid < staged) s_k[kTileKeys + tid] = keys[tile_start + kTileKeys + tid];
+    }
+    __syncthreads();
+    const uint64_t p_before = tile_start > 0 ? pre(keys[tile_start - 1]) : 0ull;
+
+    // ---- phase A: fix the runs that start in this tile (stable insertion sort, smem) -----
+    for (uint32_t i = tid; i < (uint32_t)(tile_end - tile_start); i += kThreads) {
+        const uint64_t g = tile_start + i;
+        if (g + 1 >= count) continue;
+        const uint64_t p = pre(s_k[i]);
+        const bool has_prev = g > 0;
+        const uint64_t pp = i > 0 ? pre(s_k[i - 1]) : p_before;
+        if (!is_run_start(p, pp, i + 1 < staged ? pre(s_k[i + 1]) : ~p, has_prev, i + 1 < staged))
+            continue;
+        uint32_t len = 2;
+        while (i + len < staged && len <= kMaxRun && pre(s_k[i + len]) == p) ++len;
+        if (len > kMaxRun || (i + len == staged && ext_end < count)) {
+            atomicOr(redo, 1u);  // too long to fix here: the caller re-sorts every digit
+            continue;
+        }
+        bool sorted = true;
+        for (uint32_t a = 1; a < len; ++a) sorted = sorted && s_k[i + a - 1] <= s_k[i + a];
+        if (sorted) continue;  // already in (length, u, v) order
+        // stable insertion sort of keys (shared) and their columns (global, rare)
+        for (uint32_t a = 1; a < len; ++a) {
+            const uint64_t k = s_k[i + a];
+            const uint32_t v = vals[g + a];
+            uint32_t j = a;
+            while (j > 0 && s_k[i + j - 1] > k) {
+                s_k[i + j] = s_k[i + j - 1];
+                vals[g + j] = vals[g + j - 1];
+                --j;
+            }
+            s_k[i + j] = k;
+            vals[g + j] = v;
+        }
+        for (uint32_t a = 0; a < len; ++a) keys[g + a] = s_k[i + a];
+    }
+    __syncthreads();
+
+    // ---- ownership: skip a run continuing from the previous tile; extend through the run
+    // that crosses the tile end ---------------------------------------------------------------
+    if (tid == 0) {
+        uint32_t st = 0;
+        if (tile_start > 0)
+            while (st < (uint32_t)(tile_end - tile_start) && pre(s_k[st]) == p_before) ++st;
+        uint32_t e = (uint32_t)(tile_end - tile_start);
+        if (e > st && e < staged) {
+            const uint64_t pl = pre(s_k[e - 1]);
+            while (e < staged && pre(s_k[e]) == pl) ++e;
+        }
+        if (st >= (uint32_t)(tile_end - tile_start)) st = e = (uint32_t)(tile_end - tile_start);
+        s_own[0] = (int)st;
+        s_own[1] = (int)e;
+    }
+    __syncthreads();
+    const uint32_t os = (uint32_t)s_own[0], oe = (uint32_t)s_own[1];
+    uint32_t total = 0;
+    for (uint32_t i0 = 0; i0 < oe; i0 += kThreads) {
+        const uint32_t i = i0 + tid;
+        const bool f = i >= os && i < oe &&
+                       (tile_start + i == 0 || (i > 0 ? s_k[i] != s_k[i - 1]
+                                                      : s_k[0] != keys[tile_start - 1]));
+        total += __popc(__ballot_sync(0xffffffffu, f));
+    }
+    if (lane == 0) s_warp_tot[warp] = total;
+    __syncthreads();
+    if (tid == 0) {
+        uint32_t t = 0;
+        for (int w = 0; w < kWarps; ++w) t += s_warp_tot[w];
+        counts[blockIdx.x] = t;
+        own[blockIdx.x] = make_int2((int)os, (int)oe);
+    }
+}
+
+__global__ void k3_scan(const uint32_t* __restrict__ counts, uint32_t tiles,
+                        uint64_t* __restrict__ offsets, uint64_t* n_scale) {
+    __shared__ uint64_t s_carry;
+    __shared__ uint64_t s_warp[32];
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+    if (threadIdx.x == 0) s_carry = 0;
+    __syncthreads();
+    for (uint32_t t0 = 0; t0 < tiles; t0 += blockDim.x) {
+        const uint32_t t = t0 + threadIdx.x;
+        const uint64_t x = t < tiles ? counts[t] : 0u;
+        uint64_t inc = x;
+        for (int o = 1; o < 32; o <<= 1) {
+            const uint64_t y = __shfl_up_sync(0xffffffffu, inc, o);
+            if (lane >= o) inc += y;
+        }
+        if (lane == 31) s_warp[warp] = inc;
+        __syncthreads();
+        uint64_t wb = 0, tot = 0;
+        for (int w = 0; w < nw; ++w) {
+            wb += w < warp ? s_warp[w] : 0u;
+            tot += s_warp[w];
+        }
+        const uint64_t carry = s_carry;
+        if (t < tiles) offsets[t] = carry + wb + inc - x;
+        __syncthreads();
+        if (threadIdx.x == 0) s_carry = carry + tot;
+        __syncthreads();
+    }
+    if (threadIdx.x == 0) *n_scale = s_carry;
+}
+
+__global__ void __launch_bounds__(kThreads)
+    k3_write(const uint64_t* __restrict__ keys, uint64_t count, const int2* __restrict__ own,
+             const uint64_t* __restrict__ offsets, double* __restrict__ scale,
+             uint32_t* __restrict__ grade) {
+    __shared__ uint32_t s_warp_tot[kWarps];
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const uint64_t tile_start = (uint64_t)blockIdx.x * kTileKeys;
+    const uint64_t tile_end = tile_start + kTileKeys < count ? tile_start + kTileKeys : count;
+    const int2 ow = own[blockIdx.x];
+    const uint64_t own_start = tile_start + (uint64_t)ow.x, own_end = tile_start + (uint64_t)ow.y;
+    const uint64_t wbase = tile_start + (uint64_t)warp * (32 * kItems) + lane;
+    uint64_t k[kItems];
     uint32_t ball[kItems];
     uint32_t total = 0;
+#pragma unroll
+    for (int i = 0; i < kItems; ++i) {  // all loads in flight before any use
+        const uint64_t idx = wbase + 32 * i;
+        k[i] = idx < tile_end ? keys[idx] : 0ull;
+    }
+    const uint64_t k_before = (lane == 0 && wbase > 0) ? keys[wbase - 1] : 0ull;
 #pragma unroll
     for (int i = 0; i < kItems; ++i) {
         const uint64_t idx = wbase + 32 * i;
         const bool valid = idx < tile_end;
         uint64_t prev = __shfl_up_sync(0xffffffffu, k[i], 1);
-        if (lane == 0 && valid && idx > 0) prev = keys[idx - 1];
+        const uint64_t last = __shfl_sync(0xffffffffu, i ? k[i - 1] : 0ull, 31);
+        if (lane == 0) prev = i ? last : k_before;
         const bool owned = valid && idx >= own_start && idx < own_end;
-        const bool flag = owned && (idx == 0 || k[i] != prev);
-        ball[i] = __ballot_sync(0xffffffffu, flag);
+        ball[i] = __ballot_sync(0xffffffffu, owned && (idx == 0 || k[i] != prev));
         total += __popc(ball[i]);
     }
     if (lane == 0) s_warp_tot[warp] = total;
     __syncthreads();
-    uint32_t warp_base = 0, tile_tot = 0;
+    uint32_t warp_base = 0, main_tot = 0;
 #pragma unroll
     for (int w = 0; w < kWarps; ++w) {
         warp_base += (w < warp) ? s_warp_tot[w] : 0u;
-        tile_tot += s_warp_tot[w];
+        main_tot += s_warp_tot[w];
     }
-    const uint32_t main_tot = tile_tot;
-    if (low_bits) tile_tot += s_ext_tot;
-    if (tid == 0) {
-        uint64_t* my = status + tile;
-        uint32_t excl = 0;
-        if (tile == 0) {
-            st_relaxed_u64(my, pack_status(kStateInclusive, epoch, tile_tot));
-        } else {
-            st_relaxed_u64(my, pack_status(kStateAggregate, epoch, tile_tot));
-            excl = lookback_window<8>(status, 1, tile, epoch);
-            st_relaxed_u64(my, pack_status(kStateInclusive, epoch, excl + tile_tot));
-        }
-        s_prefix = excl;
-        const uint64_t tiles = (count + kTileKeys - 1) / kTileKeys;
-        if (tile == tiles - 1) *n_scale = (uint64_t)excl + tile_tot;
-        // the extension: elements past the tile end that belong to this tile's last run
-        if (low_bits) {
-            uint32_t r = excl + main_tot;
-            for (uint64_t g = tile_end; g < own_end; ++g) {
-                const bool f = keys[g] != keys[g - 1];
-                if (f) scale[r] = __longlong_as_double((long long)keys[g]);
-                r += f ? 1u : 0u;
-                if (grade) grade[g] = r;
-            }
-        }
-    }
-    __syncthreads();
-    uint32_t run = s_prefix + warp_base;
+    const uint64_t base = offsets[blockIdx.x];
+    uint64_t run = base + warp_base;
     const uint32_t lt = lanemask_lt();
 #pragma unroll
     for (int i = 0; i < kItems; ++i) {
         const uint64_t idx = wbase + 32 * i;
         const bool flag = (ball[i] >> lane) & 1u;
-        const uint32_t before = run + __popc(ball[i] & lt);  // flags strictly before idx
+        const uint64_t before = run + __popc(ball[i] & lt);  // flags strictly before idx
         if (flag) scale[before] = __longlong_as_double((long long)k[i]);
-        if (grade && idx >= own_start && idx < own_end) grade[idx] = before + (flag ? 1u : 0u);
+        if (grade && idx >= own_start && idx < own_end)
+            grade[idx] = (uint32_t)(before + (flag ? 1u : 0u));
         run += __popc(ball[i]);
+    }
+    // the extension: elements past the tile end that belong to this tile's last run
+    if (tid == 0 && own_end > tile_end) {
+        uint64_t r = base + main_tot;
+        for (uint64_t g = tile_end; g < own_end; ++g) {
+            const bool f = keys[g] != keys[g - 1];
+            if (f) scale[r] = __longlong_as_double((long long)keys[g]);
+            r += f ? 1u : 0u;
+            if (grade) grade[g] = (uint32_t)r;
+        }
     }
 }
 
 }  // namespace
+
+// ---- persistent single-pass unique (default) ---------------------------------------------
+// Static tile order over co-resident CTAs (deadlock-free look-back), the next tile's keys
+// (+ the kMaxRun extension) prefetched with a TMA bulk copy while this tile is fixed up,
+// counted, looked back and written.  One read of the keys, one write of D.
+__device__ __forceinline__ uint32_t u_smem(const void* p) {
+    return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+
+constexpr int kUT = 4096;  // keys per tile
+constexpr int kUThreads = 512;
+constexpr int kUWarps = kUThreads / 32;
+constexpr int kUItems = kUT / kUThreads;
+constexpr int kUStage = kUT + 72;  // tile + extension (>= kExt), 16 B multiple
+
+__global__ void __launch_bounds__(kUThreads, 3)
+    k3_unique_p(uint64_t* __restrict__ keys, uint32_t* __restrict__ vals, uint64_t count,
+                uint64_t kmin, uint32_t low_bits, double* __restrict__ scale,
+                uint32_t* __restrict__ grade, uint64_t* __restrict__ status, uint32_t epoch,
+                uint64_t* n_scale, uint32_t* redo, uint32_t num_tiles) {
+    extern __shared__ __align__(128) uint64_t up_dyn[];
+    __shared__ __align__(8) uint64_t s_bar[2];
+    __shared__ uint32_t s_warp_tot[kUWarps];
+    __shared__ int s_own[2];
+    __shared__ uint32_t s_ext_tot;
+    __shared__ uint64_t s_prefix;
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    auto pre = [&](uint64_t kk) { return (kk - kmin) >> low_bits; };
+    if (tid == 0) {
+        asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(u_smem(&s_bar[0])));
+        asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(u_smem(&s_bar[1])));
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    __syncthreads();
+    auto issue = [&](uint32_t tl, int b) {
+        const uint64_t b0 = (uint64_t)tl * kUT;
+        const uint64_t n = count - b0 < (uint64_t)kUStage ? count - b0 : (uint64_t)kUStage;
+        const uint32_t bytes = (uint32_t)((n * 8 + 15) & ~15ull);
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+        asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(
+                         u_smem(&s_bar[b])),
+                     "r"(bytes)
+                     : "memory");
+        asm volatile(
+            "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, "
+            "[%3];" ::"r"(u_smem(up_dyn + b * kUStage)),
+            "l"(keys + b0), "r"(bytes), "r"(u_smem(&s_bar[b]))
+            : "memory");
+    };
+    uint32_t tile = blockIdx.x;
+    if (tid == 0 && tile < num_tiles) issue(tile, 0);
+    uint32_t phase[2] = {0, 0};
+    int b = 0;
+    for (; tile < num_tiles; tile += gridDim.x, b ^= 1) {
+        uint64_t* s_k = up_dyn + b * kUStage;
+        const uint64_t tile_start = (uint64_t)tile * kUT;
+        const uint64_t tile_end = tile_start + kUT < count ? tile_start + kUT : count;
+        const uint32_t tn = (uint32_t)(tile_end - tile_start);
+        const uint64_t ext_end = tile_end + kExt < count ? tile_end + kExt : count;
+        const uint32_t staged = (uint32_t)(ext_end - tile_start);
+        {
+            const uint32_t par = phase[b];
+            asm volatile(
+                "{\n\t.reg .pred p;\n"
+                "UW_%=:\n\t"
+                "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
+                "@!p bra UW_%=;\n}" ::"r"(u_smem(&s_bar[b])),
+                "r"(par)
+                : "memory");
+            phase[b] ^= 1u;
+        }
+        __syncthreads();  // everyone is done with the other buffer: prefetch into it
+        const uint32_t next = tile + gridDim.x;
+        if (tid == 0 && next < num_tiles) issue(next, b ^ 1);
+        const uint64_t k_before = tile_start > 0 ? keys[tile_start - 1] : 0ull;
+
+        uint32_t os = 0, oe = tn;
+        if (low_bits) {
+            // ---- fix the equal-prefix runs that start in this tile (stable, in smem) -----
+            const uint64_t p_before = pre(k_before);
+            for (uint32_t i = tid; i < tn; i += kUThreads) {
+                const uint64_t g = tile_start + i;
+                if (g + 1 >= count || i + 1 >= staged) continue;
+                const uint64_t p = pre(s_k[i]);
+                if (pre(s_k[i + 1]) != p) continue;
+                if (g > 0 && (i > 0 ? pre(s_k[i - 1]) : p_before) == p) continue;
+                uint32_t len = 2;
+                while (i + len < staged && len <= kMaxRun && pre(s_k[i + len]) == p) ++len;
+                if (len > kMaxRun || (i + len == staged && ext_end < count)) {
+                    atomicOr(redo, 1u);
+                    continue;
+                }
+                bool sorted = true;
+                for (uint32_t a = 1; a < len; ++a) sorted = sorted && s_k[i + a - 1] <= s_k[i + a];
+                if (sorted) continue;
+                for (uint32_t a = 1; a < len; ++a) {
+                    const uint64_t kk = s_k[i + a];
+                    const uint32_t v = vals[g + a];
+                    uint32_t j = a;
+                    while (j > 0 && s_k[i + j - 1] > kk) {
+                        s_k[i + j] = s_k[i + j - 1];
+                        vals[g + j] = vals[g + j - 1];
+                        --j;
+                    }
+                    s_k[i + j] = kk;
+                    vals[g + j] = v;
+                }
+                for (uint32_t a = 0; a < len; ++a) keys[g + a] = s_k[i + a];
+            }
+            __syncthreads();
+            if (tid == 0) {
+                uint32_t st = 0;
+                if (tile_start > 0)
+                    while (st < tn && pre(s_k[st]) == p_before) ++st;
+                uint32_t e = tn;
+                if (e > st && e < staged) {
+                    const uint64_t pl = pre(s_k[e - 1]);
+                    while (e < staged && pre(s_k[e]) == pl) ++e;
+                }
+                if (st >= tn) st = e = tn;
+                uint32_t ext = 0;
+                for (uint32_t g = tn; g < e; ++g) ext += s_k[g] != s_k[g - 1] ? 1u : 0u;
+                s_own[0] = (int)st;
+                s_own[1] = (int)e;
+                s_ext_tot = ext;
+            }
+            __syncthreads();
+            os = (uint32_t)s_own[0];
+            oe = (uint32_t)s_own[1];
+        }
+
+        // ---- flags and counts (keys from shared memory) ------------------------------------
+        uint32_t ball[kUItems];
+        uint32_t total = 0;
+        const uint32_t wofs = warp * (32 * kUItems) + lane;
+#pragma unroll
+        for (int i = 0; i < kUItems; ++i) {
+            const uint32_t pos = wofs + 32 * i;
+            const bool owned = pos < tn && pos >= os && pos < oe;
+            const uint64_t prev = pos > 0 ? s_k[pos - 1] : k_before;
+            const bool f = owned && (tile_start + pos == 0 || s_k[pos] != prev);
+            ball[i] = __ballot_sync(0xffffffffu, f);
+            total += __popc(ball[i]);
+        }
+        if (lane == 0) s_warp_tot[warp] = total;
+        __syncthreads();
+        uint32_t warp_base = 0, main_tot = 0;
+#pragma unroll
+        for (int w = 0; w < kUWarps; ++w) {
+            warp_base += (w < warp) ? s_warp_tot[w] : 0u;
+            main_tot += s_warp_tot[w];
+        }
+        const uint32_t tile_tot = main_tot + (low_bits ? s_ext_tot : 0u);
+        if (tid == 0) {
+            uint64_t* my = status + tile;
+            uint32_t excl = 0;
+            if (tile == 0) {
+                st_relaxed_u64(my, pack_status(kStateInclusive, epoch, tile_tot));
+            } else {
+                st_relaxed_u64(my, pack_status(kStateAggregate, epoch, tile_tot));
+                excl = lookback_window<8>(status, 1, tile, epoch);
+                st_relaxed_u64(my, pack_status(kStateInclusive, epoch, excl + tile_tot));
+            }
+            s_prefix = excl;
+            if (tile == num_tiles - 1) *n_scale = (uint64_t)excl + tile_tot;
+        }
+        __syncthreads();
+        const uint64_t base = s_prefix;
+        uint64_t run = base + warp_base;
+        const uint32_t lt = lanemask_lt();
+#pragma unroll
+        for (int i = 0; i < kUItems; ++i) {
+            const uint32_t pos = wofs + 32 * i;
+            const bool flag = (ball[i] >> lane) & 1u;
+            const uint64_t before = run + __popc(ball[i] & lt);
+            if (flag) scale[before] = __longlong_as_double((long long)s_k[pos]);
+            if (grade && pos < tn && pos >= os && pos < oe)
+                grade[tile_start + pos] = (uint32_t)(before + (flag ? 1u : 0u));
+            run += __popc(ball[i]);
+        }
+        if (low_bits && tid == 0 && oe > tn) {  // the extension of this tile's last run
+            uint64_t r = base + main_tot;
+            for (uint32_t g = tn; g < oe; ++g) {
+                const bool f = s_k[g] != s_k[g - 1];
+                if (f) scale[r] = __longlong_as_double((long long)s_k[g]);
+                r += f ? 1u : 0u;
+                if (grade) grade[tile_start + g] = (uint32_t)r;
+            }
+        }
+    }
+}
+
+uint64_t unique_scratch_words(uint64_t count) {
+    const uint64_t tiles = (count + kTileKeys - 1) / kTileKeys;
+    return (tiles + 1) / 2 + 1 + 2 * (tiles + 1) + 1;
+}
 
 int launch_unique(const UniqueArgs& a, cudaStream_t s) {
     if (a.count == 0) {
         cudaMemsetAsync(a.n_scale, 0, sizeof(uint64_t), s);
         return 0;
     }
+    static const bool three_kernels = [] {
+        const char* e = getenv("PH0B_UNIQUE");
+        return e && e[0] == '3';
+    }();
+    if (!three_kernels) {
+        const size_t smem = (size_t)2 * kUStage * 8;
+        static int per_sm = 0;
+        static int num_sms = 0;
+        if (!per_sm) {
+            cudaFuncSetAttribute(k3_unique_p, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+            cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k3_unique_p, kUThreads, smem);
+            if (per_sm < 1) per_sm = 1;
+            int dev = 0;
+            cudaGetDevice(&dev);
+            cudaDeviceGetAttribute(&num_sms, cudaDevAttrMultiProcessorCount, dev);
+        }
+        const uint64_t tiles = (a.count + kUT - 1) / kUT;
+        uint64_t grid = (uint64_t)num_sms * per_sm;
+        if (grid > tiles) grid = tiles;
+        k3_unique_p<<<(unsigned)grid, kUThreads, smem, s>>>(
+            a.keys, a.vals, a.count, a.kmin, a.low_bits, a.scale, a.grade, a.status, a.epoch,
+            a.n_scale, a.redo, (uint32_t)tiles);
+        return 1;
+    }
     const uint64_t tiles = (a.count + kTileKeys - 1) / kTileKeys;
-    cudaMemsetAsync(a.tile_counter, 0, sizeof(uint32_t), s);
-    k3_unique<<<(unsigned)tiles, kThreads, 0, s>>>(a.keys, a.vals, a.count, a.kmin, a.low_bits,
-                                                   a.scale, a.grade, a.status, a.tile_counter,
-                                                   a.epoch, a.n_scale, a.redo);
-    return 1;
+    // scratch: counts (u32) | own (int2) | offsets (u64), unique_scratch_words(count) words
+    uint32_t* counts = reinterpret_cast<uint32_t*>(a.scratch);
+    int2* own = reinterpret_cast<int2*>(a.scratch + (tiles + 1) / 2 + 1);
+    uint64_t* offsets = a.scratch + (tiles + 1) / 2 + 1 + tiles + 1;
+    const size_t smem = a.low_bits ? (size_t)(kTileKeys + kExt) * 8 : 0;
+    static bool configured = false;
+    if (!configured) {
+        cudaFuncSetAttribute(k3_count, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             (kTileKeys + kExt) * 8);
+        configured = true;
+    }
+    k3_count<<<(unsigned)tiles, kThreads, smem, s>>>(a.keys, a.vals, a.count, a.kmin, a.low_bits,
+                                                    counts, own, a.redo);
+    k3_scan<<<1, 1024, 0, s>>>(counts, (uint32_t)tiles, offsets, a.n_scale);
+    k3_write<<<(unsigned)tiles, kThreads, 0, s>>>(a.keys, a.count, own, offsets, a.scale, a.grade);
+    return 3;
 }
 
 }  // namespace ph0b
