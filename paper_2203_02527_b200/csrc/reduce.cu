@@ -45,9 +45,11 @@ constexpr int kCntSurv = 1;      // surviving columns found so far
 constexpr int kCntHooks = 2;     // hooks made by the last resolve round
 constexpr int kCntOverflow = 3;  // filter exceeded the candidate capacity
 
-__global__ void k4_init(uint32_t* comp, uint32_t* best, uint32_t* par, uint32_t n) {
+__global__ void k4_init(uint32_t* comp, uint32_t* best, uint32_t* par, uint32_t n,
+                        uint16_t* comp16) {
     for (uint32_t v = blockIdx.x * blockDim.x + threadIdx.x; v < n; v += gridDim.x * blockDim.x) {
         comp[v] = v;
+        comp16[v] = (uint16_t)v;
         par[v] = v;
         best[v] = kNone;
     }
@@ -83,6 +85,64 @@ __global__ void __launch_bounds__(kThreads)
                     counters[kCntOverflow] = 1;
             }
         }
+    }
+}
+
+// Clearing filter over a window of the filtration with 8 columns per thread (two 16-byte
+// loads, 16 independent label gathers from a 128 KB u16 label copy that stays in L1).
+__global__ void __launch_bounds__(kThreads)
+    k4_filter_range(const uint32_t* __restrict__ uv, uint64_t begin, uint64_t end,
+                    const uint16_t* __restrict__ comp16, uint32_t* __restrict__ out, uint64_t cap,
+                    uint32_t* counters) {
+    const uint32_t lane = threadIdx.x & 31;
+    const uint64_t a0 = begin & ~7ull;  // 8-column (32 B) aligned groups
+    const uint64_t groups = (end - a0 + 7) / 8;
+    const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+    for (uint64_t g0 = (uint64_t)blockIdx.x * blockDim.x; g0 < groups; g0 += stride) {
+        const uint64_t g = g0 + threadIdx.x;
+        uint32_t e[8];
+        uint32_t keep = 0;
+        if (g < groups) {
+            const uint64_t first = a0 + 8 * g;
+            if (first + 8 <= end) {
+                const uint4* p = reinterpret_cast<const uint4*>(uv + first);
+                const uint4 x = __ldg(p), y = __ldg(p + 1);
+                e[0] = x.x; e[1] = x.y; e[2] = x.z; e[3] = x.w;
+                e[4] = y.x; e[5] = y.y; e[6] = y.z; e[7] = y.w;
+            } else {
+#pragma unroll
+                for (int i = 0; i < 8; ++i) e[i] = first + i < end ? __ldg(uv + first + i) : 0u;
+            }
+            uint16_t lu[8], lv[8];
+#pragma unroll
+            for (int i = 0; i < 8; ++i) {
+                lu[i] = __ldg(comp16 + (e[i] >> 16));
+                lv[i] = __ldg(comp16 + (e[i] & 0xFFFFu));
+            }
+#pragma unroll
+            for (int i = 0; i < 8; ++i) {
+                const uint64_t j = a0 + 8 * g + i;
+                if (j >= begin && j < end && lu[i] != lv[i]) keep |= 1u << i;
+            }
+        }
+        const uint32_t c = __popc(keep);
+        uint32_t inc = c;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const uint32_t y = __shfl_up_sync(0xffffffffu, inc, o);
+            if (lane >= o) inc += y;
+        }
+        const uint32_t wtot = __shfl_sync(0xffffffffu, inc, 31);
+        if (wtot == 0) continue;
+        uint32_t slot = 0;
+        if (lane == 31) slot = atomicAdd(&counters[kCntCand], wtot);
+        slot = __shfl_sync(0xffffffffu, slot, 31) + inc - c;
+        if (slot + c > cap) {
+            if (c) counters[kCntOverflow] = 1;
+            continue;
+        }
+        for (int i = 0; i < 8; ++i)
+            if (keep & (1u << i)) out[slot++] = (uint32_t)(a0 + 8 * g + i);
     }
 }
 
@@ -142,9 +202,11 @@ __global__ void k4_jump_roots(uint32_t n, const uint32_t* __restrict__ comp, uin
 }
 
 __global__ void k4_relabel(uint32_t n, uint32_t* comp, const uint32_t* __restrict__ par,
-                           uint32_t* best) {
+                           uint32_t* best, uint16_t* comp16) {
     for (uint32_t v = blockIdx.x * blockDim.x + threadIdx.x; v < n; v += gridDim.x * blockDim.x) {
-        comp[v] = par[comp[v]];
+        const uint32_t c = par[comp[v]];
+        comp[v] = c;
+        comp16[v] = (uint16_t)c;
         best[v] = kNone;
     }
 }
@@ -169,10 +231,11 @@ int run_reduction(ReduceState& st, cudaStream_t s, int num_sms, uint32_t& epoch,
         cudaMemsetAsync(st.counters, 0, sizeof(uint32_t) * 8, s);
         return 0;
     }
-    uint32_t* par = st.best + n;  // best buffer holds [best | par]
+    uint32_t* par = st.best + n;  // best buffer holds [best | par | comp16]
+    uint16_t* comp16 = reinterpret_cast<uint16_t*>(st.best + 2 * n);
     const unsigned gn = grid_for(n, num_sms, 4);
     cudaMemsetAsync(st.counters, 0, sizeof(uint32_t) * 8, s);
-    k4_init<<<gn, kThreads, 0, s>>>(st.comp, st.best, par, n);
+    k4_init<<<gn, kThreads, 0, s>>>(st.comp, st.best, par, n, comp16);
     S.launches += 1;
 
     uint32_t* h = st.host_counters;
@@ -189,8 +252,8 @@ int run_reduction(ReduceState& st, cudaStream_t s, int num_sms, uint32_t& epoch,
         // (i) clearing filter over the window
         cudaMemsetAsync(st.counters + kCntCand, 0, sizeof(uint32_t), s);
         cudaMemsetAsync(st.counters + kCntOverflow, 0, sizeof(uint32_t), s);
-        k4_filter<<<grid_for(end - pos, num_sms), kThreads, 0, s>>>(
-            st.uv, pos, end, nullptr, 0, st.comp, st.cand[0], st.cap, st.counters);
+        k4_filter_range<<<grid_for((end - pos + 7) / 8, num_sms), kThreads, 0, s>>>(
+            st.uv, pos, end, comp16, st.cand[0], st.cap, st.counters);
         S.launches += 1;
         pull();
         if (h[kCntOverflow]) {  // too many live columns in this window: shrink and retry
@@ -210,7 +273,7 @@ int run_reduction(ReduceState& st, cudaStream_t s, int num_sms, uint32_t& epoch,
             k4_hook<<<gn, kThreads, 0, s>>>(n, st.uv, st.comp, st.best, par, st.surv,
                                             st.counters);
             k4_jump_roots<<<gn, kThreads, 0, s>>>(n, st.comp, par);
-            k4_relabel<<<gn, kThreads, 0, s>>>(n, st.comp, par, st.best);
+            k4_relabel<<<gn, kThreads, 0, s>>>(n, st.comp, par, st.best, comp16);
             cudaMemsetAsync(st.counters + kCntCand, 0, sizeof(uint32_t), s);
             k4_filter<<<grid_for(ncand, num_sms), kThreads, 0, s>>>(
                 st.uv, 0, 0, st.cand[cur], ncand, st.comp, st.cand[cur ^ 1], st.cap,
