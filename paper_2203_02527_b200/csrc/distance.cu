@@ -109,7 +109,7 @@ __device__ __forceinline__ void tile_edges(const double* __restrict__ xu_src,
                 vals[e] = (u << 16) | v;
                 kmin = key < kmin ? key : kmin;
                 kmax = key > kmax ? key : kmax;
-                atomicAdd(&sh_hist[key & 0xFFu], 1u);
+                if (sh_hist) atomicAdd(&sh_hist[key & 0xFFu], 1u);
             }
         }
     }
@@ -140,8 +140,9 @@ __device__ __forceinline__ void finish_block(uint64_t kmin, uint64_t kmax, uint3
         if (kmax > *reinterpret_cast<volatile uint64_t*>(&minmax[1]))
             atomicMax(reinterpret_cast<unsigned long long*>(&minmax[1]), kmax);
     }
-    for (int b = threadIdx.x; b < 256; b += kThreads)
-        if (sh_hist[b]) atomicAdd(&hist0[b], sh_hist[b]);
+    if (hist0)
+        for (int b = threadIdx.x; b < 256; b += kThreads)
+            if (sh_hist[b]) atomicAdd(&hist0[b], sh_hist[b]);
 }
 
 // Shared-memory TMA path, d <= 32 (D = 0: runtime d).
@@ -192,7 +193,7 @@ __global__ void __launch_bounds__(kThreads)
         uint32_t bu, bv;
         tile_coords(tile + t0, nb, bu, bv);
         tile_edges<D>(buf[b], buf[b] + tile_elems, kTile, dim, n, bu * kTile, bv * kTile, u_lo,
-                      u_hi, e_off, keys, vals, kmin, kmax, sh_hist);
+                      u_hi, e_off, keys, vals, kmin, kmax, hist0 ? sh_hist : nullptr);
         b ^= 1;
     }
     __syncthreads();
@@ -214,7 +215,8 @@ __global__ void __launch_bounds__(kThreads)
         uint32_t bu, bv;
         tile_coords(tile + t0, nb, bu, bv);
         tile_edges<0>(xpad + bu * kTile, xpad + bv * kTile, ldx, (int)dd, n, bu * kTile,
-                      bv * kTile, u_lo, u_hi, e_off, keys, vals, kmin, kmax, sh_hist);
+                      bv * kTile, u_lo, u_hi, e_off, keys, vals, kmin, kmax,
+                      hist0 ? sh_hist : nullptr);
     }
     __syncthreads();
     finish_block(kmin, kmax, sh_hist, sh_min, sh_max, minmax, hist0);

@@ -255,7 +255,13 @@ Status Context::stage_distances(const double* dX, uint64_t n, uint64_t d, uint32
     launches += launch_pack_points(dX, layout, (uint32_t)n, (uint32_t)d, xpad_, ldx,
                                    reinterpret_cast<uint32_t*>(small_ + 3), st);
     PH0B_CHECK_LAUNCH("pack_points");
-    DistanceArgs da{xpad_, ldx, (uint32_t)n, (uint32_t)d, keys_[0], vals_[0], small_, hist_};
+    // The raw low-byte histogram only serves the first radix pass when the key span fits in
+    // the 5-pass plan (shift 0): small problems.  Large ones count their first (truncated)
+    // digit in a separate pass anyway, so the per-edge shared atomic is skipped there.
+    const uint64_t kedges = row_base(std::min<uint64_t>(u_hi, n), n) - row_base(u_lo, n);
+    hist_valid_ = kedges < (1ull << 24);
+    DistanceArgs da{xpad_, ldx, (uint32_t)n, (uint32_t)d, keys_[0], vals_[0], small_,
+                    hist_valid_ ? hist_ : nullptr};
     da.u_lo = (uint32_t)u_lo;
     da.u_hi = (uint32_t)u_hi;
     da.e_off = u_lo < n ? row_base(u_lo, n) : 0;
@@ -306,7 +312,7 @@ Status Context::stage_sort_unique(uint64_t k, uint64_t kmin, uint64_t kmax, bool
         sa.hist = hist_;
         sa.tile_counter = counters_ + 32;
         sa.epoch_base = next_epochs(plan.passes + 1, st);
-        if (plan.passes > 0 && (plan.shift[0] != 0 || !raw_hist || attempt > 0)) {
+        if (plan.passes > 0 && (plan.shift[0] != 0 || !raw_hist || !hist_valid_ || attempt > 0)) {
             PH0B_TRY(cudaMemsetAsync(hist_, 0, 256 * 4, st), "memset");
             launches += launch_digit_histogram(keys_[src], k, kmin, plan.shift[0], hist_, st,
                                                num_sms_);

@@ -129,6 +129,7 @@ private:
     int surv_sorted_idx_ = 0;  // survkeys_ index holding the sorted survivor ids
     double* scale_ = nullptr;  // D of the last sort_unique stage
     uint64_t xpad_ld_ = 128, xpad_d_ = 0;
+    bool hist_valid_ = false;  // hist_ row 0 holds the raw low-byte histogram of keys_[0]
 };
 
 // Default per-device contexts used by the stateless C entry points.
