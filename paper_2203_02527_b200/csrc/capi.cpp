@@ -30,6 +30,16 @@ int fail(int code, const std::string& msg) {
     return code;
 }
 
+constexpr uint64_t kOverlapEdges = 1ull << 26;
+
+bool overlap_disabled() {
+    static const bool v = [] {
+        const char* e = getenv("PH0B_OVERLAP");
+        return e && e[0] == '0';
+    }();
+    return v;
+}
+
 struct Opts {
     int device = 0;
     uint32_t flags = 0;
@@ -188,10 +198,15 @@ int ph0b_run_host(ph0b_context* ctx, const double* X, uint64_t n, uint64_t d, ui
     std::lock_guard<std::mutex> lk(c->mu);
     cudaStream_t s = stream ? static_cast<cudaStream_t>(stream) : c->own_stream();
     RunOutputs r;
-    Status st = c->run_host_input(X, n, d, layout, s, StopAfter::Barcode, false, &r);
+    const uint64_t k = n * (n - (n > 0)) / 2;
+    // Large clouds returning D: overlap the D2H of D with the sort (key-range buckets).
+    const bool overlap = scale && k >= kOverlapEdges && !overlap_disabled();
+    Status st = overlap ? c->run_host_overlapped(X, n, d, layout, s, scale, scale_capacity, &r)
+                        : c->run_host_input(X, n, d, layout, s, StopAfter::Barcode, false, &r);
     g_last_launches = c->launches;
     if (!st.good()) return fail(st);
-    rc = copy_out(c, r, s, death_grade, death_length, scale, scale_capacity, scale != nullptr);
+    rc = copy_out(c, r, s, death_grade, death_length, scale, scale_capacity,
+                  scale != nullptr && !overlap);
     if (rc) return rc;
     if (n_finite) *n_finite = r.n_finite;
     if (essential_count) *essential_count = r.essential;

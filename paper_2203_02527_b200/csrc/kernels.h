@@ -74,6 +74,7 @@ struct UniqueArgs {
     uint32_t epoch;
     uint32_t* redo;         // out: set when a run exceeded the in-place fix-up limit
     uint64_t* scratch;      // unique_scratch_words(count) words
+    const uint64_t* d_base = nullptr;  // device: D index of this range's first distinct length
 };
 int launch_unique(const UniqueArgs& a, cudaStream_t s);
 uint64_t unique_scratch_words(uint64_t count);
@@ -124,7 +125,7 @@ int launch_claimed_lows(const uint32_t* surv_sorted, uint32_t m, const uint32_t*
 int launch_partition(const uint64_t* keys, const uint32_t* vals, uint64_t count,
                      const uint64_t* d_splitters, uint32_t parts, uint32_t* d_counts_scratch,
                      uint64_t* d_totals, uint64_t* d_bminmax, uint64_t* keys_out,
-                     uint32_t* vals_out, cudaStream_t s);
+                     uint32_t* vals_out, cudaStream_t s, uint32_t align = 1);
 uint64_t partition_scratch_words(uint64_t count, uint32_t parts);
 int launch_sample(const uint64_t* keys, uint64_t count, uint64_t s, uint64_t* out, cudaStream_t st);
 int launch_gather_u32(const uint32_t* src, const uint32_t* idx, uint64_t m, uint32_t* out,

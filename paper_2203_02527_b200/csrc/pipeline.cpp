@@ -6,6 +6,7 @@
 #include <cstring>
 #include <map>
 #include <memory>
+#include <vector>
 
 #include "kernels.h"
 
@@ -74,11 +75,12 @@ Context::~Context() {
     void* ps[] = {xin_,  xpad_, keys_[0], keys_[1], vals_[0], vals_[1], status_,
                   grade_, comp_, best_, surv_, surv_sorted_, lows_, cand_[0], cand_[1],
                   survkeys_[0], survkeys_[1], death_grade_, death_length_, hist_, counters_,
-                  small_, uscratch_};
+                  small_, uscratch_, dbuf_, part_counts_, part_small_};
     for (void* p : ps)
         if (p) cudaFree(p);
     if (h_small_) cudaFreeHost(h_small_);
     if (h_counters_) cudaFreeHost(h_counters_);
+    if (copy_stream_) cudaStreamDestroy(copy_stream_);
     for (auto& e : ev_)
         if (e) cudaEventDestroy(e);
     if (stream_) cudaStreamDestroy(stream_);
@@ -170,9 +172,9 @@ Status Context::reserve(uint64_t n, uint64_t d) {
 
 Status Context::reserve_recv(uint64_t k) {
     Status s;
-    if (!(s = grow(reinterpret_cast<void**>(&keys_[0]), &keys_cap_[0], k * 8 + 256)).good())
+    if (!(s = grow(reinterpret_cast<void**>(&keys_[0]), &keys_cap_[0], k * 8 + 4096)).good())
         return s;
-    return grow(reinterpret_cast<void**>(&vals_[0]), &vals_cap_[0], k * 4 + 256);
+    return grow(reinterpret_cast<void**>(&vals_[0]), &vals_cap_[0], k * 4 + 4096);
 }
 
 Status Context::sort_survivors(uint32_t m, uint64_t count, cudaStream_t st) {
@@ -209,8 +211,8 @@ Status Context::reserve_edges(uint64_t k) {
     const uint64_t cand = std::max<uint64_t>(1, std::min<uint64_t>(k, kCandCap));
     for (int i = 0; i < 2; ++i) {
         // +256 B: the TMA bulk prefetch of the last sort tile rounds its size up to 16 B
-        G(keys_[i], keys_cap_[i], k * 8 + 256);
-        G(vals_[i], vals_cap_[i], k * 4 + 256);
+        G(keys_[i], keys_cap_[i], k * 8 + 4096);  // + bucket padding, TMA size rounding
+        G(vals_[i], vals_cap_[i], k * 4 + 4096);
         G(cand_[i], cand_cap_[i], cand * 4);
     }
     if (status_words * 8 > status_cap_) status_zeroed_ = false;
@@ -280,18 +282,20 @@ Status Context::stage_distances(const double* dX, uint64_t n, uint64_t d, uint32
     return Status::ok();
 }
 
-Status Context::stage_sort_unique(uint64_t k, uint64_t kmin, uint64_t kmax, bool raw_hist,
-                                  bool want_grade, cudaStream_t st, uint32_t* passes) {
-    if (want_grade) {
-        Status s = grow(reinterpret_cast<void**>(&grade_), &grade_cap_, std::max<uint64_t>(4, k * 4));
-        if (!s.good()) return s;
-    }
+Status Context::sort_unique_range(uint64_t* kb0, uint32_t* vb0, uint64_t* kb1, uint32_t* vb1,
+                                  uint64_t k, uint64_t kmin, uint64_t kmax, bool raw_hist,
+                                  double* scale_out, const uint64_t* d_base, uint64_t* d_count,
+                                  uint32_t* grade_out, cudaStream_t st, int* res,
+                                  uint32_t* passes) {
+    uint64_t* kb[2] = {kb0, kb1};
+    uint32_t* vb[2] = {vb0, vb1};
     int src = 0;
-    cur_ = 0;
-    *passes = 0;
+    *res = 0;
     if (k == 0) {
-        PH0B_TRY(cudaMemsetAsync(small_ + 2, 0, 8, st), "memset");
-        scale_ = reinterpret_cast<double*>(keys_[1]);
+        if (d_base)
+            PH0B_TRY(cudaMemcpyAsync(d_count, d_base, 8, cudaMemcpyDeviceToDevice, st), "copy");
+        else
+            PH0B_TRY(cudaMemsetAsync(d_count, 0, 8, st), "memset");
         return Status::ok();
     }
     for (int attempt = 0;; ++attempt) {
@@ -304,17 +308,17 @@ Status Context::stage_sort_unique(uint64_t k, uint64_t kmin, uint64_t kmax, bool
         SortArgs sa{};
         sa.count = k;
         sa.kmin = kmin;
-        sa.keys[0] = keys_[src];
-        sa.keys[1] = keys_[src ^ 1];
-        sa.vals[0] = vals_[src];
-        sa.vals[1] = vals_[src ^ 1];
+        sa.keys[0] = kb[src];
+        sa.keys[1] = kb[src ^ 1];
+        sa.vals[0] = vb[src];
+        sa.vals[1] = vb[src ^ 1];
         sa.status = status_;
         sa.hist = hist_;
         sa.tile_counter = counters_ + 32;
         sa.epoch_base = next_epochs(plan.passes + 1, st);
         if (plan.passes > 0 && (plan.shift[0] != 0 || !raw_hist || !hist_valid_ || attempt > 0)) {
             PH0B_TRY(cudaMemsetAsync(hist_, 0, 256 * 4, st), "memset");
-            launches += launch_digit_histogram(keys_[src], k, kmin, plan.shift[0], hist_, st,
+            launches += launch_digit_histogram(kb[src], k, kmin, plan.shift[0], hist_, st,
                                                num_sms_);
             sa.hist0_rot = 0;
         } else {
@@ -322,29 +326,46 @@ Status Context::stage_sort_unique(uint64_t k, uint64_t kmin, uint64_t kmax, bool
         }
         int sl = 0;
         const int out = launch_sort_passes(sa, plan, st, num_sms_, &sl);
-        cur_ = src ^ out;
+        *res = src ^ out;
         launches += sl;
         PH0B_CHECK_LAUNCH("radix sort");
         PH0B_TRY(cudaEventRecord(ev_[2], st), "event");
         *passes += plan.passes;
 
-        scale_ = reinterpret_cast<double*>(keys_[cur_ ^ 1]);
+        double* scale = scale_out ? scale_out : reinterpret_cast<double*>(kb[*res ^ 1]);
         uint32_t* redo = reinterpret_cast<uint32_t*>(small_ + 4);
         PH0B_TRY(cudaMemsetAsync(redo, 0, 4, st), "memset");
         Status gs = grow(reinterpret_cast<void**>(&uscratch_), &uscratch_cap_,
                          unique_scratch_words(k) * 8);
         if (!gs.good()) return gs;
-        UniqueArgs ua{keys_[cur_], vals_[cur_], k, kmin, low_bits, scale_,
-                      want_grade ? grade_ : nullptr, status_, counters_ + 40, small_ + 2,
-                      next_epochs(1, st), redo, uscratch_};
+        UniqueArgs ua{kb[*res], vb[*res], k, kmin, low_bits, scale, grade_out, status_,
+                      counters_ + 40, d_count, next_epochs(1, st), redo, uscratch_, d_base};
         launches += launch_unique(ua, st);
         PH0B_CHECK_LAUNCH("unique kernel");
         if (low_bits == 0) break;
         PH0B_TRY(cudaMemcpyAsync(h_small_ + 4, small_ + 4, 8, cudaMemcpyDeviceToHost, st), "D2H");
         PH0B_TRY(cudaStreamSynchronize(st), "unique");
         if (static_cast<uint32_t>(h_small_[4]) == 0) break;
-        src = cur_;
+        src = *res;
     }
+    return Status::ok();
+}
+
+Status Context::stage_sort_unique(uint64_t k, uint64_t kmin, uint64_t kmax, bool raw_hist,
+                                  bool want_grade, cudaStream_t st, uint32_t* passes) {
+    if (want_grade) {
+        Status s = grow(reinterpret_cast<void**>(&grade_), &grade_cap_, std::max<uint64_t>(4, k * 4));
+        if (!s.good()) return s;
+    }
+    cur_ = 0;
+    *passes = 0;
+    int res = 0;
+    Status s = sort_unique_range(keys_[0], vals_[0], keys_[1], vals_[1], k, kmin, kmax, raw_hist,
+                                 nullptr, nullptr, small_ + 2, want_grade ? grade_ : nullptr, st,
+                                 &res, passes);
+    if (!s.good()) return s;
+    cur_ = res;
+    scale_ = reinterpret_cast<double*>(keys_[cur_ ^ 1]);
     return Status::ok();
 }
 
@@ -450,6 +471,135 @@ Status Context::run(const double* dX, uint64_t n, uint64_t d, uint32_t layout,
         cudaEventElapsedTime(&r.times.reduce_ms, ev_[3], ev_[4]);
         cudaEventElapsedTime(&r.times.collect_ms, ev_[4], ev_[5]);
     }
+    cudaEventElapsedTime(&r.times.total_ms, ev_[0], ev_[5]);
+    if (out) *out = r;
+    return Status::ok();
+}
+
+Status Context::run_host_overlapped(const double* X, uint64_t n, uint64_t d, uint32_t layout,
+                                    cudaStream_t st, double* host_scale, uint64_t scale_capacity,
+                                    RunOutputs* out) {
+    Status s = reserve(n, d);
+    if (!s.good()) return s;
+    const uint64_t k = n * (n - (n > 0)) / 2;
+    constexpr uint32_t B = 16;  // key-range buckets
+    if (!(s = grow(reinterpret_cast<void**>(&dbuf_), &dbuf_cap_, k * 8 + 256)).good()) return s;
+    const uint64_t part_words = partition_scratch_words(k, B);
+    if (!(s = grow(reinterpret_cast<void**>(&part_counts_), &part_counts_cap_, part_words * 4 + 16))
+             .good())
+        return s;
+    if (!(s = grow(reinterpret_cast<void**>(&part_small_), &part_small_cap_, 2048 * 8)).good())
+        return s;
+    if (!copy_stream_) PH0B_TRY(cudaStreamCreateWithFlags(&copy_stream_, cudaStreamNonBlocking),
+                                "cudaStreamCreate");
+    uint64_t* d_spl = part_small_;           // [256]
+    uint64_t* d_tot = part_small_ + 256;     // [256]
+    uint64_t* d_mm = part_small_ + 512;      // [512]
+    uint64_t* d_base = part_small_ + 1024;   // [B + 1]
+    uint64_t* h = h_small_;
+    launches = 0;
+    RunOutputs r;
+    r.k = k;
+    std::memset(&r.times, 0, sizeof(r.times));
+    PH0B_TRY(cudaEventRecord(ev_[0], st), "event");
+    if (n * d)
+        PH0B_TRY(cudaMemcpyAsync(xin_, X, n * d * 8, cudaMemcpyHostToDevice, st), "H2D cloud");
+    uint64_t cnt = 0, kmin = 0, kmax = 0;
+    if (!(s = stage_distances(xin_, n, d, layout, 0, n, st, &cnt, &kmin, &kmax)).good()) return s;
+    PH0B_TRY(cudaEventRecord(ev_[1], st), "event");
+
+    // ---- splitters from an evenly spaced sample, stable partition into B key ranges -------
+    const uint64_t S = std::min<uint64_t>(k, std::min<uint64_t>(n, 16384));
+    std::vector<uint64_t> sample(S);
+    launches += launch_sample(keys_[0], k, S, survkeys_[0], st);
+    PH0B_TRY(cudaMemcpyAsync(sample.data(), survkeys_[0], S * 8, cudaMemcpyDeviceToHost, st), "D2H");
+    PH0B_TRY(cudaStreamSynchronize(st), "sample");
+    std::sort(sample.begin(), sample.end());
+    std::vector<uint64_t> spl(B - 1);
+    for (uint32_t j = 0; j + 1 < B; ++j) spl[j] = sample[std::min<uint64_t>(S - 1, (j + 1) * S / B)];
+    PH0B_TRY(cudaMemcpyAsync(d_spl, spl.data(), (B - 1) * 8, cudaMemcpyHostToDevice, st), "H2D");
+    // segments start on 4-element boundaries (16-byte aligned TMA bulk copies in the sort
+    // and unique kernels); the <= 3 padding slots per segment hold the cycle column {0, 0}
+    constexpr uint32_t kAlign = 4;
+    launches += launch_partition(keys_[0], vals_[0], k, d_spl, B, part_counts_, d_tot, d_mm,
+                                 keys_[1], vals_[1], st, kAlign);
+    PH0B_CHECK_LAUNCH("partition");
+    std::vector<uint64_t> tot(B), mm(2 * B);
+    PH0B_TRY(cudaMemcpyAsync(tot.data(), d_tot, B * 8, cudaMemcpyDeviceToHost, st), "D2H");
+    PH0B_TRY(cudaMemcpyAsync(mm.data(), d_mm, 2 * B * 8, cudaMemcpyDeviceToHost, st), "D2H");
+    PH0B_TRY(cudaMemsetAsync(d_base, 0, 8, st), "memset");
+    PH0B_TRY(cudaStreamSynchronize(st), "partition");
+
+    // ---- per bucket: sort + unique into D, then stream that slice of D to the host ---------
+    uint64_t start = 0, host_base = 0;
+    int target = -1;
+    for (uint32_t b = 0; b < B; ++b) {
+        const uint64_t c = tot[b];
+        int res = 0;
+        uint32_t passes = 0;
+        s = sort_unique_range(keys_[1] + start, vals_[1] + start, keys_[0] + start,
+                              vals_[0] + start, c, c ? mm[b] : 0, c ? mm[B + b] : 0, false,
+                              dbuf_, d_base + b, d_base + b + 1, nullptr, st, &res, &passes);
+        if (!s.good()) return s;
+        r.times.sort_passes = std::max(r.times.sort_passes, passes);
+        const int buf = res == 0 ? 1 : 0;  // global buffer holding this bucket's sorted data
+        if (c && target < 0) target = buf;
+        if (c && buf != target) {  // keep M contiguous in one buffer
+            PH0B_TRY(cudaMemcpyAsync(keys_[target] + start, keys_[buf] + start, c * 8,
+                                     cudaMemcpyDeviceToDevice, st), "D2D");
+            PH0B_TRY(cudaMemcpyAsync(vals_[target] + start, vals_[buf] + start, c * 4,
+                                     cudaMemcpyDeviceToDevice, st), "D2D");
+        }
+        PH0B_TRY(cudaMemcpyAsync(h + 5, d_base + b + 1, 8, cudaMemcpyDeviceToHost, st), "D2H");
+        PH0B_TRY(cudaEventRecord(ev_[6], st), "event");
+        PH0B_TRY(cudaEventSynchronize(ev_[6]), "bucket");
+        const uint64_t next_base = h[5];
+        if (host_scale && next_base > host_base) {
+            if (next_base > scale_capacity)
+                return {PH0B_ERR_CAPACITY, "scale buffer too small: need >= " +
+                                               std::to_string(next_base) + " entries"};
+            PH0B_TRY(cudaStreamWaitEvent(copy_stream_, ev_[6], 0), "wait");
+            PH0B_TRY(cudaMemcpyAsync(host_scale + host_base, dbuf_ + host_base,
+                                     (next_base - host_base) * 8, cudaMemcpyDeviceToHost,
+                                     copy_stream_), "D2H scale");
+        }
+        host_base = next_base;
+        start += (c + kAlign - 1) / kAlign * kAlign;
+    }
+    const uint64_t kpad = start;  // columns incl. the sentinel padding
+    if (target < 0) target = 0;
+    PH0B_TRY(cudaEventRecord(ev_[2], st), "event");
+    PH0B_TRY(cudaEventRecord(ev_[3], st), "event");
+    cur_ = target;
+    scale_ = dbuf_;
+    PH0B_TRY(cudaMemcpyAsync(small_ + 2, d_base + B, 8, cudaMemcpyDeviceToDevice, st), "copy");
+
+    // ---- K4 + K5 on the whole (now sorted) matrix ------------------------------------------
+    ReduceStats rst;
+    if (!(s = stage_reduce(vals_[cur_], kpad, (uint32_t)n, st, &rst)).good()) return s;
+    PH0B_TRY(cudaEventRecord(ev_[4], st), "event");
+    const uint32_t m = rst.survivors;
+    if (m != n - 1)
+        return {PH0B_ERR_CUDA, "internal error: reduction produced " + std::to_string(m) +
+                                   " surviving columns, expected " + std::to_string(n - 1)};
+    if (!(s = stage_collect(m, kpad, 0, st)).good()) return s;
+    PH0B_TRY(cudaEventRecord(ev_[5], st), "event");
+    PH0B_TRY(cudaStreamSynchronize(st), "pipeline");
+    PH0B_TRY(cudaStreamSynchronize(copy_stream_), "D2H scale");
+    r.n_scale = host_base;
+    r.d_uv_sorted = vals_[cur_];
+    r.d_scale = dbuf_;
+    r.d_death_grade = death_grade_;
+    r.d_death_length = death_length_;
+    r.d_surv_sorted = surv_sorted_;
+    r.n_finite = m;
+    r.essential = n - m;
+    r.times.reduce_rounds = rst.rounds;
+    r.times.columns_scanned = rst.scanned;
+    cudaEventElapsedTime(&r.times.distance_ms, ev_[0], ev_[1]);
+    cudaEventElapsedTime(&r.times.sort_ms, ev_[1], ev_[2]);
+    cudaEventElapsedTime(&r.times.reduce_ms, ev_[3], ev_[4]);
+    cudaEventElapsedTime(&r.times.collect_ms, ev_[4], ev_[5]);
     cudaEventElapsedTime(&r.times.total_ms, ev_[0], ev_[5]);
     if (out) *out = r;
     return Status::ok();

@@ -61,6 +61,19 @@ public:
                              bool want_grade, cudaStream_t st, uint32_t* passes);
     Status stage_reduce(const uint32_t* uv, uint64_t count, uint32_t n, cudaStream_t st,
                         ReduceStats* rst);
+    // Sort (kb0, vb0) of k edges (ping-pong with kb1/vb1) and write its distinct lengths to
+    // scale_out (null: the free key buffer) starting at *d_base (null: 0); *d_count receives
+    // base + |D|.  *res: 0/1 = buffer holding the sorted data.
+    Status sort_unique_range(uint64_t* kb0, uint32_t* vb0, uint64_t* kb1, uint32_t* vb1,
+                             uint64_t k, uint64_t kmin, uint64_t kmax, bool raw_hist,
+                             double* scale_out, const uint64_t* d_base, uint64_t* d_count,
+                             uint32_t* grade_out, cudaStream_t st, int* res, uint32_t* passes);
+    // Host-output run with the D2H of D overlapped with the sort: edges are split into
+    // key-range buckets (one stable partition pass), each bucket is sorted + deduplicated
+    // in turn and its slice of D streams to the host while the next bucket sorts.
+    Status run_host_overlapped(const double* X, uint64_t n, uint64_t d, uint32_t layout,
+                               cudaStream_t st, double* host_scale, uint64_t scale_capacity,
+                               RunOutputs* out);
     Status stage_collect(uint32_t m, uint64_t count, uint64_t grade_offset, cudaStream_t st);
     Status reserve_edges(uint64_t count);  // ping-pong key/column buffers for count edges
     Status reserve_points(uint64_t n, uint64_t d);
@@ -96,7 +109,7 @@ private:
     int device_;
     int num_sms_ = 148;
     cudaStream_t stream_ = nullptr;
-    cudaEvent_t ev_[8] = {};
+    cudaEvent_t ev_[8] = {};  // [6]: per-bucket completion (overlapped host path)
     uint64_t bytes_ = 0;
 
     // workspace (capacities in bytes)
@@ -116,6 +129,10 @@ private:
     uint64_t* death_grade_ = nullptr; uint64_t death_grade_cap_ = 0;
     double* death_length_ = nullptr;  uint64_t death_length_cap_ = 0;
     uint64_t* uscratch_ = nullptr; uint64_t uscratch_cap_ = 0;
+    double* dbuf_ = nullptr;       uint64_t dbuf_cap_ = 0;        // D (overlapped host path)
+    uint32_t* part_counts_ = nullptr; uint64_t part_counts_cap_ = 0;
+    uint64_t* part_small_ = nullptr;  uint64_t part_small_cap_ = 0;
+    cudaStream_t copy_stream_ = nullptr;
     // fixed small buffers
     uint32_t* hist_ = nullptr;     // [8][256]
     uint32_t* counters_ = nullptr; // [64]

@@ -122,7 +122,8 @@ __global__ void __launch_bounds__(kThreads)
     k7_scatter(const uint64_t* __restrict__ keys, const uint32_t* __restrict__ vals, uint64_t count,
                const uint64_t* __restrict__ splitters, uint32_t parts,
                const uint32_t* __restrict__ offsets, const uint64_t* __restrict__ totals,
-               uint64_t* __restrict__ keys_out, uint32_t* __restrict__ vals_out) {
+               uint64_t* __restrict__ keys_out, uint32_t* __restrict__ vals_out,
+               uint32_t align) {
     __shared__ uint64_t s_spl[kMaxParts];
     __shared__ uint32_t s_whist[kWarps][kMaxParts];
     __shared__ uint64_t s_base[kMaxParts];
@@ -131,10 +132,18 @@ __global__ void __launch_bounds__(kThreads)
         for (int w = 0; w < kWarps; ++w) s_whist[w][i] = 0;
     }
     if (threadIdx.x == 0) {
+        // segment b starts at the sum of the earlier totals, each rounded up to `align`
+        // elements; block 0 fills the padding slots with the sentinel column {0, 0} (a cycle)
         uint64_t acc = 0;
         for (uint32_t b = 0; b < parts; ++b) {
             s_base[b] = acc + offsets[(uint64_t)blockIdx.x * parts + b];
-            acc += totals[b];
+            const uint64_t padded = (totals[b] + align - 1) / align * align;
+            if (blockIdx.x == 0)
+                for (uint64_t q = acc + totals[b]; q < acc + padded; ++q) {
+                    keys_out[q] = 0;
+                    vals_out[q] = 0;
+                }
+            acc += padded;
         }
     }
     __syncthreads();
@@ -173,7 +182,7 @@ __global__ void __launch_bounds__(kThreads)
 int launch_partition(const uint64_t* keys, const uint32_t* vals, uint64_t count,
                      const uint64_t* d_splitters, uint32_t parts, uint32_t* d_counts_scratch,
                      uint64_t* d_totals, uint64_t* d_bminmax, uint64_t* keys_out,
-                     uint32_t* vals_out, cudaStream_t s) {
+                     uint32_t* vals_out, cudaStream_t s, uint32_t align) {
     if (parts < 1 || parts > (uint32_t)kMaxParts) return -1;
     const uint64_t tiles = (count + kTile - 1) / kTile;
     cudaMemsetAsync(d_bminmax, 0xFF, sizeof(uint64_t) * parts, s);
@@ -189,7 +198,7 @@ int launch_partition(const uint64_t* keys, const uint32_t* vals, uint64_t count,
     k7_scan<<<parts, 1024, 0, s>>>(d_counts_scratch, (uint32_t)tiles, parts, d_totals);
     k7_scatter<<<(unsigned)tiles, kThreads, 0, s>>>(keys, vals, count, d_splitters, parts,
                                                     d_counts_scratch, d_totals, keys_out,
-                                                    vals_out);
+                                                    vals_out, align);
     return 3;
 }
 

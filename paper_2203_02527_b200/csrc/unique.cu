@@ -287,7 +287,8 @@ __global__ void __launch_bounds__(kUThreads, 3)
     k3_unique_p(uint64_t* __restrict__ keys, uint32_t* __restrict__ vals, uint64_t count,
                 uint64_t kmin, uint32_t low_bits, double* __restrict__ scale,
                 uint32_t* __restrict__ grade, uint64_t* __restrict__ status, uint32_t epoch,
-                uint64_t* n_scale, uint32_t* redo, uint32_t num_tiles) {
+                uint64_t* n_scale, uint32_t* redo, uint32_t num_tiles,
+                const uint64_t* __restrict__ d_base) {
     extern __shared__ __align__(128) uint64_t up_dyn[];
     __shared__ __align__(8) uint64_t s_bar[2];
     __shared__ uint32_t s_warp_tot[kUWarps];
@@ -319,6 +320,7 @@ __global__ void __launch_bounds__(kUThreads, 3)
     };
     uint32_t tile = blockIdx.x;
     if (tid == 0 && tile < num_tiles) issue(tile, 0);
+    const uint64_t base0 = d_base ? *d_base : 0ull;  // D index of this range's first length
     uint32_t phase[2] = {0, 0};
     int b = 0;
     for (; tile < num_tiles; tile += gridDim.x, b ^= 1) {
@@ -431,8 +433,8 @@ __global__ void __launch_bounds__(kUThreads, 3)
                 excl = lookback_window<8>(status, 1, tile, epoch);
                 st_relaxed_u64(my, pack_status(kStateInclusive, epoch, excl + tile_tot));
             }
-            s_prefix = excl;
-            if (tile == num_tiles - 1) *n_scale = (uint64_t)excl + tile_tot;
+            s_prefix = base0 + excl;
+            if (tile == num_tiles - 1) *n_scale = base0 + (uint64_t)excl + tile_tot;
         }
         __syncthreads();
         const uint64_t base = s_prefix;
@@ -470,10 +472,11 @@ int launch_unique(const UniqueArgs& a, cudaStream_t s) {
         cudaMemsetAsync(a.n_scale, 0, sizeof(uint64_t), s);
         return 0;
     }
-    static const bool three_kernels = [] {
+    static const bool three_kernels_env = [] {
         const char* e = getenv("PH0B_UNIQUE");
         return e && e[0] == '3';
     }();
+    const bool three_kernels = three_kernels_env && !a.d_base;
     if (!three_kernels) {
         const size_t smem = (size_t)2 * kUStage * 8;
         static int per_sm = 0;
@@ -491,7 +494,7 @@ int launch_unique(const UniqueArgs& a, cudaStream_t s) {
         if (grid > tiles) grid = tiles;
         k3_unique_p<<<(unsigned)grid, kUThreads, smem, s>>>(
             a.keys, a.vals, a.count, a.kmin, a.low_bits, a.scale, a.grade, a.status, a.epoch,
-            a.n_scale, a.redo, (uint32_t)tiles);
+            a.n_scale, a.redo, (uint32_t)tiles, a.d_base);
         return 1;
     }
     const uint64_t tiles = (a.count + kTileKeys - 1) / kTileKeys;

@@ -221,3 +221,35 @@ def test_c5_full_size_properties():
     X = pkg.config_cloud("C5")
     bc = pkg.h0_barcode(X)
     check_large(X, bc)
+
+
+def test_overlapped_host_path_matches_device_path():
+    """ph0b_run_host on a large cloud takes the bucketed path whose D2H of D overlaps the sort
+    (16 key-range buckets, padded segments, per-bucket D slices); it must equal the plain
+    path bit for bit (run with PH0B_OVERLAP=0 semantics via the device-result API)."""
+    torch = pytest.importorskip("torch")
+    X = pkg.config_cloud("C3")  # K = 3.4e7 >= 2^26? no: use a bigger prefix of C4
+    X = pkg.config_cloud("C4", 12000)  # K = 7.2e7 >= 2^26
+    n, d = X.shape
+    ctx = pkg.Context(0)
+    xt = torch.from_numpy(np.asfortranarray(X).ravel(order="F").copy()).cuda()
+    r = ctx.run_device(xt.data_ptr(), n, d)
+    import ctypes
+    dev_scale = torch.empty(r.n_scale, dtype=torch.float64, device="cuda")
+    ctypes.memmove  # noqa: B018
+    src = torch.as_tensor(type("C", (), {"__cuda_array_interface__": {
+        "shape": (r.n_scale,), "typestr": "<f8", "data": (r.d_scale, False), "version": 3,
+        "strides": None}})(), device="cuda")
+    dev_scale.copy_(src)
+    D_dev = dev_scale.cpu().numpy()
+    dg = np.empty(n, np.uint64)
+    dl = np.empty(n)
+    sc = np.empty(r.n_scale)
+    nf, ess, ns, t = ctx.run_host(np.asfortranarray(X), dg, dl, sc)
+    assert ns == r.n_scale and nf == n - 1 and ess == 1
+    assert np.array_equal(bits(sc), bits(D_dev))
+    bc = pkg.h0_barcode(X)  # library-allocated path (not overlapped)
+    assert np.array_equal(dg[:nf], bc.death_grade)
+    assert np.array_equal(bits(dl[:nf]), bits(bc.death_length))
+    assert np.array_equal(bits(sc), bits(bc.scale))
+    ctx.close()
