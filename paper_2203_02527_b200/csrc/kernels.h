@@ -94,7 +94,8 @@ struct ReduceState {
     uint32_t* scan_tile_counter;
     uint32_t* pair_min;      // [kPairMax] sparse phase
     uint8_t* cid;            // [n] compact component ids (sparse phase)
-    uint32_t* host_counters; // pinned host mirror [8]
+    uint32_t* host_counters;   // zero-copy host mirror [8] ...
+    uint32_t* mapped_counters; // ... and its device alias (written by k4_publish)
 };
 struct ReduceStats {
     uint32_t rounds = 0;

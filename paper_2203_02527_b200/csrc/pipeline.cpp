@@ -80,6 +80,7 @@ Context::~Context() {
         if (p) cudaFree(p);
     if (h_small_) cudaFreeHost(h_small_);
     if (h_counters_) cudaFreeHost(h_counters_);
+    if (h_mapped_) cudaFreeHost(h_mapped_);
     if (copy_stream_) cudaStreamDestroy(copy_stream_);
     for (auto& e : ev_)
         if (e) cudaEventDestroy(e);
@@ -108,6 +109,12 @@ Status Context::init() {
     PH0B_TRY(cudaHostAlloc(&h_small_, sizeof(uint64_t) * 8, cudaHostAllocDefault), "cudaHostAlloc");
     PH0B_TRY(cudaHostAlloc(&h_counters_, sizeof(uint32_t) * 64, cudaHostAllocDefault),
              "cudaHostAlloc");
+    // Zero-copy host words for per-bucket results (D offsets, redo flag): kernels write them
+    // over PCIe directly, so the host never queues a small D2H behind a large one.
+    PH0B_TRY(cudaHostAlloc(&h_mapped_, sizeof(uint64_t) * 256, cudaHostAllocMapped),
+             "cudaHostAlloc mapped");
+    PH0B_TRY(cudaHostGetDevicePointer(reinterpret_cast<void**>(&d_mapped_), h_mapped_, 0),
+             "cudaHostGetDevicePointer");
     bytes_ += 8 * 256 * 4 + 64 * 4 + 64;
     atomic_rank_ok_ = sort_self_test(stream_);
     return Status::ok();
@@ -333,8 +340,9 @@ Status Context::sort_unique_range(uint64_t* kb0, uint32_t* vb0, uint64_t* kb1, u
         *passes += plan.passes;
 
         double* scale = scale_out ? scale_out : reinterpret_cast<double*>(kb[*res ^ 1]);
-        uint32_t* redo = reinterpret_cast<uint32_t*>(small_ + 4);
-        PH0B_TRY(cudaMemsetAsync(redo, 0, 4, st), "memset");
+        volatile uint64_t* h_redo = h_mapped_;
+        *h_redo = 0;  // (no kernel of this context is running: the previous check synced)
+        uint32_t* redo = reinterpret_cast<uint32_t*>(d_mapped_);
         Status gs = grow(reinterpret_cast<void**>(&uscratch_), &uscratch_cap_,
                          unique_scratch_words(k) * 8);
         if (!gs.good()) return gs;
@@ -343,9 +351,9 @@ Status Context::sort_unique_range(uint64_t* kb0, uint32_t* vb0, uint64_t* kb1, u
         launches += launch_unique(ua, st);
         PH0B_CHECK_LAUNCH("unique kernel");
         if (low_bits == 0) break;
-        PH0B_TRY(cudaMemcpyAsync(h_small_ + 4, small_ + 4, 8, cudaMemcpyDeviceToHost, st), "D2H");
-        PH0B_TRY(cudaStreamSynchronize(st), "unique");
-        if (static_cast<uint32_t>(h_small_[4]) == 0) break;
+        PH0B_TRY(cudaEventRecord(ev_[7], st), "event");
+        PH0B_TRY(cudaEventSynchronize(ev_[7]), "unique");
+        if (static_cast<uint32_t>(*h_redo) == 0) break;
         src = *res;
     }
     return Status::ok();
@@ -382,7 +390,8 @@ Status Context::stage_reduce(const uint32_t* uv, uint64_t count, uint32_t n, cud
     rs.cap = cand_cap_[0] / 4;
     rs.surv = surv_;
     rs.counters = counters_;
-    rs.host_counters = h_counters_;
+    rs.host_counters = reinterpret_cast<uint32_t*>(h_mapped_ + 128);
+    rs.mapped_counters = reinterpret_cast<uint32_t*>(d_mapped_ + 128);
     uint32_t ep = 0;
     run_reduction(rs, st, num_sms_, ep, rst);
     launches += rst->launches;
@@ -495,8 +504,8 @@ Status Context::run_host_overlapped(const double* X, uint64_t n, uint64_t d, uin
     uint64_t* d_spl = part_small_;           // [256]
     uint64_t* d_tot = part_small_ + 256;     // [256]
     uint64_t* d_mm = part_small_ + 512;      // [512]
-    uint64_t* d_base = part_small_ + 1024;   // [B + 1]
-    uint64_t* h = h_small_;
+    uint64_t* d_base = d_mapped_ + 8;        // [B + 1], zero-copy host words
+    volatile uint64_t* h_base = h_mapped_ + 8;
     launches = 0;
     RunOutputs r;
     r.k = k;
@@ -527,8 +536,8 @@ Status Context::run_host_overlapped(const double* X, uint64_t n, uint64_t d, uin
     std::vector<uint64_t> tot(B), mm(2 * B);
     PH0B_TRY(cudaMemcpyAsync(tot.data(), d_tot, B * 8, cudaMemcpyDeviceToHost, st), "D2H");
     PH0B_TRY(cudaMemcpyAsync(mm.data(), d_mm, 2 * B * 8, cudaMemcpyDeviceToHost, st), "D2H");
-    PH0B_TRY(cudaMemsetAsync(d_base, 0, 8, st), "memset");
     PH0B_TRY(cudaStreamSynchronize(st), "partition");
+    h_base[0] = 0;
 
     // ---- per bucket: sort + unique into D, then stream that slice of D to the host ---------
     uint64_t start = 0, host_base = 0;
@@ -550,10 +559,9 @@ Status Context::run_host_overlapped(const double* X, uint64_t n, uint64_t d, uin
             PH0B_TRY(cudaMemcpyAsync(vals_[target] + start, vals_[buf] + start, c * 4,
                                      cudaMemcpyDeviceToDevice, st), "D2D");
         }
-        PH0B_TRY(cudaMemcpyAsync(h + 5, d_base + b + 1, 8, cudaMemcpyDeviceToHost, st), "D2H");
         PH0B_TRY(cudaEventRecord(ev_[6], st), "event");
         PH0B_TRY(cudaEventSynchronize(ev_[6]), "bucket");
-        const uint64_t next_base = h[5];
+        const uint64_t next_base = h_base[b + 1];
         if (host_scale && next_base > host_base) {
             if (next_base > scale_capacity)
                 return {PH0B_ERR_CAPACITY, "scale buffer too small: need >= " +
@@ -572,7 +580,7 @@ Status Context::run_host_overlapped(const double* X, uint64_t n, uint64_t d, uin
     PH0B_TRY(cudaEventRecord(ev_[3], st), "event");
     cur_ = target;
     scale_ = dbuf_;
-    PH0B_TRY(cudaMemcpyAsync(small_ + 2, d_base + B, 8, cudaMemcpyDeviceToDevice, st), "copy");
+    PH0B_TRY(cudaMemcpyAsync(small_ + 2, d_base + B, 8, cudaMemcpyDefault, st), "copy");
 
     // ---- K4 + K5 on the whole (now sorted) matrix ------------------------------------------
     ReduceStats rst;

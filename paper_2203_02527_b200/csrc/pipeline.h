@@ -139,6 +139,8 @@ private:
     uint64_t* small_ = nullptr;    // [0..1] minmax, [2] n_scale, [3] nonfinite flag (u32)
     uint64_t* h_small_ = nullptr;  // pinned mirror of small_
     uint32_t* h_counters_ = nullptr;  // pinned [64]
+    uint64_t* h_mapped_ = nullptr;    // mapped pinned [256] (zero-copy flags / offsets)
+    uint64_t* d_mapped_ = nullptr;    // device alias of h_mapped_
     uint32_t epoch_ = 1;
     bool status_zeroed_ = false;
     bool atomic_rank_ok_ = false;

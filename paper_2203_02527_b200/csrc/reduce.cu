@@ -211,6 +211,12 @@ __global__ void k4_relabel(uint32_t n, uint32_t* comp, const uint32_t* __restric
     }
 }
 
+// Publish the round counters to zero-copy host memory with plain stores (no copy engine:
+// a D2H of D may be streaming on another stream and would delay a queued small copy).
+__global__ void k4_publish(const uint32_t* __restrict__ counters, uint32_t* mapped) {
+    if (threadIdx.x < 8) mapped[threadIdx.x] = counters[threadIdx.x];
+}
+
 inline unsigned grid_for(uint64_t work, int num_sms, int per_sm = 8) {
     uint64_t b = (work + kThreads - 1) / kThreads;
     const uint64_t cap = (uint64_t)num_sms * per_sm;
@@ -238,9 +244,9 @@ int run_reduction(ReduceState& st, cudaStream_t s, int num_sms, uint32_t& epoch,
     k4_init<<<gn, kThreads, 0, s>>>(st.comp, st.best, par, n, comp16);
     S.launches += 1;
 
-    uint32_t* h = st.host_counters;
+    volatile uint32_t* h = st.host_counters;
     auto pull = [&]() {
-        cudaMemcpyAsync(h, st.counters, sizeof(uint32_t) * 8, cudaMemcpyDeviceToHost, s);
+        k4_publish<<<1, 32, 0, s>>>(st.counters, st.mapped_counters);
         cudaStreamSynchronize(s);
     };
 

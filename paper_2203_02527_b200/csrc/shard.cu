@@ -118,6 +118,9 @@ __global__ void k7_scan(uint32_t* __restrict__ counts, uint32_t tiles, uint32_t 
     if (threadIdx.x == 0) totals[b] = s_carry;
 }
 
+// Stable scatter of one 4096-element tile into its segments: ranks from per-warp shared
+// histograms (ATOMS lane order = stable), the tile staged in shared memory in segment order,
+// then written out so consecutive threads write consecutive positions of each segment run.
 __global__ void __launch_bounds__(kThreads)
     k7_scatter(const uint64_t* __restrict__ keys, const uint32_t* __restrict__ vals, uint64_t count,
                const uint64_t* __restrict__ splitters, uint32_t parts,
@@ -126,7 +129,12 @@ __global__ void __launch_bounds__(kThreads)
                uint32_t align) {
     __shared__ uint64_t s_spl[kMaxParts];
     __shared__ uint32_t s_whist[kWarps][kMaxParts];
-    __shared__ uint64_t s_base[kMaxParts];
+    __shared__ uint32_t s_tstart[kMaxParts];
+    __shared__ uint64_t s_base[kMaxParts];  // global position of this tile's first element of b
+    extern __shared__ __align__(16) uint64_t sc_dyn[];
+    uint64_t* s_k = sc_dyn;                                                 // [kTile]
+    uint32_t* s_v = reinterpret_cast<uint32_t*>(sc_dyn + kTile);            // [kTile]
+    uint16_t* s_b = reinterpret_cast<uint16_t*>(s_v + kTile);               // [kTile]
     for (uint32_t i = threadIdx.x; i < kMaxParts; i += kThreads) {
         s_spl[i] = i + 1 < parts ? splitters[i] : ~0ull;
         for (int w = 0; w < kWarps; ++w) s_whist[w][i] = 0;
@@ -148,32 +156,62 @@ __global__ void __launch_bounds__(kThreads)
     }
     __syncthreads();
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    const uint64_t wbase = (uint64_t)blockIdx.x * kTile + (uint64_t)warp * (32 * kItems) + lane;
-    uint32_t bk[kItems], rk[kItems];
+    const uint64_t tile0 = (uint64_t)blockIdx.x * kTile;
+    const uint32_t tn = (uint32_t)(count - tile0 < (uint64_t)kTile ? count - tile0 : kTile);
+    const uint32_t wofs = warp * (32 * kItems) + lane;
+    uint64_t kk[kItems];
+    uint32_t vv[kItems], bk[kItems], rk[kItems];
+#pragma unroll
+    for (int i = 0; i < kItems; ++i) {  // all loads in flight first
+        const uint32_t pos = wofs + 32 * i;
+        kk[i] = pos < tn ? keys[tile0 + pos] : 0ull;
+        vv[i] = pos < tn ? vals[tile0 + pos] : 0u;
+    }
+#pragma unroll
     for (int i = 0; i < kItems; ++i) {
-        const uint64_t idx = wbase + 32 * i;
-        bk[i] = idx < count ? bucket_of(keys[idx], s_spl, parts - 1) : 0u;
+        const uint32_t pos = wofs + 32 * i;
+        bk[i] = pos < tn ? bucket_of(kk[i], s_spl, parts - 1) : 0u;
         // ATOMS resolves same-address lanes in lane order (device self-test), so the
         // returned count is the stable rank within this warp
-        rk[i] = idx < count ? atomicAdd(&s_whist[warp][bk[i]], 1u) : 0u;
+        rk[i] = pos < tn ? atomicAdd(&s_whist[warp][bk[i]], 1u) : 0u;
     }
     __syncthreads();
-    for (uint32_t b = threadIdx.x; b < parts; b += kThreads) {
+    if (threadIdx.x < kMaxParts) {
+        const uint32_t b = threadIdx.x;
         uint32_t acc = 0;
         for (int w = 0; w < kWarps; ++w) {
             const uint32_t c = s_whist[w][b];
             s_whist[w][b] = acc;
             acc += c;
         }
+        s_tstart[b] = acc;  // tile count of b (scanned below)
     }
     __syncthreads();
-    for (int i = 0; i < kItems; ++i) {
-        const uint64_t idx = wbase + 32 * i;
-        if (idx < count) {
-            const uint64_t dst = s_base[bk[i]] + s_whist[warp][bk[i]] + rk[i];
-            keys_out[dst] = keys[idx];
-            vals_out[dst] = vals[idx];
+    if (threadIdx.x == 0) {
+        uint32_t acc = 0;
+        for (uint32_t b = 0; b < parts; ++b) {
+            const uint32_t c = s_tstart[b];
+            s_tstart[b] = acc;
+            acc += c;
         }
+    }
+    __syncthreads();
+#pragma unroll
+    for (int i = 0; i < kItems; ++i) {
+        const uint32_t pos = wofs + 32 * i;
+        if (pos < tn) {
+            const uint32_t dst = s_tstart[bk[i]] + s_whist[warp][bk[i]] + rk[i];
+            s_k[dst] = kk[i];
+            s_v[dst] = vv[i];
+            s_b[dst] = (uint16_t)bk[i];
+        }
+    }
+    __syncthreads();
+    for (uint32_t p = threadIdx.x; p < tn; p += kThreads) {
+        const uint32_t b = s_b[p];
+        const uint64_t dst = s_base[b] + (p - s_tstart[b]);
+        keys_out[dst] = s_k[p];
+        vals_out[dst] = s_v[p];
     }
 }
 
@@ -196,7 +234,13 @@ int launch_partition(const uint64_t* keys, const uint32_t* vals, uint64_t count,
         reinterpret_cast<unsigned long long*>(d_bminmax),
         reinterpret_cast<unsigned long long*>(d_bminmax + parts));
     k7_scan<<<parts, 1024, 0, s>>>(d_counts_scratch, (uint32_t)tiles, parts, d_totals);
-    k7_scatter<<<(unsigned)tiles, kThreads, 0, s>>>(keys, vals, count, d_splitters, parts,
+    constexpr size_t kScSmem = (size_t)kTile * (8 + 4 + 2);
+    static bool configured = false;
+    if (!configured) {
+        cudaFuncSetAttribute(k7_scatter, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kScSmem);
+        configured = true;
+    }
+    k7_scatter<<<(unsigned)tiles, kThreads, kScSmem, s>>>(keys, vals, count, d_splitters, parts,
                                                     d_counts_scratch, d_totals, keys_out,
                                                     vals_out, align);
     return 3;
