@@ -162,7 +162,8 @@ int ph0b_shard_distances(ph0b_context* ctx, const double* dX, uint64_t n, uint64
 int ph0b_shard_sample(ph0b_context* ctx, uint64_t s, uint64_t* out_host);
 /* Stable partition of the local edges by parts-1 ascending splitter keys: segment j
  * (contiguous in the returned device send buffers) goes to rank j.  counts/part_min/
- * part_max: host arrays of `parts` entries. */
+ * part_max: host arrays of `parts` entries; part_min/part_max bound the keys of segment j
+ * ([splitter j-1, splitter j) clipped to the local key range). */
 int ph0b_shard_partition(ph0b_context* ctx, const uint64_t* splitters, uint32_t parts,
                          void* stream, uint64_t** d_keys_send, uint32_t** d_vals_send,
                          uint64_t* counts, uint64_t* part_min, uint64_t* part_max);

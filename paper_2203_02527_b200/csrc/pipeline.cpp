@@ -57,6 +57,15 @@ inline uint32_t truncated_plan(uint64_t span, uint32_t max_passes, SortPlan* pla
 
 inline uint64_t row_base(uint64_t u, uint64_t n) { return u * (2 * n - u - 1) / 2; }
 
+uint64_t d2h_chunk_elems() {
+    static const uint64_t v = [] {
+        const char* e = getenv("PH0B_D2H_CHUNK_MB");
+        const uint64_t mb = e ? (uint64_t)atoll(e) : 32;
+        return (mb ? mb : 32) << 17;  // MiB -> f64 elements
+    }();
+    return v;
+}
+
 uint32_t max_sort_passes() {
     static const uint32_t v = [] {
         const char* e = getenv("PH0B_MAX_PASSES");
@@ -491,7 +500,10 @@ Status Context::run_host_overlapped(const double* X, uint64_t n, uint64_t d, uin
     Status s = reserve(n, d);
     if (!s.good()) return s;
     const uint64_t k = n * (n - (n > 0)) / 2;
-    constexpr uint32_t B = 16;  // key-range buckets
+    // key-range buckets: the first ones small (1/256, 1/256, 1/128, 1/64, 1/32 of the edges)
+    // so the first D slice reaches the copy engine early and every later bucket is sorted
+    // before the copy of the previous one ends; then 15 buckets of 1/16
+    constexpr uint32_t B = 20;
     if (!(s = grow(reinterpret_cast<void**>(&dbuf_), &dbuf_cap_, k * 8 + 256)).good()) return s;
     const uint64_t part_words = partition_scratch_words(k, B);
     if (!(s = grow(reinterpret_cast<void**>(&part_counts_), &part_counts_cap_, part_words * 4 + 16))
@@ -502,8 +514,8 @@ Status Context::run_host_overlapped(const double* X, uint64_t n, uint64_t d, uin
     if (!copy_stream_) PH0B_TRY(cudaStreamCreateWithFlags(&copy_stream_, cudaStreamNonBlocking),
                                 "cudaStreamCreate");
     uint64_t* d_spl = part_small_;           // [256]
-    uint64_t* d_tot = part_small_ + 256;     // [256]
-    uint64_t* d_mm = part_small_ + 512;      // [512]
+    uint64_t* d_tot = part_small_ + 256;     // [512]: totals | segment starts
+    uint64_t* d_mm = part_small_ + 768;      // [512]: key bounds
     uint64_t* d_base = d_mapped_ + 8;        // [B + 1], zero-copy host words
     volatile uint64_t* h_base = h_mapped_ + 8;
     launches = 0;
@@ -525,13 +537,16 @@ Status Context::run_host_overlapped(const double* X, uint64_t n, uint64_t d, uin
     PH0B_TRY(cudaStreamSynchronize(st), "sample");
     std::sort(sample.begin(), sample.end());
     std::vector<uint64_t> spl(B - 1);
-    for (uint32_t j = 0; j + 1 < B; ++j) spl[j] = sample[std::min<uint64_t>(S - 1, (j + 1) * S / B)];
+    for (uint32_t j = 0; j + 1 < B; ++j) {
+        const uint64_t num = j < 4 ? (1ull << j) : 16ull * (j - 3);  // cumulative, /256
+        spl[j] = sample[std::min<uint64_t>(S - 1, num * S / 256)];
+    }
     PH0B_TRY(cudaMemcpyAsync(d_spl, spl.data(), (B - 1) * 8, cudaMemcpyHostToDevice, st), "H2D");
     // segments start on 4-element boundaries (16-byte aligned TMA bulk copies in the sort
     // and unique kernels); the <= 3 padding slots per segment hold the cycle column {0, 0}
     constexpr uint32_t kAlign = 4;
     launches += launch_partition(keys_[0], vals_[0], k, d_spl, B, part_counts_, d_tot, d_mm,
-                                 keys_[1], vals_[1], st, kAlign);
+                                 keys_[1], vals_[1], st, kAlign, kmin, kmax);
     PH0B_CHECK_LAUNCH("partition");
     std::vector<uint64_t> tot(B), mm(2 * B);
     PH0B_TRY(cudaMemcpyAsync(tot.data(), d_tot, B * 8, cudaMemcpyDeviceToHost, st), "D2H");
@@ -567,9 +582,13 @@ Status Context::run_host_overlapped(const double* X, uint64_t n, uint64_t d, uin
                 return {PH0B_ERR_CAPACITY, "scale buffer too small: need >= " +
                                                std::to_string(next_base) + " entries"};
             PH0B_TRY(cudaStreamWaitEvent(copy_stream_, ev_[6], 0), "wait");
-            PH0B_TRY(cudaMemcpyAsync(host_scale + host_base, dbuf_ + host_base,
-                                     (next_base - host_base) * 8, cudaMemcpyDeviceToHost,
-                                     copy_stream_), "D2H scale");
+            // several medium copies sustain a higher PCIe rate than one large one (measured
+            // 55 vs 52 GB/s for 17 GB, tools/d2h_big.py)
+            for (uint64_t q = host_base; q < next_base; q += d2h_chunk_elems()) {
+                const uint64_t e = std::min<uint64_t>(next_base, q + d2h_chunk_elems());
+                PH0B_TRY(cudaMemcpyAsync(host_scale + q, dbuf_ + q, (e - q) * 8,
+                                         cudaMemcpyDeviceToHost, copy_stream_), "D2H scale");
+            }
         }
         host_base = next_base;
         start += (c + kAlign - 1) / kAlign * kAlign;

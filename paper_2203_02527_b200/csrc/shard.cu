@@ -35,39 +35,55 @@ __device__ __forceinline__ uint32_t bucket_of(uint64_t key, const uint64_t* spl,
     return lo;
 }
 
+__device__ __forceinline__ uint32_t block_scan_256(uint32_t x, uint32_t* sh_warp,
+                                                 uint32_t* total) {
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    uint32_t inc = x;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        const uint32_t y = __shfl_up_sync(0xffffffffu, inc, o);
+        if (lane >= o) inc += y;
+    }
+    if (lane == 31) sh_warp[warp] = inc;
+    __syncthreads();
+    uint32_t wb = 0, tot = 0;
+#pragma unroll
+    for (int w = 0; w < kWarps; ++w) {
+        const uint32_t t = sh_warp[w];
+        wb += (w < warp) ? t : 0u;
+        tot += t;
+    }
+    if (total) *total = tot;
+    return wb + inc - x;
+}
+
+// Per-tile bucket counts (one ATOMS per key; the bucket key ranges themselves come from the
+// splitters, so no per-key min/max is needed).
 __global__ void __launch_bounds__(kThreads)
     k7_count(const uint64_t* __restrict__ keys, uint64_t count, const uint64_t* __restrict__ splitters,
-             uint32_t parts, uint32_t* __restrict__ counts, unsigned long long* bmin,
-             unsigned long long* bmax) {
+             uint32_t parts, uint32_t* __restrict__ counts) {
     __shared__ uint64_t s_spl[kMaxParts];
     __shared__ uint32_t s_cnt[kMaxParts];
-    __shared__ unsigned long long s_min[kMaxParts], s_max[kMaxParts];
     for (uint32_t i = threadIdx.x; i < kMaxParts; i += kThreads) {
         s_spl[i] = i + 1 < parts ? splitters[i] : ~0ull;
         s_cnt[i] = 0;
-        s_min[i] = ~0ull;
-        s_max[i] = 0;
     }
-    __syncthreads();
     const uint64_t base = (uint64_t)blockIdx.x * kTile;
+    const uint32_t tn = (uint32_t)(count - base < (uint64_t)kTile ? count - base : kTile);
+    uint64_t k[kItems];
+#pragma unroll
     for (int i = 0; i < kItems; ++i) {
-        const uint64_t idx = base + (uint64_t)i * kThreads + threadIdx.x;
-        if (idx < count) {
-            const uint64_t k = keys[idx];
-            const uint32_t b = bucket_of(k, s_spl, parts - 1);
-            atomicAdd(&s_cnt[b], 1u);
-            atomicMin(&s_min[b], (unsigned long long)k);
-            atomicMax(&s_max[b], (unsigned long long)k);
-        }
+        const uint32_t j = (uint32_t)i * kThreads + threadIdx.x;
+        k[i] = j < tn ? keys[base + j] : 0ull;
     }
     __syncthreads();
-    for (uint32_t b = threadIdx.x; b < parts; b += kThreads) {
+#pragma unroll
+    for (int i = 0; i < kItems; ++i)
+        if ((uint32_t)i * kThreads + threadIdx.x < tn)
+            atomicAdd(&s_cnt[bucket_of(k[i], s_spl, parts - 1)], 1u);
+    __syncthreads();
+    for (uint32_t b = threadIdx.x; b < parts; b += kThreads)
         counts[(uint64_t)blockIdx.x * parts + b] = s_cnt[b];
-        if (s_cnt[b]) {
-            atomicMin(&bmin[b], s_min[b]);
-            atomicMax(&bmax[b], s_max[b]);
-        }
-    }
 }
 
 // Evenly spaced sample of keys[0..count) (splitter selection).
@@ -118,55 +134,72 @@ __global__ void k7_scan(uint32_t* __restrict__ counts, uint32_t tiles, uint32_t 
     if (threadIdx.x == 0) totals[b] = s_carry;
 }
 
+// One block: padded segment starts (segments begin on `align`-element boundaries), the
+// sentinel column {0, 0} in the padding slots, and each segment's key bounds: segment b
+// holds keys in [splitter[b-1], splitter[b]) within the local range [kmin, kmax].
+__global__ void k7_layout(const uint64_t* __restrict__ totals, const uint64_t* __restrict__ splitters,
+                          uint32_t parts, uint32_t align, uint64_t kmin, uint64_t kmax,
+                          uint64_t* __restrict__ starts, uint64_t* __restrict__ bminmax,
+                          uint64_t* __restrict__ keys_out, uint32_t* __restrict__ vals_out) {
+    __shared__ uint64_t s_start[kMaxParts + 1];
+    if (threadIdx.x == 0) {
+        uint64_t acc = 0;
+        for (uint32_t b = 0; b < parts; ++b) {
+            s_start[b] = acc;
+            acc += (totals[b] + align - 1) / align * align;
+        }
+        s_start[parts] = acc;
+    }
+    __syncthreads();
+    for (uint32_t b = threadIdx.x; b < parts; b += blockDim.x) {
+        starts[b] = s_start[b];
+        const uint64_t lo = b > 0 && splitters[b - 1] > kmin ? splitters[b - 1] : kmin;
+        const uint64_t hi = b + 1 < parts && splitters[b] - 1 < kmax ? splitters[b] - 1 : kmax;
+        bminmax[b] = lo;
+        bminmax[parts + b] = hi;
+        for (uint64_t q = s_start[b] + totals[b]; q < s_start[b + 1]; ++q) {
+            keys_out[q] = 0;
+            vals_out[q] = 0;
+        }
+    }
+}
+
 // Stable scatter of one 4096-element tile into its segments: ranks from per-warp shared
 // histograms (ATOMS lane order = stable), the tile staged in shared memory in segment order,
 // then written out so consecutive threads write consecutive positions of each segment run.
-__global__ void __launch_bounds__(kThreads)
+__global__ void __launch_bounds__(kThreads, 3)
     k7_scatter(const uint64_t* __restrict__ keys, const uint32_t* __restrict__ vals, uint64_t count,
                const uint64_t* __restrict__ splitters, uint32_t parts,
-               const uint32_t* __restrict__ offsets, const uint64_t* __restrict__ totals,
-               uint64_t* __restrict__ keys_out, uint32_t* __restrict__ vals_out,
-               uint32_t align) {
+               const uint32_t* __restrict__ offsets, const uint64_t* __restrict__ starts,
+               uint64_t* __restrict__ keys_out, uint32_t* __restrict__ vals_out) {
     __shared__ uint64_t s_spl[kMaxParts];
     __shared__ uint32_t s_whist[kWarps][kMaxParts];
     __shared__ uint32_t s_tstart[kMaxParts];
     __shared__ uint64_t s_base[kMaxParts];  // global position of this tile's first element of b
+    __shared__ uint32_t s_scan[kWarps];
     extern __shared__ __align__(16) uint64_t sc_dyn[];
     uint64_t* s_k = sc_dyn;                                                 // [kTile]
     uint32_t* s_v = reinterpret_cast<uint32_t*>(sc_dyn + kTile);            // [kTile]
-    uint16_t* s_b = reinterpret_cast<uint16_t*>(s_v + kTile);               // [kTile]
-    for (uint32_t i = threadIdx.x; i < kMaxParts; i += kThreads) {
-        s_spl[i] = i + 1 < parts ? splitters[i] : ~0ull;
-        for (int w = 0; w < kWarps; ++w) s_whist[w][i] = 0;
-    }
-    if (threadIdx.x == 0) {
-        // segment b starts at the sum of the earlier totals, each rounded up to `align`
-        // elements; block 0 fills the padding slots with the sentinel column {0, 0} (a cycle)
-        uint64_t acc = 0;
-        for (uint32_t b = 0; b < parts; ++b) {
-            s_base[b] = acc + offsets[(uint64_t)blockIdx.x * parts + b];
-            const uint64_t padded = (totals[b] + align - 1) / align * align;
-            if (blockIdx.x == 0)
-                for (uint64_t q = acc + totals[b]; q < acc + padded; ++q) {
-                    keys_out[q] = 0;
-                    vals_out[q] = 0;
-                }
-            acc += padded;
-        }
-    }
-    __syncthreads();
-    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    uint8_t* s_b = reinterpret_cast<uint8_t*>(s_v + kTile);                 // [kTile]
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const uint64_t tile0 = (uint64_t)blockIdx.x * kTile;
     const uint32_t tn = (uint32_t)(count - tile0 < (uint64_t)kTile ? count - tile0 : kTile);
     const uint32_t wofs = warp * (32 * kItems) + lane;
     uint64_t kk[kItems];
-    uint32_t vv[kItems], bk[kItems], rk[kItems];
+    uint32_t vv[kItems];
 #pragma unroll
     for (int i = 0; i < kItems; ++i) {  // all loads in flight first
         const uint32_t pos = wofs + 32 * i;
         kk[i] = pos < tn ? keys[tile0 + pos] : 0ull;
         vv[i] = pos < tn ? vals[tile0 + pos] : 0u;
     }
+    // kThreads == kMaxParts: thread b owns bucket b in the per-bucket steps
+    s_spl[tid] = (uint32_t)tid + 1 < parts ? splitters[tid] : ~0ull;
+    const uint64_t my_base = (uint32_t)tid < parts ? starts[tid] + offsets[(uint64_t)blockIdx.x * parts + tid] : 0ull;
+#pragma unroll
+    for (int w = 0; w < kWarps; ++w) s_whist[w][tid] = 0;
+    __syncthreads();
+    uint32_t bk[kItems], rk[kItems];
 #pragma unroll
     for (int i = 0; i < kItems; ++i) {
         const uint32_t pos = wofs + 32 * i;
@@ -176,42 +209,38 @@ __global__ void __launch_bounds__(kThreads)
         rk[i] = pos < tn ? atomicAdd(&s_whist[warp][bk[i]], 1u) : 0u;
     }
     __syncthreads();
-    if (threadIdx.x < kMaxParts) {
-        const uint32_t b = threadIdx.x;
-        uint32_t acc = 0;
-        for (int w = 0; w < kWarps; ++w) {
-            const uint32_t c = s_whist[w][b];
-            s_whist[w][b] = acc;
-            acc += c;
-        }
-        s_tstart[b] = acc;  // tile count of b (scanned below)
+    uint32_t acc = 0;
+#pragma unroll
+    for (int w = 0; w < kWarps; ++w) {
+        const uint32_t c = s_whist[w][tid];
+        s_whist[w][tid] = acc;
+        acc += c;
     }
-    __syncthreads();
-    if (threadIdx.x == 0) {
-        uint32_t acc = 0;
-        for (uint32_t b = 0; b < parts; ++b) {
-            const uint32_t c = s_tstart[b];
-            s_tstart[b] = acc;
-            acc += c;
-        }
-    }
+    const uint32_t tstart = block_scan_256(acc, s_scan, nullptr);
+    s_tstart[tid] = tstart;
+    s_base[tid] = my_base - tstart;  // global position of tile slot p of bucket b = base + p
+#pragma unroll
+    for (int w = 0; w < kWarps; ++w) s_whist[w][tid] += tstart;
     __syncthreads();
 #pragma unroll
     for (int i = 0; i < kItems; ++i) {
         const uint32_t pos = wofs + 32 * i;
         if (pos < tn) {
-            const uint32_t dst = s_tstart[bk[i]] + s_whist[warp][bk[i]] + rk[i];
+            const uint32_t dst = s_whist[warp][bk[i]] + rk[i];
             s_k[dst] = kk[i];
             s_v[dst] = vv[i];
-            s_b[dst] = (uint16_t)bk[i];
+            s_b[dst] = (uint8_t)bk[i];
         }
     }
     __syncthreads();
-    for (uint32_t p = threadIdx.x; p < tn; p += kThreads) {
-        const uint32_t b = s_b[p];
-        const uint64_t dst = s_base[b] + (p - s_tstart[b]);
-        keys_out[dst] = s_k[p];
-        vals_out[dst] = s_v[p];
+#pragma unroll 4
+    for (int i = 0; i < kItems; ++i) {
+        const uint32_t p = (uint32_t)i * kThreads + tid;
+        if (p < tn) {
+            const uint64_t dst = s_base[s_b[p]] + p;
+            keys_out[dst] = s_k[p];
+            vals_out[dst] = s_v[p];
+        }
     }
 }
 
@@ -220,30 +249,33 @@ __global__ void __launch_bounds__(kThreads)
 int launch_partition(const uint64_t* keys, const uint32_t* vals, uint64_t count,
                      const uint64_t* d_splitters, uint32_t parts, uint32_t* d_counts_scratch,
                      uint64_t* d_totals, uint64_t* d_bminmax, uint64_t* keys_out,
-                     uint32_t* vals_out, cudaStream_t s, uint32_t align) {
+                     uint32_t* vals_out, cudaStream_t s, uint32_t align, uint64_t kmin,
+                     uint64_t kmax) {
+    static_assert(kThreads == kMaxParts, "one thread per bucket in k7_scatter");
     if (parts < 1 || parts > (uint32_t)kMaxParts) return -1;
     const uint64_t tiles = (count + kTile - 1) / kTile;
-    cudaMemsetAsync(d_bminmax, 0xFF, sizeof(uint64_t) * parts, s);
-    cudaMemsetAsync(d_bminmax + parts, 0, sizeof(uint64_t) * parts, s);
     if (tiles == 0) {
         cudaMemsetAsync(d_totals, 0, sizeof(uint64_t) * parts, s);
-        return 1;
+        k7_layout<<<1, 256, 0, s>>>(d_totals, d_splitters, parts, align, kmin, kmax,
+                                    d_totals + parts, d_bminmax, keys_out, vals_out);
+        return 2;
     }
-    k7_count<<<(unsigned)tiles, kThreads, 0, s>>>(
-        keys, count, d_splitters, parts, d_counts_scratch,
-        reinterpret_cast<unsigned long long*>(d_bminmax),
-        reinterpret_cast<unsigned long long*>(d_bminmax + parts));
+    k7_count<<<(unsigned)tiles, kThreads, 0, s>>>(keys, count, d_splitters, parts,
+                                                  d_counts_scratch);
     k7_scan<<<parts, 1024, 0, s>>>(d_counts_scratch, (uint32_t)tiles, parts, d_totals);
-    constexpr size_t kScSmem = (size_t)kTile * (8 + 4 + 2);
+    // d_totals has room for 2 * parts words: [totals | segment starts]
+    k7_layout<<<1, 256, 0, s>>>(d_totals, d_splitters, parts, align, kmin, kmax,
+                                d_totals + parts, d_bminmax, keys_out, vals_out);
+    constexpr size_t kScSmem = (size_t)kTile * (8 + 4 + 1);
     static bool configured = false;
     if (!configured) {
         cudaFuncSetAttribute(k7_scatter, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kScSmem);
         configured = true;
     }
     k7_scatter<<<(unsigned)tiles, kThreads, kScSmem, s>>>(keys, vals, count, d_splitters, parts,
-                                                    d_counts_scratch, d_totals, keys_out,
-                                                    vals_out, align);
-    return 3;
+                                                          d_counts_scratch, d_totals + parts,
+                                                          keys_out, vals_out);
+    return 4;
 }
 
 int launch_sample(const uint64_t* keys, uint64_t count, uint64_t s, uint64_t* out, cudaStream_t st) {

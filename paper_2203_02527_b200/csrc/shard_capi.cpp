@@ -38,6 +38,7 @@ struct ShardScratch {
     uint32_t* d_cand_uv = nullptr;  // candidate columns of this rank
     uint64_t cand_cap = 0;
     uint64_t local_count = 0;       // edges produced by shard_distances
+    uint64_t local_kmin = 0, local_kmax = 0;
 };
 
 ShardScratch& scratch(Context* c) {
@@ -89,6 +90,8 @@ int ph0b_shard_distances(ph0b_context* ctx, const double* dX, uint64_t n, uint64
     ph0b::capi_set_launches(c->launches);
     if (!s.good()) return ph0b::capi_fail(s);
     scratch(c).local_count = cnt;
+    scratch(c).local_kmin = lo;
+    scratch(c).local_kmax = hi;
     if (count) *count = cnt;
     if (kmin) *kmin = lo;
     if (kmax) *kmax = hi;
@@ -125,7 +128,7 @@ int ph0b_shard_partition(ph0b_context* ctx, const uint64_t* splitters, uint32_t 
     if (!sc.d_spl) {
         if ((rc = ensure(reinterpret_cast<void**>(&sc.d_spl), &cap, 256 * 8))) return rc;
         cap = 0;
-        if ((rc = ensure(reinterpret_cast<void**>(&sc.d_totals), &cap, 256 * 8))) return rc;
+        if ((rc = ensure(reinterpret_cast<void**>(&sc.d_totals), &cap, 512 * 8))) return rc;
         cap = 0;
         if ((rc = ensure(reinterpret_cast<void**>(&sc.d_bminmax), &cap, 512 * 8))) return rc;
     }
@@ -137,7 +140,7 @@ int ph0b_shard_partition(ph0b_context* ctx, const uint64_t* splitters, uint32_t 
         return ph0b::capi_fail(PH0B_ERR_CUDA, "H2D splitters");
     c->launches = ph0b::launch_partition(c->keys(0), c->vals(0), sc.local_count, sc.d_spl, parts,
                                          sc.d_counts, sc.d_totals, sc.d_bminmax, c->keys(1),
-                                         c->vals(1), st);
+                                         c->vals(1), st, 1, sc.local_kmin, sc.local_kmax);
     ph0b::capi_set_launches(c->launches);
     std::vector<uint64_t> mm(2 * parts);
     if (cudaGetLastError() != cudaSuccess ||

@@ -423,18 +423,21 @@ __global__ void __launch_bounds__(kUThreads, 3)
             main_tot += s_warp_tot[w];
         }
         const uint32_t tile_tot = main_tot + (low_bits ? s_ext_tot : 0u);
-        if (tid == 0) {
+        if (warp == 0) {  // warp-wide look-back: 32 predecessors per round trip
             uint64_t* my = status + tile;
             uint32_t excl = 0;
             if (tile == 0) {
-                st_relaxed_u64(my, pack_status(kStateInclusive, epoch, tile_tot));
+                if (lane == 0) st_relaxed_u64(my, pack_status(kStateInclusive, epoch, tile_tot));
             } else {
-                st_relaxed_u64(my, pack_status(kStateAggregate, epoch, tile_tot));
-                excl = lookback_window<8>(status, 1, tile, epoch);
-                st_relaxed_u64(my, pack_status(kStateInclusive, epoch, excl + tile_tot));
+                if (lane == 0) st_relaxed_u64(my, pack_status(kStateAggregate, epoch, tile_tot));
+                excl = lookback_warp(status, 1, tile, epoch, lane);
+                if (lane == 0)
+                    st_relaxed_u64(my, pack_status(kStateInclusive, epoch, excl + tile_tot));
             }
-            s_prefix = base0 + excl;
-            if (tile == num_tiles - 1) *n_scale = base0 + (uint64_t)excl + tile_tot;
+            if (lane == 0) {
+                s_prefix = base0 + excl;
+                if (tile == num_tiles - 1) *n_scale = base0 + (uint64_t)excl + tile_tot;
+            }
         }
         __syncthreads();
         const uint64_t base = s_prefix;
