@@ -52,6 +52,9 @@ extern "C" {
 
 /* ph0b_options.flags */
 #define PH0B_FLAG_NO_SCALE 0x1u   /* do not copy D back (n_scale is still reported) */
+#define PH0B_FLAG_KRUSKAL 0x2u    /* barcode by union-find over the filtration (the reference's
+                                     kruskal_barcode, oracle.cpp:32-46) instead of the column
+                                     reduction; same result (acceptance.cpp:79-90) */
 
 typedef struct ph0b_options {
     uint32_t struct_size; /* sizeof(ph0b_options); 0 = all defaults */
@@ -94,6 +97,13 @@ typedef struct ph0b_result {
  * ph0b_result_free).  Replaces the five-call composition above. */
 int ph0b_h0_barcode(const double* X, uint64_t n, uint64_t d, uint32_t layout,
                     const ph0b_options* opt, ph0b_result* out);
+
+/* Replaces kruskal_barcode(build_filtration(pairwise_distances(cloud)), n)
+ * (oracle.cpp:32-46, the `oracle` subcommand of ph0_cli.cpp:73-80): the same filtration on
+ * the GPU, then a GPU union-find in filtration order with early stop at n-1 merges.  Equal
+ * to ph0b_h0_barcode with PH0B_FLAG_KRUSKAL. */
+int ph0b_kruskal_barcode(const double* X, uint64_t n, uint64_t d, uint32_t layout,
+                         const ph0b_options* opt, ph0b_result* out);
 void ph0b_result_free(ph0b_result* r);
 
 /* Same, writing into caller-provided host buffers (no allocation inside the call; pinned
@@ -198,6 +208,14 @@ uint64_t ph0b_last_launch_count(void);
  *       2 = noisy unit circle (z=0 plane) + n_background uniform points in [lo,hi]^d (C2);
  *       3 = two equal Gaussian clusters centred at (lo,..,lo) and (hi,..,hi) (config C1).
  * All randomness is SplitMix64 (splitmix64.hpp:20-43). */
+/* Replaces generate_uniform_cloud(n, dim, seed) (point_cloud.cpp:20-29) on the device: the
+ * identical SplitMix64 stream (jumpable, zero draws rejected exactly as next_unit_open does),
+ * written column-major into d_out (n*dim doubles, device memory) on `stream` (NULL: the
+ * context's stream).  n > 0 with dim < 1 -> PH0B_ERR_INVALID_ARGUMENT, "point dimension
+ * must be at least 1" (point_cloud.cpp:21-22). */
+int ph0b_generate_uniform_cloud_device(ph0b_context* ctx, uint64_t n, uint64_t dim,
+                                       uint64_t seed, double* d_out, void* stream);
+
 int ph0b_generate_cloud(uint32_t kind, uint64_t n, uint64_t d, uint64_t seed, uint32_t clusters,
                         double sigma, double lo, double hi, uint64_t n_background,
                         double* out_colmajor);

@@ -135,6 +135,23 @@ inline Barcode h0_barcode(const double* x, std::size_t n, std::size_t d,
     return bc;
 }
 
+// kruskal_barcode (oracle.cpp:32-46): union-find over the GPU filtration (ph0b_kruskal_barcode).
+inline Barcode kruskal_barcode(const double* x, std::size_t n, std::size_t d,
+                               std::vector<double>* scale = nullptr, int device = 0) {
+    ph0b_options o = detail::opts({}, device);
+    if (!scale) o.flags |= PH0B_FLAG_NO_SCALE;
+    ph0b_result r{};
+    detail::check(ph0b_kruskal_barcode(x, n, d, PH0B_COL_MAJOR, &o, &r));
+    Barcode bc;
+    bc.finite.resize(r.n_finite);
+    for (std::uint64_t i = 0; i < r.n_finite; ++i)
+        bc.finite[i] = {0.0, r.death_grade[i], r.death_length[i]};
+    bc.essential_count = r.essential_count;
+    if (scale) scale->assign(r.scale, r.scale + r.n_scale);
+    ph0b_result_free(&r);
+    return bc;
+}
+
 // Claimed low of every surviving column (reduction.cpp:44-45), filtration order.
 inline std::vector<std::uint32_t> claimed_lows(const double* x, std::size_t n, std::size_t d,
                                                int device = 0) {

@@ -184,6 +184,32 @@ int ph0b_run_device(ph0b_context* ctx, const double* dX, uint64_t n, uint64_t d,
     return PH0B_OK;
 }
 
+int ph0b_generate_uniform_cloud_device(ph0b_context* ctx, uint64_t n, uint64_t dim,
+                                       uint64_t seed, double* d_out, void* stream) {
+    if (!ctx) return fail(PH0B_ERR_INVALID_ARGUMENT, "null context");
+    if (n > 0 && dim < 1)
+        return fail(PH0B_ERR_INVALID_ARGUMENT, "point dimension must be at least 1");
+    if (n * dim == 0) return PH0B_OK;
+    if (!d_out) return fail(PH0B_ERR_INVALID_ARGUMENT, "null output");
+    Context* c = reinterpret_cast<Context*>(ctx);
+    std::lock_guard<std::mutex> lk(c->mu);
+    cudaSetDevice(c->device());
+    cudaStream_t s = stream ? static_cast<cudaStream_t>(stream) : c->own_stream();
+    unsigned long long *dz = nullptr, *hz = nullptr;
+    if (cudaMalloc(&dz, 65 * 8) != cudaSuccess || cudaMallocHost(&hz, 65 * 8) != cudaSuccess) {
+        if (dz) cudaFree(dz);
+        cudaGetLastError();
+        return fail(PH0B_ERR_OUT_OF_MEMORY, "generator scratch");
+    }
+    const int l = ph0b::launch_uniform_cloud(n, dim, seed, d_out, dz, hz, s, c->num_sms());
+    cudaFree(dz);
+    cudaFreeHost(hz);
+    g_last_launches = l > 0 ? (uint64_t)l : 0;
+    if (l == -2) return fail(PH0B_ERR_INVALID_ARGUMENT, "more than 64 zero draws (impossible in practice)");
+    if (l < 0 || cudaGetLastError() != cudaSuccess) return fail(PH0B_ERR_CUDA, "generator kernel");
+    return PH0B_OK;
+}
+
 int ph0b_run_host(ph0b_context* ctx, const double* X, uint64_t n, uint64_t d, uint32_t layout,
                   void* stream, uint64_t* death_grade, double* death_length, uint64_t* n_finite,
                   uint64_t* essential_count, double* scale, uint64_t scale_capacity,
@@ -248,7 +274,9 @@ int ph0b_h0_barcode(const double* X, uint64_t n, uint64_t d, uint32_t layout,
     std::lock_guard<std::mutex> lk(c->mu);
     cudaStream_t s = c->own_stream();
     RunOutputs r;
+    c->kruskal_mode = (o.flags & PH0B_FLAG_KRUSKAL) != 0;
     Status st = c->run_host_input(X, n, d, layout, s, StopAfter::Barcode, false, &r);
+    c->kruskal_mode = false;
     g_last_launches = c->launches;
     if (!st.good()) return fail(st);
     const bool want_scale = !(o.flags & PH0B_FLAG_NO_SCALE);
@@ -270,6 +298,20 @@ int ph0b_h0_barcode(const double* X, uint64_t n, uint64_t d, uint32_t layout,
     out->n_scale = r.n_scale;
     out->times = r.times;
     return PH0B_OK;
+}
+
+int ph0b_kruskal_barcode(const double* X, uint64_t n, uint64_t d, uint32_t layout,
+                         const ph0b_options* opt, ph0b_result* out) {
+    ph0b_options o{};
+    if (opt && opt->struct_size != 0) {
+        o = *opt;
+    } else {  // all defaults (struct_size 0 means defaults, as in parse())
+        o.struct_size = sizeof(o);
+        o.workers = 1;
+        o.pivoting = 1;
+    }
+    o.flags |= PH0B_FLAG_KRUSKAL;
+    return ph0b_h0_barcode(X, n, d, layout, &o, out);
 }
 
 void ph0b_result_free(ph0b_result* r) {

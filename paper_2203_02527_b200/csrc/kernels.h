@@ -108,6 +108,19 @@ struct ReduceStats {
 int run_reduction(ReduceState& st, cudaStream_t s, int num_sms, uint32_t& epoch,
                   ReduceStats* stats);
 
+// ---- K8: on-device generate_uniform_cloud (generate.cu) --------------------------------
+// returns launches (>0), -1 on a CUDA error, -2 if more than 64 zero draws were met
+int launch_uniform_cloud(uint64_t n, uint64_t dim, uint64_t seed, double* d_out,
+                         unsigned long long* d_zeros, unsigned long long* h_zeros,
+                         cudaStream_t s, int num_sms);
+
+// ---- K6: GPU Kruskal oracle (kruskal.cu) ----------------------------------------------
+size_t kruskal_smem_bytes();
+int launch_kruskal(const uint32_t* uv, const uint64_t* sorted_keys, uint64_t count, uint32_t n,
+                   const double* D, const uint64_t* n_scale, uint32_t* accepted,
+                   uint32_t* n_accepted, uint64_t* death_grade, double* death_length,
+                   cudaStream_t s);
+
 // ---- K5: barcode collect (collect.cu) --------------------------------------------------
 // cols_sorted: survivor column ids in filtration order (u64, from the keys-only sort).
 // Writes surv_sorted (u32), death_grade = 1 + lower_bound(D, length), death_length.

@@ -457,7 +457,16 @@ Status Context::run(const double* dX, uint64_t n, uint64_t d, uint32_t layout,
     r.d_grade = want_grade ? grade_ : nullptr;
     r.d_scale = scale_;
 
-    if (stop == StopAfter::Barcode) {
+    if (stop == StopAfter::Barcode && kruskal_mode) {
+        uint32_t m = 0;
+        s = stage_kruskal(k, (uint32_t)n, st, &m);
+        if (!s.good()) return s;
+        PH0B_TRY(cudaEventRecord(ev_[4], st), "event");
+        r.d_death_grade = death_grade_;
+        r.d_death_length = death_length_;
+        r.n_finite = m;
+        r.essential = n - m;
+    } else if (stop == StopAfter::Barcode) {
         // ---- K4: column reduction ----------------------------------------------------------
         ReduceStats rst;
         s = stage_reduce(vals_[cur_], k, (uint32_t)n, st, &rst);
@@ -601,15 +610,21 @@ Status Context::run_host_overlapped(const double* X, uint64_t n, uint64_t d, uin
     scale_ = dbuf_;
     PH0B_TRY(cudaMemcpyAsync(small_ + 2, d_base + B, 8, cudaMemcpyDefault, st), "copy");
 
-    // ---- K4 + K5 on the whole (now sorted) matrix ------------------------------------------
+    // ---- K4 + K5 (or the union-find oracle) on the whole (now sorted) matrix -------------
     ReduceStats rst;
-    if (!(s = stage_reduce(vals_[cur_], kpad, (uint32_t)n, st, &rst)).good()) return s;
-    PH0B_TRY(cudaEventRecord(ev_[4], st), "event");
-    const uint32_t m = rst.survivors;
-    if (m != n - 1)
-        return {PH0B_ERR_CUDA, "internal error: reduction produced " + std::to_string(m) +
-                                   " surviving columns, expected " + std::to_string(n - 1)};
-    if (!(s = stage_collect(m, kpad, 0, st)).good()) return s;
+    uint32_t m = 0;
+    if (kruskal_mode) {
+        if (!(s = stage_kruskal(kpad, (uint32_t)n, st, &m)).good()) return s;
+        PH0B_TRY(cudaEventRecord(ev_[4], st), "event");
+    } else {
+        if (!(s = stage_reduce(vals_[cur_], kpad, (uint32_t)n, st, &rst)).good()) return s;
+        PH0B_TRY(cudaEventRecord(ev_[4], st), "event");
+        m = rst.survivors;
+        if (m != n - 1)
+            return {PH0B_ERR_CUDA, "internal error: reduction produced " + std::to_string(m) +
+                                       " surviving columns, expected " + std::to_string(n - 1)};
+        if (!(s = stage_collect(m, kpad, 0, st)).good()) return s;
+    }
     PH0B_TRY(cudaEventRecord(ev_[5], st), "event");
     PH0B_TRY(cudaStreamSynchronize(st), "pipeline");
     PH0B_TRY(cudaStreamSynchronize(copy_stream_), "D2H scale");
@@ -629,6 +644,19 @@ Status Context::run_host_overlapped(const double* X, uint64_t n, uint64_t d, uin
     cudaEventElapsedTime(&r.times.collect_ms, ev_[4], ev_[5]);
     cudaEventElapsedTime(&r.times.total_ms, ev_[0], ev_[5]);
     if (out) *out = r;
+    return Status::ok();
+}
+
+Status Context::stage_kruskal(uint64_t count, uint32_t n, cudaStream_t st, uint32_t* merges) {
+    if (n > 65536) return {PH0B_ERR_TOO_LARGE, "union-find forest is limited to 65536 points"};
+    uint32_t* d_count = reinterpret_cast<uint32_t*>(d_mapped_ + 250);
+    volatile uint32_t* h_count = reinterpret_cast<volatile uint32_t*>(h_mapped_ + 250);
+    *h_count = 0;
+    launches += launch_kruskal(vals_[cur_], keys_[cur_], count, n, scale_, small_ + 2, surv_,
+                               d_count, death_grade_, death_length_, st);
+    PH0B_CHECK_LAUNCH("kruskal");
+    PH0B_TRY(cudaStreamSynchronize(st), "kruskal");
+    *merges = *h_count;
     return Status::ok();
 }
 

@@ -75,6 +75,9 @@ public:
                                cudaStream_t st, double* host_scale, uint64_t scale_capacity,
                                RunOutputs* out);
     Status stage_collect(uint32_t m, uint64_t count, uint64_t grade_offset, cudaStream_t st);
+    // Barcode by the GPU union-find (Kruskal) over the sorted columns instead of K4 + K5.
+    Status stage_kruskal(uint64_t count, uint32_t n, cudaStream_t st, uint32_t* merges);
+    bool kruskal_mode = false;  // set by the C entry points (under mu) for one run
     Status reserve_edges(uint64_t count);  // ping-pong key/column buffers for count edges
     Status reserve_points(uint64_t n, uint64_t d);
     Status reserve_recv(uint64_t count);   // sharded receive side: buffer 0 only

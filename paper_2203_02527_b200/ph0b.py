@@ -26,6 +26,7 @@ PH0B_ERR_CAPACITY = 7
 COL_MAJOR = 0
 ROW_MAJOR = 1
 FLAG_NO_SCALE = 1
+FLAG_KRUSKAL = 2
 
 EXPORTED_SYMBOLS = [
     "ph0b_h0_barcode", "ph0b_result_free", "ph0b_h0_barcode_into", "ph0b_pairwise_distances",
@@ -34,7 +35,7 @@ EXPORTED_SYMBOLS = [
     "ph0b_last_error", "ph0b_abi_version", "ph0b_host_alloc", "ph0b_host_free",
     "ph0b_last_launch_count", "ph0b_generate_cloud", "ph0b_shard_distances", "ph0b_shard_sample",
     "ph0b_shard_partition", "ph0b_shard_recv", "ph0b_shard_sort_unique", "ph0b_shard_reduce",
-    "ph0b_reduce_columns",
+    "ph0b_reduce_columns", "ph0b_kruskal_barcode", "ph0b_generate_uniform_cloud_device",
 ]
 
 
@@ -90,6 +91,9 @@ def lib() -> C.CDLL:
     sig = {
         "ph0b_h0_barcode": (C.c_int, [vp, u64, u64, u32, C.POINTER(Options), C.POINTER(Result)]),
         "ph0b_result_free": (None, [C.POINTER(Result)]),
+        "ph0b_kruskal_barcode": (C.c_int, [vp, u64, u64, u32, C.POINTER(Options),
+                                           C.POINTER(Result)]),
+        "ph0b_generate_uniform_cloud_device": (C.c_int, [vp, u64, u64, u64, vp, vp]),
         "ph0b_h0_barcode_into": (C.c_int, [vp, u64, u64, u32, C.POINTER(Options), vp, vp, u64p,
                                            u64p, vp, u64, u64p, C.POINTER(StageTimes)]),
         "ph0b_pairwise_distances": (C.c_int, [vp, u64, u64, u32, C.POINTER(Options), vp]),
@@ -161,14 +165,37 @@ class Barcode:
 
 
 def h0_barcode(X, *, device: int = 0, return_scale: bool = True, workers: int = 1,
-               pivoting: bool = True) -> Barcode:
-    """pairwise_distances ∘ build_filtration ∘ build_boundary_matrix ∘ reduce ∘ extract_barcode."""
+               pivoting: bool = True, kruskal: bool = False) -> Barcode:
+    """pairwise_distances ∘ build_filtration ∘ build_boundary_matrix ∘ reduce ∘ extract_barcode
+    (kruskal=True: the union-find barcode of oracle.cpp:32-46 over the same GPU filtration)."""
     Xf, n, d = _as_cloud(X)
     L = lib()
     res = Result()
-    opt = _opts(device, 0 if return_scale else FLAG_NO_SCALE, workers, pivoting)
+    flags = (0 if return_scale else FLAG_NO_SCALE) | (FLAG_KRUSKAL if kruskal else 0)
+    opt = _opts(device, flags, workers, pivoting)
     rc = L.ph0b_h0_barcode(_ptr(Xf), n, d, COL_MAJOR, C.byref(opt), C.byref(res))
     _check(rc)
+    try:
+        m = res.n_finite
+        g = np.ctypeslib.as_array(res.death_grade, (m,)).copy() if m else np.zeros(0, np.uint64)
+        ln = np.ctypeslib.as_array(res.death_length, (m,)).copy() if m else np.zeros(0)
+        sc = None
+        if return_scale:
+            sc = (np.ctypeslib.as_array(res.scale, (res.n_scale,)).copy() if res.n_scale
+                  else np.zeros(0))
+        return Barcode(g, ln, int(res.essential_count), sc, res.times.as_dict())
+    finally:
+        L.ph0b_result_free(C.byref(res))
+
+
+def kruskal_barcode(X, *, device: int = 0, return_scale: bool = True) -> Barcode:
+    """kruskal_barcode(build_filtration(pairwise_distances(X)), n) (oracle.cpp:32-46) on the
+    GPU: the ph0b_kruskal_barcode entry point."""
+    Xf, n, d = _as_cloud(X)
+    L = lib()
+    res = Result()
+    opt = _opts(device, 0 if return_scale else FLAG_NO_SCALE)
+    _check(L.ph0b_kruskal_barcode(_ptr(Xf), n, d, COL_MAJOR, C.byref(opt), C.byref(res)))
     try:
         m = res.n_finite
         g = np.ctypeslib.as_array(res.death_grade, (m,)).copy() if m else np.zeros(0, np.uint64)
@@ -265,6 +292,13 @@ class Context:
 
     def reserve(self, n: int, d: int):
         _check(lib().ph0b_context_reserve(self._h, n, d))
+
+    def generate_uniform_cloud(self, n: int, dim: int, seed: int, d_out_ptr: int,
+                               stream: int = 0):
+        """generate_uniform_cloud (point_cloud.cpp:20-29) on the device, column-major."""
+        _check(lib().ph0b_generate_uniform_cloud_device(self._h, n, dim, seed,
+                                                        C.c_void_p(d_out_ptr),
+                                                        C.c_void_p(stream or None)))
 
     @property
     def workspace_bytes(self) -> int:

@@ -222,6 +222,12 @@ TEST_CASE("acceptance: oracle equivalence and bar-count law on 200 clouds") {  /
         const ph0b::Filtration f = ph0b::build_filtration(c.x.data(), c.n, c.d);
         const ph0b::Barcode oracle = kruskal(f, n);
         CHECK(ph0b::finite_death_grades(bc) == ph0b::finite_death_grades(oracle));
+        const ph0b::Barcode gpu_oracle = ph0b::kruskal_barcode(c.x.data(), c.n, c.d);
+        REQUIRE(gpu_oracle.finite.size() == bc.finite.size());
+        for (std::size_t j = 0; j < bc.finite.size(); ++j) {  // ordered, not just multisets
+            CHECK(gpu_oracle.finite[j].death_grade == bc.finite[j].death_grade);
+            CHECK(gpu_oracle.finite[j].death_length == bc.finite[j].death_length);
+        }
         CHECK(bc.finite.size() == n - 1);
         CHECK(bc.essential_count == 1);
         CHECK(scale == f.scale);
