@@ -12,12 +12,14 @@
 #include <cstdint>
 #include <cstring>
 #include <exception>
+#include <sstream>
 #include <string>
 #include <vector>
 
 #include "ph0/barcode.hpp"
 #include "ph0/boundary_matrix.hpp"
 #include "ph0/filtration.hpp"
+#include "ph0/format.hpp"
 #include "ph0/oracle.hpp"
 #include "ph0/point_cloud.hpp"
 #include "ph0/reduction.hpp"
@@ -148,6 +150,52 @@ int ref_h0_barcode(const double* x, std::uint64_t n, std::uint64_t d, int mode, 
         return 0;
     } catch (const std::exception& e) {
         g_err = e.what();
+        return 1;
+    }
+}
+
+// Text front-end of the reference CLI (ph0_cli.cpp:58-80, :199-205) without CLI11: the text a
+// `compute`/`oracle` (mode 0/1) run prints for a point file's contents, or "error: <what>\n"
+// (ph0_cli.cpp:278-281) with return 1; `generate` as write_points(generate_uniform_cloud).
+// The output is copied into out[cap] (NUL-terminated); *len receives its full length.
+static int put_text(const std::string& t, char* out, std::uint64_t cap, std::uint64_t* len) {
+    if (len) *len = t.size();
+    if (out && cap) {
+        const std::size_t k = t.size() < cap - 1 ? t.size() : cap - 1;
+        std::memcpy(out, t.data(), k);
+        out[k] = 0;
+    }
+    return 0;
+}
+
+int ref_cli_text(const char* points_text, std::uint64_t gen_n, std::uint64_t gen_dim,
+                 std::uint64_t gen_seed, int mode, int show_essential, char* out,
+                 std::uint64_t cap, std::uint64_t* len) {
+    try {
+        ph0::PointCloud cloud = [&] {
+            if (points_text) {
+                std::istringstream in(points_text);
+                return ph0::read_points(in);
+            }
+            return ph0::generate_uniform_cloud(gen_n, gen_dim, gen_seed);
+        }();
+        if (mode == 2) {
+            std::ostringstream os;
+            ph0::write_points(os, cloud);
+            return put_text(os.str(), out, cap, len);
+        }
+        const ph0::Filtration f = ph0::build_filtration(ph0::pairwise_distances(cloud));
+        ph0::Barcode bc;
+        if (mode == 1) {
+            bc = ph0::kruskal_barcode(f, static_cast<std::size_t>(cloud.size()));
+        } else {
+            ph0::BoundaryMatrix m = ph0::build_boundary_matrix(f, static_cast<std::size_t>(cloud.size()));
+            ph0::reduce(m, ph0::ReductionOptions{true, 1});
+            bc = ph0::extract_barcode(m, f);
+        }
+        return put_text(ph0::format_barcode(bc, show_essential != 0), out, cap, len);
+    } catch (const std::exception& e) {
+        put_text(std::string("error: ") + e.what() + "\n", out, cap, len);
         return 1;
     }
 }

@@ -61,7 +61,25 @@ def build_library(verbose: bool = False, force: bool = False) -> Path:
         res = subprocess.run(cmd, capture_output=True, text=True)
         if res.returncode != 0:
             raise RuntimeError(f"link failed:\n{res.stdout}\n{res.stderr}")
+    build_cli()
     return LIB
+
+
+CLI_SRC = PKG / "cli" / "ph0b_cli.cpp"
+CLI_BIN = PKG / "ph0b"
+
+
+def build_cli() -> Path:
+    """The `ph0b` front-end (generate/compute/oracle), linked against libph0b.so."""
+    deps = [CLI_SRC, LIB, ROOT / "include" / "ph0b.hpp", ROOT / "include" / "ph0b_io.hpp"]
+    if CLI_BIN.exists() and CLI_BIN.stat().st_mtime >= max(p.stat().st_mtime for p in deps):
+        return CLI_BIN
+    cmd = [os.environ.get("CXX", "g++"), "-std=c++17", "-O2", "-Wall", f"-I{ROOT / 'include'}",
+           str(CLI_SRC), "-o", str(CLI_BIN), f"-L{PKG}", "-lph0b", "-Wl,-rpath,$ORIGIN"]
+    res = subprocess.run(cmd, capture_output=True, text=True)
+    if res.returncode != 0:
+        raise RuntimeError(f"CLI build failed:\n{res.stdout}\n{res.stderr}")
+    return CLI_BIN
 
 
 if __name__ == "__main__":
