@@ -147,7 +147,11 @@ int ph0b_context_create(int device, ph0b_context** out) {
     return PH0B_OK;
 }
 
-void ph0b_context_destroy(ph0b_context* ctx) { delete reinterpret_cast<Context*>(ctx); }
+void ph0b_context_destroy(ph0b_context* ctx) {
+    if (!ctx) return;
+    ph0b::shard_scratch_release(reinterpret_cast<Context*>(ctx));
+    delete reinterpret_cast<Context*>(ctx);
+}
 
 int ph0b_context_reserve(ph0b_context* ctx, uint64_t n, uint64_t d) {
     Context* c = reinterpret_cast<Context*>(ctx);

@@ -3,6 +3,8 @@
 #include "pipeline.h"
 
 #include <algorithm>
+#include <chrono>
+#include <cstdio>
 #include <cstring>
 #include <map>
 #include <memory>
@@ -56,6 +58,25 @@ inline uint32_t truncated_plan(uint64_t span, uint32_t max_passes, SortPlan* pla
 }
 
 inline uint64_t row_base(uint64_t u, uint64_t n) { return u * (2 * n - u - 1) / 2; }
+
+// PH0B_TRACE=1: host-side timeline of the overlapped host path on stderr (diagnostics only).
+struct Trace {
+    bool on;
+    std::chrono::steady_clock::time_point t0 = std::chrono::steady_clock::now();
+    Trace() {
+        const char* e = getenv("PH0B_TRACE");
+        on = e && e[0] == '1';
+    }
+    void mark(const char* what, long a = -1) {
+        if (!on) return;
+        const double ms = std::chrono::duration<double, std::milli>(
+                              std::chrono::steady_clock::now() - t0).count();
+        if (a >= 0)
+            fprintf(stderr, "[ph0b trace] %8.2f ms %s %ld\n", ms, what, a);
+        else
+            fprintf(stderr, "[ph0b trace] %8.2f ms %s\n", ms, what);
+    }
+};
 
 uint64_t d2h_chunk_elems() {
     static const uint64_t v = [] {
@@ -518,7 +539,7 @@ Status Context::run_host_overlapped(const double* X, uint64_t n, uint64_t d, uin
     if (!(s = grow(reinterpret_cast<void**>(&part_counts_), &part_counts_cap_, part_words * 4 + 16))
              .good())
         return s;
-    if (!(s = grow(reinterpret_cast<void**>(&part_small_), &part_small_cap_, 2048 * 8)).good())
+    if (!(s = grow(reinterpret_cast<void**>(&part_small_), &part_small_cap_, 4096 * 8)).good())
         return s;
     if (!copy_stream_) PH0B_TRY(cudaStreamCreateWithFlags(&copy_stream_, cudaStreamNonBlocking),
                                 "cudaStreamCreate");
@@ -528,6 +549,7 @@ Status Context::run_host_overlapped(const double* X, uint64_t n, uint64_t d, uin
     uint64_t* d_base = d_mapped_ + 8;        // [B + 1], zero-copy host words
     volatile uint64_t* h_base = h_mapped_ + 8;
     launches = 0;
+    Trace tr;
     RunOutputs r;
     r.k = k;
     std::memset(&r.times, 0, sizeof(r.times));
@@ -537,6 +559,7 @@ Status Context::run_host_overlapped(const double* X, uint64_t n, uint64_t d, uin
     uint64_t cnt = 0, kmin = 0, kmax = 0;
     if (!(s = stage_distances(xin_, n, d, layout, 0, n, st, &cnt, &kmin, &kmax)).good()) return s;
     PH0B_TRY(cudaEventRecord(ev_[1], st), "event");
+    tr.mark("distances done");
 
     // ---- splitters from an evenly spaced sample, stable partition into B key ranges -------
     const uint64_t S = std::min<uint64_t>(k, std::min<uint64_t>(n, 16384));
@@ -555,12 +578,14 @@ Status Context::run_host_overlapped(const double* X, uint64_t n, uint64_t d, uin
     // and unique kernels); the <= 3 padding slots per segment hold the cycle column {0, 0}
     constexpr uint32_t kAlign = 4;
     launches += launch_partition(keys_[0], vals_[0], k, d_spl, B, part_counts_, d_tot, d_mm,
-                                 keys_[1], vals_[1], st, kAlign, kmin, kmax);
+                                 keys_[1], vals_[1], st, kAlign, kmin, kmax, spl.data(),
+                                 reinterpret_cast<uint16_t*>(part_small_ + 1280));
     PH0B_CHECK_LAUNCH("partition");
     std::vector<uint64_t> tot(B), mm(2 * B);
     PH0B_TRY(cudaMemcpyAsync(tot.data(), d_tot, B * 8, cudaMemcpyDeviceToHost, st), "D2H");
     PH0B_TRY(cudaMemcpyAsync(mm.data(), d_mm, 2 * B * 8, cudaMemcpyDeviceToHost, st), "D2H");
     PH0B_TRY(cudaStreamSynchronize(st), "partition");
+    tr.mark("partition done");
     h_base[0] = 0;
 
     // ---- per bucket: sort + unique into D, then stream that slice of D to the host ---------
@@ -585,6 +610,7 @@ Status Context::run_host_overlapped(const double* X, uint64_t n, uint64_t d, uin
         }
         PH0B_TRY(cudaEventRecord(ev_[6], st), "event");
         PH0B_TRY(cudaEventSynchronize(ev_[6]), "bucket");
+        tr.mark("bucket sorted", (long)b);
         const uint64_t next_base = h_base[b + 1];
         if (host_scale && next_base > host_base) {
             if (next_base > scale_capacity)
@@ -627,7 +653,9 @@ Status Context::run_host_overlapped(const double* X, uint64_t n, uint64_t d, uin
     }
     PH0B_TRY(cudaEventRecord(ev_[5], st), "event");
     PH0B_TRY(cudaStreamSynchronize(st), "pipeline");
+    tr.mark("reduce+collect done");
     PH0B_TRY(cudaStreamSynchronize(copy_stream_), "D2H scale");
+    tr.mark("D2H done");
     r.n_scale = host_base;
     r.d_uv_sorted = vals_[cur_];
     r.d_scale = dbuf_;

@@ -154,6 +154,8 @@ private:
     bool hist_valid_ = false;  // hist_ row 0 holds the raw low-byte histogram of keys_[0]
 };
 
+void shard_scratch_release(Context* c);  // shard_capi.cpp
+
 // Default per-device contexts used by the stateless C entry points.
 Context* default_context(int device, Status* st);
 

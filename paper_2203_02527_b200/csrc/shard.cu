@@ -8,6 +8,7 @@
 #include <cuda_runtime.h>
 
 #include <cstdint>
+#include <vector>
 
 #include "common.cuh"
 #include "kernels.h"
@@ -59,15 +60,40 @@ __device__ __forceinline__ uint32_t block_scan_256(uint32_t x, uint32_t* sh_warp
 
 // Per-tile bucket counts (one ATOMS per key; the bucket key ranges themselves come from the
 // splitters, so no per-key min/max is needed).
+// Bucket lookup table over the top kCellBits of (key - kmin): the bucket of every cell that
+// no splitter falls inside, or kAmbiguous (binary search) for the <= parts-1 cells that hold a
+// splitter.  Built on the host per partition (build_cell_table).
+constexpr int kCellBits = 12;
+constexpr int kCells = 1 << kCellBits;
+constexpr uint16_t kAmbiguous = 0xFFFF;
+
+struct CellMap {
+    uint64_t kmin;
+    uint32_t shift;  // cell = (key - kmin) >> shift
+};
+
+__device__ __forceinline__ uint32_t bucket_fast(uint64_t key, const uint16_t* s_cell,
+                                                const uint64_t* s_spl, uint32_t nspl,
+                                                CellMap cm) {
+    const uint64_t rel = key - cm.kmin;
+    const uint32_t c = (uint32_t)(rel >> cm.shift);
+    const uint32_t b = c < (uint32_t)kCells ? s_cell[c] : (uint32_t)kAmbiguous;
+    return b != kAmbiguous ? b : bucket_of(key, s_spl, nspl);
+}
+
 __global__ void __launch_bounds__(kThreads)
     k7_count(const uint64_t* __restrict__ keys, uint64_t count, const uint64_t* __restrict__ splitters,
-             uint32_t parts, uint32_t* __restrict__ counts) {
+             uint32_t parts, uint32_t* __restrict__ counts, const uint16_t* __restrict__ cells,
+             CellMap cm) {
     __shared__ uint64_t s_spl[kMaxParts];
     __shared__ uint32_t s_cnt[kMaxParts];
+    __shared__ uint16_t s_cell[kCells];
     for (uint32_t i = threadIdx.x; i < kMaxParts; i += kThreads) {
         s_spl[i] = i + 1 < parts ? splitters[i] : ~0ull;
         s_cnt[i] = 0;
     }
+    for (uint32_t i = threadIdx.x; i < kCells / 8; i += kThreads)
+        reinterpret_cast<uint4*>(s_cell)[i] = reinterpret_cast<const uint4*>(cells)[i];
     const uint64_t base = (uint64_t)blockIdx.x * kTile;
     const uint32_t tn = (uint32_t)(count - base < (uint64_t)kTile ? count - base : kTile);
     uint64_t k[kItems];
@@ -80,7 +106,7 @@ __global__ void __launch_bounds__(kThreads)
 #pragma unroll
     for (int i = 0; i < kItems; ++i)
         if ((uint32_t)i * kThreads + threadIdx.x < tn)
-            atomicAdd(&s_cnt[bucket_of(k[i], s_spl, parts - 1)], 1u);
+            atomicAdd(&s_cnt[bucket_fast(k[i], s_cell, s_spl, parts - 1, cm)], 1u);
     __syncthreads();
     for (uint32_t b = threadIdx.x; b < parts; b += kThreads)
         counts[(uint64_t)blockIdx.x * parts + b] = s_cnt[b];
@@ -171,8 +197,10 @@ __global__ void __launch_bounds__(kThreads, 3)
     k7_scatter(const uint64_t* __restrict__ keys, const uint32_t* __restrict__ vals, uint64_t count,
                const uint64_t* __restrict__ splitters, uint32_t parts,
                const uint32_t* __restrict__ offsets, const uint64_t* __restrict__ starts,
-               uint64_t* __restrict__ keys_out, uint32_t* __restrict__ vals_out) {
+               uint64_t* __restrict__ keys_out, uint32_t* __restrict__ vals_out,
+               const uint16_t* __restrict__ cells, CellMap cm) {
     __shared__ uint64_t s_spl[kMaxParts];
+    __shared__ uint16_t s_cell[kCells];
     __shared__ uint32_t s_whist[kWarps][kMaxParts];
     __shared__ uint32_t s_tstart[kMaxParts];
     __shared__ uint64_t s_base[kMaxParts];  // global position of this tile's first element of b
@@ -195,18 +223,20 @@ __global__ void __launch_bounds__(kThreads, 3)
     }
     // kThreads == kMaxParts: thread b owns bucket b in the per-bucket steps
     s_spl[tid] = (uint32_t)tid + 1 < parts ? splitters[tid] : ~0ull;
+    for (uint32_t i = tid; i < kCells / 8; i += kThreads)
+        reinterpret_cast<uint4*>(s_cell)[i] = reinterpret_cast<const uint4*>(cells)[i];
     const uint64_t my_base = (uint32_t)tid < parts ? starts[tid] + offsets[(uint64_t)blockIdx.x * parts + tid] : 0ull;
 #pragma unroll
     for (int w = 0; w < kWarps; ++w) s_whist[w][tid] = 0;
     __syncthreads();
-    uint32_t bk[kItems], rk[kItems];
+    uint32_t br[kItems];  // bucket << 16 | rank within the warp (rank < 512)
 #pragma unroll
     for (int i = 0; i < kItems; ++i) {
         const uint32_t pos = wofs + 32 * i;
-        bk[i] = pos < tn ? bucket_of(kk[i], s_spl, parts - 1) : 0u;
+        const uint32_t b = pos < tn ? bucket_fast(kk[i], s_cell, s_spl, parts - 1, cm) : 0u;
         // ATOMS resolves same-address lanes in lane order (device self-test), so the
         // returned count is the stable rank within this warp
-        rk[i] = pos < tn ? atomicAdd(&s_whist[warp][bk[i]], 1u) : 0u;
+        br[i] = (b << 16) | (pos < tn ? atomicAdd(&s_whist[warp][b], 1u) : 0u);
     }
     __syncthreads();
     uint32_t acc = 0;
@@ -226,10 +256,10 @@ __global__ void __launch_bounds__(kThreads, 3)
     for (int i = 0; i < kItems; ++i) {
         const uint32_t pos = wofs + 32 * i;
         if (pos < tn) {
-            const uint32_t dst = s_whist[warp][bk[i]] + rk[i];
+            const uint32_t dst = s_whist[warp][br[i] >> 16] + (br[i] & 0xFFFFu);
             s_k[dst] = kk[i];
             s_v[dst] = vv[i];
-            s_b[dst] = (uint8_t)bk[i];
+            s_b[dst] = (uint8_t)(br[i] >> 16);
         }
     }
     __syncthreads();
@@ -246,14 +276,51 @@ __global__ void __launch_bounds__(kThreads, 3)
 
 }  // namespace
 
+namespace {
+// Host: the cell -> bucket table for splitters h_spl[parts-1] over keys in [kmin, kmax].
+CellMap build_cell_table(const uint64_t* h_spl, uint32_t parts, uint64_t kmin, uint64_t kmax,
+                         uint16_t* table) {
+    const uint64_t span = kmax >= kmin ? kmax - kmin : 0;
+    const uint32_t bits = span ? 64u - (uint32_t)__builtin_clzll(span) : 0u;
+    CellMap cm{kmin, bits > (uint32_t)kCellBits ? bits - kCellBits : 0u};
+    auto ub = [&](uint64_t key) {  // upper_bound over the splitters
+        uint32_t lo = 0, hi = parts - 1;
+        while (lo < hi) {
+            const uint32_t mid = (lo + hi) >> 1;
+            if (h_spl[mid] <= key) lo = mid + 1; else hi = mid;
+        }
+        return lo;
+    };
+    for (uint32_t c = 0; c < (uint32_t)kCells; ++c) {
+        const uint64_t lo_rel = (uint64_t)c << cm.shift;
+        if (lo_rel > span) {
+            table[c] = kAmbiguous;
+            continue;
+        }
+        const uint64_t hi_rel = ((uint64_t)(c + 1) << cm.shift) - 1;
+        const uint64_t lo_key = kmin + lo_rel;
+        const uint64_t hi_key = hi_rel > span ? kmax : kmin + hi_rel;
+        const uint32_t a = ub(lo_key), b = ub(hi_key);
+        table[c] = a == b ? (uint16_t)a : kAmbiguous;
+    }
+    return cm;
+}
+}  // namespace
+
+size_t partition_table_bytes() { return kCells * sizeof(uint16_t); }
+
 int launch_partition(const uint64_t* keys, const uint32_t* vals, uint64_t count,
                      const uint64_t* d_splitters, uint32_t parts, uint32_t* d_counts_scratch,
                      uint64_t* d_totals, uint64_t* d_bminmax, uint64_t* keys_out,
                      uint32_t* vals_out, cudaStream_t s, uint32_t align, uint64_t kmin,
-                     uint64_t kmax) {
+                     uint64_t kmax, const uint64_t* h_splitters, uint16_t* d_table) {
     static_assert(kThreads == kMaxParts, "one thread per bucket in k7_scatter");
     if (parts < 1 || parts > (uint32_t)kMaxParts) return -1;
     const uint64_t tiles = (count + kTile - 1) / kTile;
+    static thread_local std::vector<uint16_t> h_table(kCells);
+    const CellMap cm = build_cell_table(h_splitters, parts, kmin, kmax, h_table.data());
+    // pageable source: the copy is staged before the call returns, so reuse is safe
+    cudaMemcpyAsync(d_table, h_table.data(), kCells * sizeof(uint16_t), cudaMemcpyHostToDevice, s);
     if (tiles == 0) {
         cudaMemsetAsync(d_totals, 0, sizeof(uint64_t) * parts, s);
         k7_layout<<<1, 256, 0, s>>>(d_totals, d_splitters, parts, align, kmin, kmax,
@@ -261,7 +328,7 @@ int launch_partition(const uint64_t* keys, const uint32_t* vals, uint64_t count,
         return 2;
     }
     k7_count<<<(unsigned)tiles, kThreads, 0, s>>>(keys, count, d_splitters, parts,
-                                                  d_counts_scratch);
+                                                  d_counts_scratch, d_table, cm);
     k7_scan<<<parts, 1024, 0, s>>>(d_counts_scratch, (uint32_t)tiles, parts, d_totals);
     // d_totals has room for 2 * parts words: [totals | segment starts]
     k7_layout<<<1, 256, 0, s>>>(d_totals, d_splitters, parts, align, kmin, kmax,
@@ -274,7 +341,7 @@ int launch_partition(const uint64_t* keys, const uint32_t* vals, uint64_t count,
     }
     k7_scatter<<<(unsigned)tiles, kThreads, kScSmem, s>>>(keys, vals, count, d_splitters, parts,
                                                           d_counts_scratch, d_totals + parts,
-                                                          keys_out, vals_out);
+                                                          keys_out, vals_out, d_table, cm);
     return 4;
 }
 

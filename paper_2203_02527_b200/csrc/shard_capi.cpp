@@ -9,6 +9,7 @@
 #include <algorithm>
 #include <cstring>
 #include <string>
+#include <mutex>
 #include <vector>
 
 #include "../../include/ph0b.h"
@@ -31,6 +32,7 @@ struct ShardScratch {
     uint64_t* d_spl = nullptr;      // splitters (<= 255)
     uint64_t* d_totals = nullptr;   // per-part totals
     uint64_t* d_bminmax = nullptr;  // per-part [min | max]
+    uint16_t* d_table = nullptr;    // partition bucket lookup table
     uint32_t* d_counts = nullptr;   // per (tile, part)
     uint64_t counts_cap = 0;
     uint64_t* d_sample = nullptr;
@@ -41,8 +43,15 @@ struct ShardScratch {
     uint64_t local_kmin = 0, local_kmax = 0;
 };
 
-ShardScratch& scratch(Context* c) {
+std::mutex g_scratch_mu;
+std::vector<std::pair<Context*, ShardScratch>>& all_scratch() {
     static std::vector<std::pair<Context*, ShardScratch>> all;
+    return all;
+}
+
+ShardScratch& scratch(Context* c) {
+    std::lock_guard<std::mutex> lk(g_scratch_mu);
+    auto& all = all_scratch();
     for (auto& p : all)
         if (p.first == c) return p.second;
     all.emplace_back(c, ShardScratch{});
@@ -69,6 +78,25 @@ int ensure(void** p, uint64_t* cap, uint64_t bytes) {
 inline uint64_t row_base(uint64_t u, uint64_t n) { return u * (2 * n - u - 1) / 2; }
 
 }  // namespace
+
+namespace ph0b {
+// Frees the shard scratch of a context being destroyed (called by ph0b_context_destroy).
+void shard_scratch_release(Context* c) {
+    std::lock_guard<std::mutex> lk(g_scratch_mu);
+    auto& all = all_scratch();
+    for (size_t i = 0; i < all.size(); ++i) {
+        if (all[i].first != c) continue;
+        ShardScratch& sc = all[i].second;
+        cudaSetDevice(c->device());
+        void* ps[] = {sc.d_spl, sc.d_totals, sc.d_bminmax, sc.d_table, sc.d_counts,
+                      sc.d_sample, sc.d_cand_uv};
+        for (void* p : ps)
+            if (p) cudaFree(p);
+        all.erase(all.begin() + (long)i);
+        return;
+    }
+}
+}  // namespace ph0b
 
 extern "C" {
 
@@ -131,6 +159,10 @@ int ph0b_shard_partition(ph0b_context* ctx, const uint64_t* splitters, uint32_t 
         if ((rc = ensure(reinterpret_cast<void**>(&sc.d_totals), &cap, 512 * 8))) return rc;
         cap = 0;
         if ((rc = ensure(reinterpret_cast<void**>(&sc.d_bminmax), &cap, 512 * 8))) return rc;
+        cap = 0;
+        if ((rc = ensure(reinterpret_cast<void**>(&sc.d_table), &cap,
+                         ph0b::partition_table_bytes())))
+            return rc;
     }
     const uint64_t words = ph0b::partition_scratch_words(sc.local_count, parts);
     if ((rc = ensure(reinterpret_cast<void**>(&sc.d_counts), &sc.counts_cap, words * 4 + 4)))
@@ -140,7 +172,8 @@ int ph0b_shard_partition(ph0b_context* ctx, const uint64_t* splitters, uint32_t 
         return ph0b::capi_fail(PH0B_ERR_CUDA, "H2D splitters");
     c->launches = ph0b::launch_partition(c->keys(0), c->vals(0), sc.local_count, sc.d_spl, parts,
                                          sc.d_counts, sc.d_totals, sc.d_bminmax, c->keys(1),
-                                         c->vals(1), st, 1, sc.local_kmin, sc.local_kmax);
+                                         c->vals(1), st, 1, sc.local_kmin, sc.local_kmax,
+                                         splitters, sc.d_table);
     ph0b::capi_set_launches(c->launches);
     std::vector<uint64_t> mm(2 * parts);
     if (cudaGetLastError() != cudaSuccess ||
