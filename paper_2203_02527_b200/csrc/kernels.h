@@ -142,6 +142,25 @@ int launch_partition(const uint64_t* keys, const uint32_t* vals, uint64_t count,
                      uint32_t* vals_out, cudaStream_t s, uint32_t align, uint64_t kmin,
                      uint64_t kmax, const uint64_t* h_splitters, uint16_t* d_table);
 size_t partition_table_bytes();  // device scratch for the bucket lookup table
+// The same in phases: counts + scan + layout (segment starts, padding, key bounds); optional
+// early extraction of one segment; the scatter of every other segment.
+int launch_partition_count(const uint64_t* keys, uint64_t count, const uint64_t* d_splitters,
+                           uint32_t parts, uint32_t* d_counts_scratch, uint64_t* d_totals,
+                           uint64_t* d_bminmax, uint64_t* keys_out, uint32_t* vals_out,
+                           cudaStream_t s, uint32_t align, uint64_t kmin, uint64_t kmax,
+                           const uint64_t* h_splitters, uint16_t* d_table);
+int launch_partition_select(const uint64_t* keys, const uint32_t* vals, uint64_t count,
+                            uint32_t parts, uint32_t bucket, const uint32_t* d_counts_scratch,
+                            const uint64_t* d_totals, const uint64_t* d_bminmax,
+                            uint64_t* keys_out, uint32_t* vals_out, cudaStream_t s);
+int launch_partition_pad(const uint64_t* d_totals, uint32_t parts, uint32_t align,
+                         uint64_t* keys, uint32_t* vals, cudaStream_t s);
+int launch_partition_scatter(const uint64_t* keys, const uint32_t* vals, uint64_t count,
+                             const uint64_t* d_splitters, uint32_t parts,
+                             const uint32_t* d_counts_scratch, const uint64_t* d_totals,
+                             uint64_t* keys_out, uint32_t* vals_out, cudaStream_t s,
+                             uint64_t kmin, uint64_t kmax, const uint16_t* d_table,
+                             uint32_t skip_bucket);
 uint64_t partition_scratch_words(uint64_t count, uint32_t parts);
 int launch_sample(const uint64_t* keys, uint64_t count, uint64_t s, uint64_t* out, cudaStream_t st);
 int launch_gather_u32(const uint32_t* src, const uint32_t* idx, uint64_t m, uint32_t* out,

@@ -530,10 +530,13 @@ Status Context::run_host_overlapped(const double* X, uint64_t n, uint64_t d, uin
     Status s = reserve(n, d);
     if (!s.good()) return s;
     const uint64_t k = n * (n - (n > 0)) / 2;
-    // key-range buckets: the first ones small (1/256, 1/256, 1/128, 1/64, 1/32 of the edges)
-    // so the first D slice reaches the copy engine early and every later bucket is sorted
-    // before the copy of the previous one ends; then 15 buckets of 1/16
-    constexpr uint32_t B = 20;
+    // key-range buckets (cumulative edge fractions, /256): bucket 0 (1/16) is extracted and
+    // sorted before the rest is partitioned, so its D slice (~19 ms on PCIe) covers the
+    // partition; then small buckets (1/256 .. 1/32) so the copy engine never starves, then
+    // buckets of 1/16
+    static constexpr uint32_t kCum[] = {16, 17, 19, 23, 31, 47, 63, 79, 95, 111, 127,
+                                        143, 159, 175, 191, 207, 223, 239};
+    constexpr uint32_t B = sizeof(kCum) / sizeof(kCum[0]) + 1;
     if (!(s = grow(reinterpret_cast<void**>(&dbuf_), &dbuf_cap_, k * 8 + 256)).good()) return s;
     const uint64_t part_words = partition_scratch_words(k, B);
     if (!(s = grow(reinterpret_cast<void**>(&part_counts_), &part_counts_cap_, part_words * 4 + 16))
@@ -569,29 +572,92 @@ Status Context::run_host_overlapped(const double* X, uint64_t n, uint64_t d, uin
     PH0B_TRY(cudaStreamSynchronize(st), "sample");
     std::sort(sample.begin(), sample.end());
     std::vector<uint64_t> spl(B - 1);
-    for (uint32_t j = 0; j + 1 < B; ++j) {
-        const uint64_t num = j < 4 ? (1ull << j) : 16ull * (j - 3);  // cumulative, /256
-        spl[j] = sample[std::min<uint64_t>(S - 1, num * S / 256)];
-    }
+    for (uint32_t j = 0; j + 1 < B; ++j)
+        spl[j] = sample[std::min<uint64_t>(S - 1, (uint64_t)kCum[j] * S / 256)];
     PH0B_TRY(cudaMemcpyAsync(d_spl, spl.data(), (B - 1) * 8, cudaMemcpyHostToDevice, st), "H2D");
     // segments start on 4-element boundaries (16-byte aligned TMA bulk copies in the sort
     // and unique kernels); the <= 3 padding slots per segment hold the cycle column {0, 0}
     constexpr uint32_t kAlign = 4;
-    launches += launch_partition(keys_[0], vals_[0], k, d_spl, B, part_counts_, d_tot, d_mm,
-                                 keys_[1], vals_[1], st, kAlign, kmin, kmax, spl.data(),
-                                 reinterpret_cast<uint16_t*>(part_small_ + 1280));
-    PH0B_CHECK_LAUNCH("partition");
+    uint16_t* d_table = reinterpret_cast<uint16_t*>(part_small_ + 1280);
+    const int lc = launch_partition_count(keys_[0], k, d_spl, B, part_counts_, d_tot, d_mm,
+                                          keys_[1], vals_[1], st, kAlign, kmin, kmax, spl.data(),
+                                          d_table);
+    if (lc < 0) return {PH0B_ERR_INVALID_ARGUMENT, "partition: bad bucket count"};
+    launches += lc;
+    PH0B_CHECK_LAUNCH("partition counts");
     std::vector<uint64_t> tot(B), mm(2 * B);
     PH0B_TRY(cudaMemcpyAsync(tot.data(), d_tot, B * 8, cudaMemcpyDeviceToHost, st), "D2H");
     PH0B_TRY(cudaMemcpyAsync(mm.data(), d_mm, 2 * B * 8, cudaMemcpyDeviceToHost, st), "D2H");
     PH0B_TRY(cudaStreamSynchronize(st), "partition");
-    tr.mark("partition done");
+    tr.mark("partition counts done");
     h_base[0] = 0;
-
-    // ---- per bucket: sort + unique into D, then stream that slice of D to the host ---------
     uint64_t start = 0, host_base = 0;
     int target = -1;
-    for (uint32_t b = 0; b < B; ++b) {
+    auto pad = [&](uint64_t c) { return (c + kAlign - 1) / kAlign * kAlign; };
+    // D slice [host_base, d_base[b+1]) of a finished bucket -> host, in medium chunks (several
+    // medium copies sustain a higher PCIe rate than one large one: 55 vs 52 GB/s for 17 GB,
+    // tools/d2h_big.py)
+    auto ship = [&](uint32_t b) -> Status {
+        PH0B_TRY(cudaEventRecord(ev_[6], st), "event");
+        PH0B_TRY(cudaEventSynchronize(ev_[6]), "bucket");
+        tr.mark("bucket sorted", (long)b);
+        const uint64_t next_base = h_base[b + 1];
+        if (host_scale && next_base > host_base) {
+            if (next_base > scale_capacity)
+                return {PH0B_ERR_CAPACITY, "scale buffer too small: need >= " +
+                                               std::to_string(next_base) + " entries"};
+            PH0B_TRY(cudaStreamWaitEvent(copy_stream_, ev_[6], 0), "wait");
+            for (uint64_t q = host_base; q < next_base; q += d2h_chunk_elems()) {
+                const uint64_t e = std::min<uint64_t>(next_base, q + d2h_chunk_elems());
+                PH0B_TRY(cudaMemcpyAsync(host_scale + q, dbuf_ + q, (e - q) * 8,
+                                         cudaMemcpyDeviceToHost, copy_stream_), "D2H scale");
+            }
+        }
+        host_base = next_base;
+        return Status::ok();
+    };
+
+    // ---- bucket 0 ahead of the partition: extract it (stable) into its segment, sort it
+    // there (ping-pong with the free space after it), and start its D2H ---------------------
+    {
+        const uint64_t c0 = tot[0];
+        launches += launch_partition_select(keys_[0], vals_[0], k, B, 0, part_counts_, d_tot,
+                                            d_mm, keys_[1], vals_[1], st);
+        int res = 0;
+        uint32_t passes = 0;
+        const uint64_t c0p = pad(c0);
+        s = sort_unique_range(keys_[1], vals_[1], keys_[1] + c0p, vals_[1] + c0p, c0,
+                              c0 ? mm[0] : 0, c0 ? mm[B] : 0, false, dbuf_, d_base,
+                              d_base + 1, nullptr, st, &res, &passes);
+        if (!s.good()) return s;
+        r.times.sort_passes = passes;
+        if (c0 && res == 1) {  // sorted data ended in the scratch half, which the scatter
+                               // below overwrites: back into segment 0 first
+            PH0B_TRY(cudaMemcpyAsync(keys_[1], keys_[1] + c0p, c0 * 8, cudaMemcpyDeviceToDevice,
+                                     st), "D2D");
+            PH0B_TRY(cudaMemcpyAsync(vals_[1], vals_[1] + c0p, c0 * 4, cudaMemcpyDeviceToDevice,
+                                     st), "D2D");
+        }
+        if (!(s = ship(0)).good()) return s;
+        // ---- the rest of the partition (segment 0 is already in place) --------------------
+        launches += launch_partition_scatter(keys_[0], vals_[0], k, d_spl, B, part_counts_,
+                                             d_tot, keys_[1], vals_[1], st, kmin, kmax, d_table,
+                                             0u);
+        PH0B_CHECK_LAUNCH("partition");
+        // M is assembled in buffer 0 (the 5-pass buckets end there): once the scatter has
+        // consumed the u-major input, move sorted bucket 0 into its segment of buffer 0
+        if (c0) {
+            PH0B_TRY(cudaMemcpyAsync(keys_[0], keys_[1], c0 * 8, cudaMemcpyDeviceToDevice, st),
+                     "D2D");
+            PH0B_TRY(cudaMemcpyAsync(vals_[0], vals_[1], c0 * 4, cudaMemcpyDeviceToDevice, st),
+                     "D2D");
+            target = 0;
+        }
+        start = c0p;
+    }
+
+    // ---- per bucket: sort + unique into D, then stream that slice of D to the host ---------
+    for (uint32_t b = 1; b < B; ++b) {
         const uint64_t c = tot[b];
         int res = 0;
         uint32_t passes = 0;
@@ -608,28 +674,13 @@ Status Context::run_host_overlapped(const double* X, uint64_t n, uint64_t d, uin
             PH0B_TRY(cudaMemcpyAsync(vals_[target] + start, vals_[buf] + start, c * 4,
                                      cudaMemcpyDeviceToDevice, st), "D2D");
         }
-        PH0B_TRY(cudaEventRecord(ev_[6], st), "event");
-        PH0B_TRY(cudaEventSynchronize(ev_[6]), "bucket");
-        tr.mark("bucket sorted", (long)b);
-        const uint64_t next_base = h_base[b + 1];
-        if (host_scale && next_base > host_base) {
-            if (next_base > scale_capacity)
-                return {PH0B_ERR_CAPACITY, "scale buffer too small: need >= " +
-                                               std::to_string(next_base) + " entries"};
-            PH0B_TRY(cudaStreamWaitEvent(copy_stream_, ev_[6], 0), "wait");
-            // several medium copies sustain a higher PCIe rate than one large one (measured
-            // 55 vs 52 GB/s for 17 GB, tools/d2h_big.py)
-            for (uint64_t q = host_base; q < next_base; q += d2h_chunk_elems()) {
-                const uint64_t e = std::min<uint64_t>(next_base, q + d2h_chunk_elems());
-                PH0B_TRY(cudaMemcpyAsync(host_scale + q, dbuf_ + q, (e - q) * 8,
-                                         cudaMemcpyDeviceToHost, copy_stream_), "D2H scale");
-            }
-        }
-        host_base = next_base;
-        start += (c + kAlign - 1) / kAlign * kAlign;
+        if (!(s = ship(b)).good()) return s;
+        start += pad(c);
     }
     const uint64_t kpad = start;  // columns incl. the sentinel padding
     if (target < 0) target = 0;
+    // padding slots of M hold the cycle column {0, 0} in whichever buffer M ended up
+    launches += launch_partition_pad(d_tot, B, kAlign, keys_[target], vals_[target], st);
     PH0B_TRY(cudaEventRecord(ev_[2], st), "event");
     PH0B_TRY(cudaEventRecord(ev_[3], st), "event");
     cur_ = target;

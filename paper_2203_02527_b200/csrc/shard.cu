@@ -198,7 +198,7 @@ __global__ void __launch_bounds__(kThreads, 3)
                const uint64_t* __restrict__ splitters, uint32_t parts,
                const uint32_t* __restrict__ offsets, const uint64_t* __restrict__ starts,
                uint64_t* __restrict__ keys_out, uint32_t* __restrict__ vals_out,
-               const uint16_t* __restrict__ cells, CellMap cm) {
+               const uint16_t* __restrict__ cells, CellMap cm, uint32_t skip_bucket) {
     __shared__ uint64_t s_spl[kMaxParts];
     __shared__ uint16_t s_cell[kCells];
     __shared__ uint32_t s_whist[kWarps][kMaxParts];
@@ -266,10 +266,69 @@ __global__ void __launch_bounds__(kThreads, 3)
 #pragma unroll 4
     for (int i = 0; i < kItems; ++i) {
         const uint32_t p = (uint32_t)i * kThreads + tid;
-        if (p < tn) {
+        if (p < tn && s_b[p] != skip_bucket) {
             const uint64_t dst = s_base[s_b[p]] + p;
             keys_out[dst] = s_k[p];
             vals_out[dst] = s_v[p];
+        }
+    }
+}
+
+// Stable extraction of one segment (keys in [lo_b, hi_b]) into its place in the partition
+// output, ahead of the full scatter, so that segment can be sorted while the rest is still
+// being partitioned (overlapped host path).  Same tiles and offsets as k7_count/k7_scan.
+__global__ void __launch_bounds__(kThreads)
+    k7_select(const uint64_t* __restrict__ keys, const uint32_t* __restrict__ vals, uint64_t count,
+              uint32_t parts, uint32_t b, const uint32_t* __restrict__ offsets,
+              const uint64_t* __restrict__ starts, const uint64_t* __restrict__ bminmax,
+              uint64_t* __restrict__ keys_out, uint32_t* __restrict__ vals_out) {
+    __shared__ uint32_t s_wt[kWarps];
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const uint64_t tile0 = (uint64_t)blockIdx.x * kTile;
+    const uint32_t tn = (uint32_t)(count - tile0 < (uint64_t)kTile ? count - tile0 : kTile);
+    const uint64_t lo = bminmax[b], hi = bminmax[parts + b];
+    const uint32_t wofs = warp * (32 * kItems) + lane;
+    uint64_t k[kItems];
+#pragma unroll
+    for (int i = 0; i < kItems; ++i) {
+        const uint32_t pos = wofs + 32 * i;
+        k[i] = pos < tn ? keys[tile0 + pos] : ~0ull;
+    }
+    uint32_t ball[kItems], total = 0;
+#pragma unroll
+    for (int i = 0; i < kItems; ++i) {
+        const uint32_t pos = wofs + 32 * i;
+        ball[i] = __ballot_sync(0xffffffffu, pos < tn && k[i] >= lo && k[i] <= hi);
+        total += __popc(ball[i]);
+    }
+    if (lane == 0) s_wt[warp] = total;
+    __syncthreads();
+    uint32_t wb = 0;
+#pragma unroll
+    for (int w = 0; w < kWarps; ++w) wb += (w < warp) ? s_wt[w] : 0u;
+    uint64_t run = starts[b] + offsets[(uint64_t)blockIdx.x * parts + b] + wb;
+    const uint32_t lt = lanemask_lt();
+#pragma unroll
+    for (int i = 0; i < kItems; ++i) {
+        if ((ball[i] >> lane) & 1u) {
+            const uint64_t dst = run + __popc(ball[i] & lt);
+            keys_out[dst] = k[i];
+            vals_out[dst] = vals[tile0 + wofs + 32 * i];
+        }
+        run += __popc(ball[i]);
+    }
+}
+
+// Sentinel column {0, 0} (key 0) in the padding slots [start_b + total_b, pad(...)) of every
+// segment of (keys, vals) — a buffer other than the one k7_layout padded.
+__global__ void k7_pad_fill(const uint64_t* __restrict__ totals, const uint64_t* __restrict__ starts,
+                            uint32_t parts, uint32_t align, uint64_t* __restrict__ keys,
+                            uint32_t* __restrict__ vals) {
+    for (uint32_t b = threadIdx.x; b < parts; b += blockDim.x) {
+        const uint64_t e = starts[b] + (totals[b] + align - 1) / align * align;
+        for (uint64_t q = starts[b] + totals[b]; q < e; ++q) {
+            keys[q] = 0;
+            vals[q] = 0;
         }
     }
 }
@@ -309,11 +368,11 @@ CellMap build_cell_table(const uint64_t* h_spl, uint32_t parts, uint64_t kmin, u
 
 size_t partition_table_bytes() { return kCells * sizeof(uint16_t); }
 
-int launch_partition(const uint64_t* keys, const uint32_t* vals, uint64_t count,
-                     const uint64_t* d_splitters, uint32_t parts, uint32_t* d_counts_scratch,
-                     uint64_t* d_totals, uint64_t* d_bminmax, uint64_t* keys_out,
-                     uint32_t* vals_out, cudaStream_t s, uint32_t align, uint64_t kmin,
-                     uint64_t kmax, const uint64_t* h_splitters, uint16_t* d_table) {
+int launch_partition_count(const uint64_t* keys, uint64_t count, const uint64_t* d_splitters,
+                           uint32_t parts, uint32_t* d_counts_scratch, uint64_t* d_totals,
+                           uint64_t* d_bminmax, uint64_t* keys_out, uint32_t* vals_out,
+                           cudaStream_t s, uint32_t align, uint64_t kmin, uint64_t kmax,
+                           const uint64_t* h_splitters, uint16_t* d_table) {
     static_assert(kThreads == kMaxParts, "one thread per bucket in k7_scatter");
     if (parts < 1 || parts > (uint32_t)kMaxParts) return -1;
     const uint64_t tiles = (count + kTile - 1) / kTile;
@@ -321,18 +380,44 @@ int launch_partition(const uint64_t* keys, const uint32_t* vals, uint64_t count,
     const CellMap cm = build_cell_table(h_splitters, parts, kmin, kmax, h_table.data());
     // pageable source: the copy is staged before the call returns, so reuse is safe
     cudaMemcpyAsync(d_table, h_table.data(), kCells * sizeof(uint16_t), cudaMemcpyHostToDevice, s);
+    int l = 1;
     if (tiles == 0) {
         cudaMemsetAsync(d_totals, 0, sizeof(uint64_t) * parts, s);
-        k7_layout<<<1, 256, 0, s>>>(d_totals, d_splitters, parts, align, kmin, kmax,
-                                    d_totals + parts, d_bminmax, keys_out, vals_out);
-        return 2;
+    } else {
+        k7_count<<<(unsigned)tiles, kThreads, 0, s>>>(keys, count, d_splitters, parts,
+                                                      d_counts_scratch, d_table, cm);
+        k7_scan<<<parts, 1024, 0, s>>>(d_counts_scratch, (uint32_t)tiles, parts, d_totals);
+        l = 3;
     }
-    k7_count<<<(unsigned)tiles, kThreads, 0, s>>>(keys, count, d_splitters, parts,
-                                                  d_counts_scratch, d_table, cm);
-    k7_scan<<<parts, 1024, 0, s>>>(d_counts_scratch, (uint32_t)tiles, parts, d_totals);
     // d_totals has room for 2 * parts words: [totals | segment starts]
     k7_layout<<<1, 256, 0, s>>>(d_totals, d_splitters, parts, align, kmin, kmax,
                                 d_totals + parts, d_bminmax, keys_out, vals_out);
+    return l;
+}
+
+int launch_partition_select(const uint64_t* keys, const uint32_t* vals, uint64_t count,
+                            uint32_t parts, uint32_t bucket, const uint32_t* d_counts_scratch,
+                            const uint64_t* d_totals, const uint64_t* d_bminmax,
+                            uint64_t* keys_out, uint32_t* vals_out, cudaStream_t s) {
+    const uint64_t tiles = (count + kTile - 1) / kTile;
+    if (tiles == 0) return 0;
+    k7_select<<<(unsigned)tiles, kThreads, 0, s>>>(keys, vals, count, parts, bucket,
+                                                   d_counts_scratch, d_totals + parts, d_bminmax,
+                                                   keys_out, vals_out);
+    return 1;
+}
+
+int launch_partition_scatter(const uint64_t* keys, const uint32_t* vals, uint64_t count,
+                             const uint64_t* d_splitters, uint32_t parts,
+                             const uint32_t* d_counts_scratch, const uint64_t* d_totals,
+                             uint64_t* keys_out, uint32_t* vals_out, cudaStream_t s,
+                             uint64_t kmin, uint64_t kmax, const uint16_t* d_table,
+                             uint32_t skip_bucket) {
+    const uint64_t tiles = (count + kTile - 1) / kTile;
+    if (tiles == 0) return 0;
+    const uint64_t span = kmax >= kmin ? kmax - kmin : 0;
+    const uint32_t bits = span ? 64u - (uint32_t)__builtin_clzll(span) : 0u;
+    const CellMap cm{kmin, bits > (uint32_t)kCellBits ? bits - kCellBits : 0u};
     constexpr size_t kScSmem = (size_t)kTile * (8 + 4 + 1);
     static bool configured = false;
     if (!configured) {
@@ -341,8 +426,29 @@ int launch_partition(const uint64_t* keys, const uint32_t* vals, uint64_t count,
     }
     k7_scatter<<<(unsigned)tiles, kThreads, kScSmem, s>>>(keys, vals, count, d_splitters, parts,
                                                           d_counts_scratch, d_totals + parts,
-                                                          keys_out, vals_out, d_table, cm);
-    return 4;
+                                                          keys_out, vals_out, d_table, cm,
+                                                          skip_bucket);
+    return 1;
+}
+
+int launch_partition_pad(const uint64_t* d_totals, uint32_t parts, uint32_t align,
+                         uint64_t* keys, uint32_t* vals, cudaStream_t s) {
+    k7_pad_fill<<<1, 256, 0, s>>>(d_totals, d_totals + parts, parts, align, keys, vals);
+    return 1;
+}
+
+int launch_partition(const uint64_t* keys, const uint32_t* vals, uint64_t count,
+                     const uint64_t* d_splitters, uint32_t parts, uint32_t* d_counts_scratch,
+                     uint64_t* d_totals, uint64_t* d_bminmax, uint64_t* keys_out,
+                     uint32_t* vals_out, cudaStream_t s, uint32_t align, uint64_t kmin,
+                     uint64_t kmax, const uint64_t* h_splitters, uint16_t* d_table) {
+    const int l = launch_partition_count(keys, count, d_splitters, parts, d_counts_scratch,
+                                         d_totals, d_bminmax, keys_out, vals_out, s, align, kmin,
+                                         kmax, h_splitters, d_table);
+    if (l < 0) return l;
+    return l + launch_partition_scatter(keys, vals, count, d_splitters, parts, d_counts_scratch,
+                                        d_totals, keys_out, vals_out, s, kmin, kmax, d_table,
+                                        ~0u);
 }
 
 int launch_sample(const uint64_t* keys, uint64_t count, uint64_t s, uint64_t* out, cudaStream_t st) {

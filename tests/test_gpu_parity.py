@@ -250,3 +250,25 @@ def test_overlapped_host_path_matches_device_path():
     assert np.array_equal(bits(dl[:nf]), bits(bc.death_length))
     assert np.array_equal(bits(sc), bits(bc.scale))
     ctx.close()
+
+
+def test_overlapped_host_path_separated_clusters():
+    """Far-apart clusters: the forest is still disconnected when late buckets are reduced, so
+    every padding slot between bucket segments of M is reached by the reduction — they must
+    hold the cycle column {0, 0} in whichever buffer M ends up (regression: stale u-major
+    columns there produced wrong bars)."""
+    rng = np.random.default_rng(5)
+    centres = np.array([[0, 0, 0], [100, 0, 0], [0, 100, 0], [0, 0, 100]], np.float64)
+    X = np.concatenate([c + rng.normal(size=(3000, 3)) for c in centres])  # N=12000, K>=2^26
+    n, d = X.shape
+    ctx = pkg.Context(0)
+    dg = np.empty(n, np.uint64)
+    dl = np.empty(n)
+    sc = np.empty(n * (n - 1) // 2)
+    nf, ess, ns, t = ctx.run_host(np.asfortranarray(X), dg, dl, sc)
+    bc = pkg.h0_barcode(X)
+    assert nf == n - 1 and ess == 1 and ns == len(bc.scale)
+    assert np.array_equal(dg[:nf], bc.death_grade)
+    assert np.array_equal(bits(dl[:nf]), bits(bc.death_length))
+    assert np.array_equal(bits(sc[:ns]), bits(bc.scale))
+    ctx.close()
