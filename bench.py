@@ -162,6 +162,19 @@ def run_reference_arm(args, cfg_name):
     print(json.dumps(line), flush=True)
 
 
+def scale_checksum(t):
+    """Order-sensitive checksum of D's bit patterns: sum_i bits_i * (2i + 1) mod 2^64
+    (int64 wrap-around), in chunks; the same value on a device or a host tensor."""
+    import torch
+    acc = torch.zeros((), dtype=torch.int64, device=t.device)
+    step = 1 << 27
+    for a in range(0, t.numel(), step):
+        c = t[a:a + step]
+        w = torch.arange(a, a + c.numel(), device=t.device, dtype=torch.int64) * 2 + 1
+        acc += (c * w).sum()
+    return int(acc.item()) & ((1 << 64) - 1)
+
+
 def load_traffic():
     p = ROOT / "profiles" / "ncu_summary.json"
     if p.exists():
@@ -356,6 +369,19 @@ def main():
     n_scale = int(r.n_scale)
     n_finite = int(r.n_finite)
 
+    # untimed: the device-path result, to check the e2e result against (bars bit for bit, D by
+    # an order-sensitive checksum)
+    def dev_tensor(ptr, count, typestr):
+        cai = type("CAI", (), {"__cuda_array_interface__": {
+            "shape": (int(count),), "typestr": typestr, "data": (int(ptr), False),
+            "version": 3, "strides": None}})()
+        return torch.as_tensor(cai, device=f"cuda:{device}")
+
+    torch.cuda.synchronize(device)
+    dev_dg = dev_tensor(r.d_death_grade, n_finite, "<i8").cpu().numpy().view(np.uint64).copy()
+    dev_dl = dev_tensor(r.d_death_length, n_finite, "<f8").cpu().numpy().copy()
+    dev_sum = scale_checksum(dev_tensor(r.d_scale, n_scale, "<i8"))
+
     # ---- end-to-end through the C ABI with host buffers (e2e) --------------------------------
     e2e_steps = args.e2e_steps or max(1, min(args.steps, 5))
     xin = pkg.PinnedArray(n * d)
@@ -384,6 +410,15 @@ def main():
     e2e_value = ws * k * e2e_steps / (e2e_ms / 1e3)
     h2d = n * d * 8
     d2h = ns_ * 8 + nf * 16
+    e2e_check = {
+        "bars_equal_device_path": bool(nf == n_finite and
+                                       np.array_equal(dg.array[:nf], dev_dg) and
+                                       np.array_equal(dl.array[:nf].view(np.uint64),
+                                                      dev_dl.view(np.uint64))),
+        "scale_equal_device_path": bool(ns_ == n_scale and
+                                        scale_checksum(torch.from_numpy(
+                                            sc.array[:ns_].view(np.int64))) == dev_sum),
+    }
     for a in (xin, dg, dl, sc):
         a.free()
 
@@ -425,7 +460,7 @@ def main():
                        "n_scale": n_scale, "bars": n_finite},
             "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": h2d,
                     "d2h_bytes_per_step": d2h, "ms_per_step": e2e_ms / e2e_steps,
-                    "steps": e2e_steps, "api": "ph0b_run_host (pinned host X, D, bars)"},
+                    "steps": e2e_steps, "api": "ph0b_run_host (pinned host X, D, bars)", "check": e2e_check},
             "roofline": roofline, "cpu_baseline": cpu, "clocks": clk.summary(),
             "gpu_launches": launches, "stage_ms": stage_ms,
             "sort_passes": passes,
