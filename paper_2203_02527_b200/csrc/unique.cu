@@ -172,59 +172,68 @@ __global__ void __launch_bounds__(kThreads)
     }
 }
 
-__global__ void k3_scan(const uint32_t* __restrict__ counts, uint32_t tiles,
-                        uint64_t* __restrict__ offsets, uint64_t* n_scale) {
-    __shared__ uint64_t s_carry;
-    __shared__ uint64_t s_warp[32];
-    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
-    if (threadIdx.x == 0) s_carry = 0;
+// Exclusive scan of the per-tile distinct counts by one block of 32 warps: warp w owns a
+// contiguous chunk and walks it 32 counts at a time (coalesced loads, warp scan, running
+// carry); the 32 chunk totals are scanned in shared memory; a second walk writes offsets.
+__global__ void __launch_bounds__(1024)
+    k3_scan(const uint32_t* __restrict__ counts, uint32_t tiles, uint64_t* __restrict__ offsets,
+            uint64_t* n_scale, const uint64_t* __restrict__ d_base) {
+    __shared__ uint64_t s_tot[32];
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const uint32_t per = ((tiles + 31) / 32 + 31) / 32 * 32;  // chunk, multiple of 32
+    const uint32_t b = warp * per;
+    const uint32_t e = b + per < tiles ? b + per : tiles;
+    uint64_t tot = 0;
+    for (uint32_t t = b; t < e; t += 32) {
+        const uint32_t c = t + lane < e ? counts[t + lane] : 0u;
+        tot += __reduce_add_sync(0xffffffffu, c);
+    }
+    if (lane == 0) s_tot[warp] = tot;
     __syncthreads();
-    for (uint32_t t0 = 0; t0 < tiles; t0 += blockDim.x) {
-        const uint32_t t = t0 + threadIdx.x;
-        const uint64_t x = t < tiles ? counts[t] : 0u;
-        uint64_t inc = x;
+    uint64_t carry = 0, all = 0;
+    for (int w = 0; w < 32; ++w) {
+        carry += w < warp ? s_tot[w] : 0u;
+        all += s_tot[w];
+    }
+    for (uint32_t t = b; t < e; t += 32) {
+        const uint32_t c = t + lane < e ? counts[t + lane] : 0u;
+        uint32_t inc = c;
+#pragma unroll
         for (int o = 1; o < 32; o <<= 1) {
-            const uint64_t y = __shfl_up_sync(0xffffffffu, inc, o);
+            const uint32_t y = __shfl_up_sync(0xffffffffu, inc, o);
             if (lane >= o) inc += y;
         }
-        if (lane == 31) s_warp[warp] = inc;
-        __syncthreads();
-        uint64_t wb = 0, tot = 0;
-        for (int w = 0; w < nw; ++w) {
-            wb += w < warp ? s_warp[w] : 0u;
-            tot += s_warp[w];
-        }
-        const uint64_t carry = s_carry;
-        if (t < tiles) offsets[t] = carry + wb + inc - x;
-        __syncthreads();
-        if (threadIdx.x == 0) s_carry = carry + tot;
-        __syncthreads();
+        if (t + lane < e) offsets[t + lane] = carry + inc - c;
+        carry += __shfl_sync(0xffffffffu, inc, 31);
     }
-    if (threadIdx.x == 0) *n_scale = s_carry;
+    if (threadIdx.x == 0) *n_scale = (d_base ? *d_base : 0ull) + all;
 }
 
-__global__ void __launch_bounds__(kThreads)
+template <int kWT>
+__global__ void __launch_bounds__(kWT)
     k3_write(const uint64_t* __restrict__ keys, uint64_t count, const int2* __restrict__ own,
              const uint64_t* __restrict__ offsets, double* __restrict__ scale,
              uint32_t* __restrict__ grade) {
-    __shared__ uint32_t s_warp_tot[kWarps];
+    constexpr int kWW = kWT / 32, kWI = kTileKeys / kWT;
+    __shared__ uint32_t s_warp_tot[kWW];
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const uint64_t tile_start = (uint64_t)blockIdx.x * kTileKeys;
     const uint64_t tile_end = tile_start + kTileKeys < count ? tile_start + kTileKeys : count;
+    const uint64_t base = offsets[blockIdx.x];  // independent of the keys: issue first
     const int2 ow = own[blockIdx.x];
     const uint64_t own_start = tile_start + (uint64_t)ow.x, own_end = tile_start + (uint64_t)ow.y;
-    const uint64_t wbase = tile_start + (uint64_t)warp * (32 * kItems) + lane;
-    uint64_t k[kItems];
-    uint32_t ball[kItems];
+    const uint64_t wbase = tile_start + (uint64_t)warp * (32 * kWI) + lane;
+    uint64_t k[kWI];
+    uint32_t ball[kWI];
     uint32_t total = 0;
 #pragma unroll
-    for (int i = 0; i < kItems; ++i) {  // all loads in flight before any use
+    for (int i = 0; i < kWI; ++i) {  // all loads in flight before any use
         const uint64_t idx = wbase + 32 * i;
         k[i] = idx < tile_end ? keys[idx] : 0ull;
     }
     const uint64_t k_before = (lane == 0 && wbase > 0) ? keys[wbase - 1] : 0ull;
 #pragma unroll
-    for (int i = 0; i < kItems; ++i) {
+    for (int i = 0; i < kWI; ++i) {
         const uint64_t idx = wbase + 32 * i;
         const bool valid = idx < tile_end;
         uint64_t prev = __shfl_up_sync(0xffffffffu, k[i], 1);
@@ -238,15 +247,14 @@ __global__ void __launch_bounds__(kThreads)
     __syncthreads();
     uint32_t warp_base = 0, main_tot = 0;
 #pragma unroll
-    for (int w = 0; w < kWarps; ++w) {
+    for (int w = 0; w < kWW; ++w) {
         warp_base += (w < warp) ? s_warp_tot[w] : 0u;
         main_tot += s_warp_tot[w];
     }
-    const uint64_t base = offsets[blockIdx.x];
     uint64_t run = base + warp_base;
     const uint32_t lt = lanemask_lt();
 #pragma unroll
-    for (int i = 0; i < kItems; ++i) {
+    for (int i = 0; i < kWI; ++i) {
         const uint64_t idx = wbase + 32 * i;
         const bool flag = (ball[i] >> lane) & 1u;
         const uint64_t before = run + __popc(ball[i] & lt);  // flags strictly before idx
@@ -283,12 +291,17 @@ constexpr int kUWarps = kUThreads / 32;
 constexpr int kUItems = kUT / kUThreads;
 constexpr int kUStage = kUT + 72;  // tile + extension (>= kExt), 16 B multiple
 
+// kMode 0: single pass (fix-ups, counts, look-back, D).  kMode 1: fix-ups + per-tile counts
+// and owned ranges only (no look-back, no D).  kMode 2: D and grades from the per-tile
+// offsets of a scan of those counts (no fix-ups, no look-back) — the chain-free split.
+template <int kMode>
 __global__ void __launch_bounds__(kUThreads, 3)
     k3_unique_p(uint64_t* __restrict__ keys, uint32_t* __restrict__ vals, uint64_t count,
                 uint64_t kmin, uint32_t low_bits, double* __restrict__ scale,
                 uint32_t* __restrict__ grade, uint64_t* __restrict__ status, uint32_t epoch,
                 uint64_t* n_scale, uint32_t* redo, uint32_t num_tiles,
-                const uint64_t* __restrict__ d_base) {
+                const uint64_t* __restrict__ d_base, uint32_t* __restrict__ tile_counts,
+                int2* __restrict__ tile_own, const uint64_t* __restrict__ tile_offsets) {
     extern __shared__ __align__(128) uint64_t up_dyn[];
     __shared__ __align__(8) uint64_t s_bar[2];
     __shared__ uint32_t s_warp_tot[kUWarps];
@@ -347,7 +360,11 @@ __global__ void __launch_bounds__(kUThreads, 3)
         const uint64_t k_before = tile_start > 0 ? keys[tile_start - 1] : 0ull;
 
         uint32_t os = 0, oe = tn;
-        if (low_bits) {
+        if (kMode == 2) {
+            const int2 ow = tile_own[tile];
+            os = (uint32_t)ow.x;
+            oe = (uint32_t)ow.y;
+        } else if (low_bits) {
             // ---- fix the equal-prefix runs that start in this tile (stable, in smem) -----
             const uint64_t p_before = pre(k_before);
             for (uint32_t i = tid; i < tn; i += kUThreads) {
@@ -365,19 +382,26 @@ __global__ void __launch_bounds__(kUThreads, 3)
                 bool sorted = true;
                 for (uint32_t a = 1; a < len; ++a) sorted = sorted && s_k[i + a - 1] <= s_k[i + a];
                 if (sorted) continue;
+                // the run's columns: all loads issued together (one memory latency), then a
+                // stable insertion sort of (key, column) with the keys in shared memory
+                uint32_t lv[kMaxRun + 1];
+                for (uint32_t a = 0; a < len; ++a) lv[a] = vals[g + a];
                 for (uint32_t a = 1; a < len; ++a) {
                     const uint64_t kk = s_k[i + a];
-                    const uint32_t v = vals[g + a];
+                    const uint32_t v = lv[a];
                     uint32_t j = a;
                     while (j > 0 && s_k[i + j - 1] > kk) {
                         s_k[i + j] = s_k[i + j - 1];
-                        vals[g + j] = vals[g + j - 1];
+                        lv[j] = lv[j - 1];
                         --j;
                     }
                     s_k[i + j] = kk;
-                    vals[g + j] = v;
+                    lv[j] = v;
                 }
-                for (uint32_t a = 0; a < len; ++a) keys[g + a] = s_k[i + a];
+                for (uint32_t a = 0; a < len; ++a) {
+                    keys[g + a] = s_k[i + a];
+                    vals[g + a] = lv[a];
+                }
             }
             __syncthreads();
             if (tid == 0) {
@@ -422,8 +446,17 @@ __global__ void __launch_bounds__(kUThreads, 3)
             warp_base += (w < warp) ? s_warp_tot[w] : 0u;
             main_tot += s_warp_tot[w];
         }
-        const uint32_t tile_tot = main_tot + (low_bits ? s_ext_tot : 0u);
-        if (warp == 0) {  // warp-wide look-back: 32 predecessors per round trip
+        if (kMode == 1) {  // counts and owned range of this tile for the scan
+            if (tid == 0) {
+                tile_counts[tile] = main_tot + (low_bits ? s_ext_tot : 0u);
+                tile_own[tile] = make_int2((int)os, (int)oe);
+            }
+            continue;  // (the loop-top barrier orders the buffer reuse)
+        }
+        const uint32_t tile_tot = main_tot + (low_bits && kMode == 0 ? s_ext_tot : 0u);
+        if (kMode == 2) {
+            if (tid == 0) s_prefix = base0 + tile_offsets[tile];
+        } else if (warp == 0) {  // warp-wide look-back: 32 predecessors per round trip
             uint64_t* my = status + tile;
             uint32_t excl = 0;
             if (tile == 0) {
@@ -453,7 +486,7 @@ __global__ void __launch_bounds__(kUThreads, 3)
                 grade[tile_start + pos] = (uint32_t)(before + (flag ? 1u : 0u));
             run += __popc(ball[i]);
         }
-        if (low_bits && tid == 0 && oe > tn) {  // the extension of this tile's last run
+        if (tid == 0 && oe > tn) {  // the extension of this tile's last run
             uint64_t r = base + main_tot;
             for (uint32_t g = tn; g < oe; ++g) {
                 const bool f = s_k[g] != s_k[g - 1];
@@ -475,47 +508,58 @@ int launch_unique(const UniqueArgs& a, cudaStream_t s) {
         cudaMemsetAsync(a.n_scale, 0, sizeof(uint64_t), s);
         return 0;
     }
-    static const bool three_kernels_env = [] {
+    static const int mode_env = [] {  // PH0B_UNIQUE: 1 single pass, 2 split (default), 3 legacy
         const char* e = getenv("PH0B_UNIQUE");
-        return e && e[0] == '3';
+        return e ? atoi(e) : 2;
     }();
-    const bool three_kernels = three_kernels_env && !a.d_base;
-    if (!three_kernels) {
-        const size_t smem = (size_t)2 * kUStage * 8;
-        static int per_sm = 0;
-        static int num_sms = 0;
-        if (!per_sm) {
-            cudaFuncSetAttribute(k3_unique_p, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-            cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k3_unique_p, kUThreads, smem);
-            if (per_sm < 1) per_sm = 1;
-            int dev = 0;
-            cudaGetDevice(&dev);
-            cudaDeviceGetAttribute(&num_sms, cudaDevAttrMultiProcessorCount, dev);
-        }
-        const uint64_t tiles = (a.count + kUT - 1) / kUT;
-        uint64_t grid = (uint64_t)num_sms * per_sm;
-        if (grid > tiles) grid = tiles;
-        k3_unique_p<<<(unsigned)grid, kUThreads, smem, s>>>(
-            a.keys, a.vals, a.count, a.kmin, a.low_bits, a.scale, a.grade, a.status, a.epoch,
-            a.n_scale, a.redo, (uint32_t)tiles, a.d_base);
-        return 1;
-    }
-    const uint64_t tiles = (a.count + kTileKeys - 1) / kTileKeys;
+    const uint64_t tiles = (a.count + kUT - 1) / kUT;
+    static_assert(kUT == kTileKeys, "the split and legacy kernels share the tiling");
     // scratch: counts (u32) | own (int2) | offsets (u64), unique_scratch_words(count) words
     uint32_t* counts = reinterpret_cast<uint32_t*>(a.scratch);
     int2* own = reinterpret_cast<int2*>(a.scratch + (tiles + 1) / 2 + 1);
     uint64_t* offsets = a.scratch + (tiles + 1) / 2 + 1 + tiles + 1;
-    const size_t smem = a.low_bits ? (size_t)(kTileKeys + kExt) * 8 : 0;
-    static bool configured = false;
-    if (!configured) {
-        cudaFuncSetAttribute(k3_count, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                             (kTileKeys + kExt) * 8);
-        configured = true;
+    if (mode_env == 3 && !a.d_base) {
+        const size_t smem = a.low_bits ? (size_t)(kTileKeys + kExt) * 8 : 0;
+        static bool configured = false;
+        if (!configured) {
+            cudaFuncSetAttribute(k3_count, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 (kTileKeys + kExt) * 8);
+            configured = true;
+        }
+        k3_count<<<(unsigned)tiles, kThreads, smem, s>>>(a.keys, a.vals, a.count, a.kmin,
+                                                        a.low_bits, counts, own, a.redo);
+        k3_scan<<<1, 1024, 0, s>>>(counts, (uint32_t)tiles, offsets, a.n_scale, nullptr);
+        k3_write<kThreads><<<(unsigned)tiles, kThreads, 0, s>>>(a.keys, a.count, own, offsets,
+                                                               a.scale, a.grade);
+        return 3;
     }
-    k3_count<<<(unsigned)tiles, kThreads, smem, s>>>(a.keys, a.vals, a.count, a.kmin, a.low_bits,
-                                                    counts, own, a.redo);
-    k3_scan<<<1, 1024, 0, s>>>(counts, (uint32_t)tiles, offsets, a.n_scale);
-    k3_write<<<(unsigned)tiles, kThreads, 0, s>>>(a.keys, a.count, own, offsets, a.scale, a.grade);
+    const size_t smem = (size_t)2 * kUStage * 8;
+    static int per_sm = 0;
+    static int num_sms = 0;
+    if (!per_sm) {
+        for (auto kern : {k3_unique_p<0>, k3_unique_p<1>, k3_unique_p<2>})
+            cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k3_unique_p<0>, kUThreads, smem);
+        if (per_sm < 1) per_sm = 1;
+        int dev = 0;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&num_sms, cudaDevAttrMultiProcessorCount, dev);
+    }
+    uint64_t grid = (uint64_t)num_sms * per_sm;
+    if (grid > tiles) grid = tiles;
+    if (mode_env == 1) {
+        k3_unique_p<0><<<(unsigned)grid, kUThreads, smem, s>>>(
+            a.keys, a.vals, a.count, a.kmin, a.low_bits, a.scale, a.grade, a.status, a.epoch,
+            a.n_scale, a.redo, (uint32_t)tiles, a.d_base, nullptr, nullptr, nullptr);
+        return 1;
+    }
+    k3_unique_p<1><<<(unsigned)grid, kUThreads, smem, s>>>(
+        a.keys, a.vals, a.count, a.kmin, a.low_bits, a.scale, a.grade, a.status, a.epoch,
+        a.n_scale, a.redo, (uint32_t)tiles, a.d_base, counts, own, nullptr);
+    k3_scan<<<1, 1024, 0, s>>>(counts, (uint32_t)tiles, offsets, a.n_scale, a.d_base);
+    k3_unique_p<2><<<(unsigned)grid, kUThreads, smem, s>>>(
+        a.keys, a.vals, a.count, a.kmin, a.low_bits, a.scale, a.grade, a.status, a.epoch,
+        a.n_scale, a.redo, (uint32_t)tiles, a.d_base, counts, own, offsets);
     return 3;
 }
 
