@@ -272,3 +272,37 @@ def test_overlapped_host_path_separated_clusters():
     assert np.array_equal(bits(dl[:nf]), bits(bc.death_length))
     assert np.array_equal(bits(sc[:ns]), bits(bc.scale))
     ctx.close()
+
+
+@pytest.mark.parametrize("kind", ["identical", "lattice", "line", "two_far"])
+def test_pathological_large(kind):
+    """~1.3e8 edges with massive ties / a zero span / duplicate lengths: exercises the
+    zero-pass plan, the equal-prefix redo (runs longer than the fix-up limit) and the
+    overlapped host path at scale; checked by size-independent invariants, the MST length
+    multiset (Prim with the reference's fold) and the GPU Kruskal oracle."""
+    n = 16384
+    if kind == "identical":
+        X = np.full((n, 3), 0.25)
+    elif kind == "lattice":
+        X = np.array([[x, y] for x in range(128) for y in range(128)], np.float64)
+    elif kind == "line":
+        X = np.arange(n, dtype=np.float64)[:, None] % 1000.0
+    else:
+        rng = np.random.default_rng(3)
+        X = rng.normal(size=(n, 4))
+        X[: n // 2] += 1e6
+    bc = pkg.h0_barcode(X)
+    check_large(X, bc)
+    kr = pkg.kruskal_barcode(X, return_scale=False)
+    assert np.array_equal(kr.death_grade, bc.death_grade)
+    assert np.array_equal(bits(kr.death_length), bits(bc.death_length))
+    ctx = pkg.Context(0)
+    dg = np.empty(n, np.uint64)
+    dl = np.empty(n)
+    sc = np.empty(len(bc.scale))
+    nf, ess, ns, t = ctx.run_host(np.asfortranarray(X), dg, dl, sc)  # overlapped (K >= 2^26)
+    assert nf == n - 1 and ess == 1 and ns == len(bc.scale)
+    assert np.array_equal(dg[:nf], bc.death_grade)
+    assert np.array_equal(bits(dl[:nf]), bits(bc.death_length))
+    assert np.array_equal(bits(sc), bits(bc.scale))
+    ctx.close()
