@@ -28,7 +28,7 @@
 extern "C" {
 #endif
 
-#define PH0B_ABI_VERSION 1u
+#define PH0B_ABI_VERSION 2u
 
 /* Return codes.  The message of ph0b_last_error() repeats the reference's exception text
  * where the reference has one. */
@@ -79,6 +79,8 @@ typedef struct ph0b_stage_times {
     uint32_t sort_passes;
     uint32_t reduce_rounds;
     uint64_t columns_scanned; /* edge columns streamed by the reduction */
+    float sort_passes_ms;     /* the radix passes alone (sort_ms minus the digit histogram) */
+    uint32_t reserved0;
 } ph0b_stage_times;
 
 /* Host-side result of ph0b_h0_barcode; arrays are owned by the library. */

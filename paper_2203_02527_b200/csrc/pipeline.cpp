@@ -362,6 +362,7 @@ Status Context::sort_unique_range(uint64_t* kb0, uint32_t* vb0, uint64_t* kb1, u
             sa.hist0_rot = (uint32_t)(kmin & 0xFFu);  // distance kernel's raw low-byte histogram
         }
         int sl = 0;
+        PH0B_TRY(cudaEventRecord(ev_[8], st), "event");
         const int out = launch_sort_passes(sa, plan, st, num_sms_, &sl);
         *res = src ^ out;
         launches += sl;
@@ -514,6 +515,7 @@ Status Context::run(const double* dX, uint64_t n, uint64_t d, uint32_t layout,
     r.n_scale = h_small_[2];
     cudaEventElapsedTime(&r.times.distance_ms, ev_[0], ev_[1]);
     cudaEventElapsedTime(&r.times.sort_ms, ev_[1], ev_[2]);
+    cudaEventElapsedTime(&r.times.sort_passes_ms, ev_[8], ev_[2]);
     cudaEventElapsedTime(&r.times.unique_ms, ev_[2], ev_[3]);
     if (stop == StopAfter::Barcode) {
         cudaEventElapsedTime(&r.times.reduce_ms, ev_[3], ev_[4]);

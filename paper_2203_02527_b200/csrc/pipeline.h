@@ -112,7 +112,7 @@ private:
     int device_;
     int num_sms_ = 148;
     cudaStream_t stream_ = nullptr;
-    cudaEvent_t ev_[8] = {};  // [6]: per-bucket completion (overlapped host path)
+    cudaEvent_t ev_[9] = {};  // [6]: per-bucket completion, [7]: redo check, [8]: passes start
     uint64_t bytes_ = 0;
 
     // workspace (capacities in bytes)

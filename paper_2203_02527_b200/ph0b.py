@@ -59,7 +59,8 @@ class StageTimes(C.Structure):
     _fields_ = [("distance_ms", C.c_float), ("sort_ms", C.c_float), ("unique_ms", C.c_float),
                 ("reduce_ms", C.c_float), ("collect_ms", C.c_float), ("total_ms", C.c_float),
                 ("sort_passes", C.c_uint32), ("reduce_rounds", C.c_uint32),
-                ("columns_scanned", C.c_uint64)]
+                ("columns_scanned", C.c_uint64), ("sort_passes_ms", C.c_float),
+                ("reserved0", C.c_uint32)]
 
     def as_dict(self):
         return {f: getattr(self, f) for f, _ in self._fields_}
