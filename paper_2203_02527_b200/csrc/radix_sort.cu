@@ -415,16 +415,43 @@ __global__ void __launch_bounds__(kThreads, 2)
 
 // Histogram of one digit of (key - kmin) (used only when the distance kernel's raw
 // low-byte histogram does not apply, e.g. for the survivor sort).
-__global__ void k2_digit_histogram(const uint64_t* __restrict__ keys, uint64_t count,
-                                   uint64_t kmin, uint32_t shift, uint32_t* hist) {
-    __shared__ uint32_t h[kBins];
-    h[threadIdx.x] = 0;
+// 8 independent 16-byte loads (16 keys) in flight per thread per step, per-warp shared
+// histograms (no cross-warp contention), one global add per bin per block.
+__global__ void __launch_bounds__(kBins)
+    k2_digit_histogram(const uint64_t* __restrict__ keys, uint64_t count, uint64_t kmin,
+                       uint32_t shift, uint32_t* hist) {
+    __shared__ uint32_t h[kBins / 32][kBins];
+    const int warp = threadIdx.x >> 5;
+#pragma unroll
+    for (int w = 0; w < kBins / 32; ++w) h[w][threadIdx.x] = 0;
     __syncthreads();
-    for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < count;
-         i += (uint64_t)gridDim.x * blockDim.x)
-        atomicAdd(&h[(uint32_t)((keys[i] - kmin) >> shift) & 0xFFu], 1u);
+    auto add = [&](uint64_t k) { atomicAdd(&h[warp][(uint32_t)((k - kmin) >> shift) & 0xFFu], 1u); };
+    constexpr int kU = 8;  // ulonglong2 loads per thread per step
+    const uint64_t pairs = count / 2;
+    const ulonglong2* k2 = reinterpret_cast<const ulonglong2*>(keys);
+    const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+    uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
+    for (; i + (kU - 1) * stride < pairs; i += kU * stride) {
+        ulonglong2 v[kU];
+#pragma unroll
+        for (int u = 0; u < kU; ++u) v[u] = k2[i + u * stride];
+#pragma unroll
+        for (int u = 0; u < kU; ++u) {
+            add(v[u].x);
+            add(v[u].y);
+        }
+    }
+    for (; i < pairs; i += stride) {
+        const ulonglong2 v = k2[i];
+        add(v.x);
+        add(v.y);
+    }
+    if ((count & 1) && blockIdx.x == 0 && threadIdx.x == 0) add(keys[count - 1]);
     __syncthreads();
-    if (h[threadIdx.x]) atomicAdd(&hist[threadIdx.x], h[threadIdx.x]);
+    uint32_t c = 0;
+#pragma unroll
+    for (int w = 0; w < kBins / 32; ++w) c += h[w][threadIdx.x];
+    if (c) atomicAdd(&hist[threadIdx.x], c);
 }
 
 template <bool kVals, bool kCountNext, int kRank, int kMinBlocks>
@@ -549,6 +576,11 @@ int launch_digit_histogram(const uint64_t* keys, uint64_t count, uint64_t kmin, 
     uint64_t blocks = (count + kBins - 1) / kBins;
     const uint64_t cap = (uint64_t)num_sms * 8;
     if (blocks > cap) blocks = cap;
+    if (reinterpret_cast<uintptr_t>(keys) & 15u) {  // 16-byte loads: peel one key
+        k2_digit_histogram<<<1, kBins, 0, s>>>(keys, 1, kmin, shift, hist);
+        ++keys;
+        --count;
+    }
     k2_digit_histogram<<<(unsigned)blocks, kBins, 0, s>>>(keys, count, kmin, shift, hist);
     return 1;
 }
