@@ -58,8 +58,6 @@ __device__ __forceinline__ uint32_t block_scan_256(uint32_t x, uint32_t* sh_warp
     return wb + inc - x;
 }
 
-// Per-tile bucket counts (one ATOMS per key; the bucket key ranges themselves come from the
-// splitters, so no per-key min/max is needed).
 // Bucket lookup table over the top kCellBits of (key - kmin): the bucket of every cell that
 // no splitter falls inside, or kAmbiguous (binary search) for the <= parts-1 cells that hold a
 // splitter.  Built on the host per partition (build_cell_table).
@@ -81,6 +79,9 @@ __device__ __forceinline__ uint32_t bucket_fast(uint64_t key, const uint16_t* s_
     return b != kAmbiguous ? b : bucket_of(key, s_spl, nspl);
 }
 
+// Per-tile bucket counts, bucket-major (counts[b * tiles + t], one block per tile); one ATOMS
+// per key (the bucket key ranges themselves come from the splitters, so no per-key min/max
+// is needed).
 __global__ void __launch_bounds__(kThreads)
     k7_count(const uint64_t* __restrict__ keys, uint64_t count, const uint64_t* __restrict__ splitters,
              uint32_t parts, uint32_t* __restrict__ counts, const uint16_t* __restrict__ cells,
@@ -109,7 +110,7 @@ __global__ void __launch_bounds__(kThreads)
             atomicAdd(&s_cnt[bucket_fast(k[i], s_cell, s_spl, parts - 1, cm)], 1u);
     __syncthreads();
     for (uint32_t b = threadIdx.x; b < parts; b += kThreads)
-        counts[(uint64_t)blockIdx.x * parts + b] = s_cnt[b];
+        counts[(uint64_t)b * gridDim.x + blockIdx.x] = s_cnt[b];
 }
 
 // Evenly spaced sample of keys[0..count) (splitter selection).
@@ -127,37 +128,60 @@ __global__ void k7_gather_u32(const uint32_t* __restrict__ src, const uint32_t* 
         out[i] = src[idx[i]];
 }
 
-// One block per bucket: exclusive scan of that bucket's per-tile counts, and its total.
-__global__ void k7_scan(uint32_t* __restrict__ counts, uint32_t tiles, uint32_t parts,
-                        uint64_t* __restrict__ totals) {
-    __shared__ uint64_t s_carry;
-    __shared__ uint32_t s_warp[32];
-    const uint32_t b = blockIdx.x;
-    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
-    if (threadIdx.x == 0) s_carry = 0;
-    __syncthreads();
-    for (uint32_t t0 = 0; t0 < tiles; t0 += blockDim.x) {
-        const uint32_t t = t0 + threadIdx.x;
-        const uint32_t x = t < tiles ? counts[(uint64_t)t * parts + b] : 0u;
-        uint32_t inc = x;
-        for (int o = 1; o < 32; o <<= 1) {
-            const uint32_t y = __shfl_up_sync(0xffffffffu, inc, o);
-            if (lane >= o) inc += y;
+// One block per bucket: exclusive scan of that bucket's (contiguous) per-tile counts, in
+// place, and its total.  Warp w walks a contiguous chunk 32 counts at a time.
+__global__ void __launch_bounds__(1024)
+    k7_scan(uint32_t* __restrict__ counts, uint32_t tiles, uint32_t parts,
+            uint64_t* __restrict__ totals) {
+    __shared__ uint64_t s_tot[32];
+    const uint32_t bk = blockIdx.x;
+    uint32_t* c = counts + (uint64_t)bk * tiles;
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const uint32_t per = ((tiles + 31) / 32 + 31) / 32 * 32;
+    const uint32_t b = warp * per;
+    const uint32_t e = b + per < tiles ? b + per : tiles;
+    uint64_t tot = 0;
+    constexpr int kU = 8;  // independent loads in flight per lane
+    for (uint32_t t0 = b; t0 < e; t0 += 32 * kU) {
+        uint32_t x[kU];
+#pragma unroll
+        for (int u = 0; u < kU; ++u) {
+            const uint32_t t = t0 + 32 * u + lane;
+            x[u] = t < e ? c[t] : 0u;
         }
-        if (lane == 31) s_warp[warp] = inc;
-        __syncthreads();
-        uint32_t wb = 0, tot = 0;
-        for (int w = 0; w < nw; ++w) {
-            wb += w < warp ? s_warp[w] : 0u;
-            tot += s_warp[w];
-        }
-        const uint64_t carry = s_carry;
-        if (t < tiles) counts[(uint64_t)t * parts + b] = (uint32_t)(carry + wb + inc - x);
-        __syncthreads();
-        if (threadIdx.x == 0) s_carry = carry + tot;
-        __syncthreads();
+        uint32_t sum = 0;
+#pragma unroll
+        for (int u = 0; u < kU; ++u) sum += x[u];
+        tot += __reduce_add_sync(0xffffffffu, sum);
     }
-    if (threadIdx.x == 0) totals[b] = s_carry;
+    if (lane == 0) s_tot[warp] = tot;
+    __syncthreads();
+    uint64_t carry = 0, all = 0;
+    for (int w = 0; w < 32; ++w) {
+        carry += w < warp ? s_tot[w] : 0u;
+        all += s_tot[w];
+    }
+    for (uint32_t t0 = b; t0 < e; t0 += 32 * kU) {
+        uint32_t x[kU];
+#pragma unroll
+        for (int u = 0; u < kU; ++u) {
+            const uint32_t t = t0 + 32 * u + lane;
+            x[u] = t < e ? c[t] : 0u;
+        }
+#pragma unroll
+        for (int u = 0; u < kU; ++u) {
+            const uint32_t t = t0 + 32 * u + lane;
+            uint32_t inc = x[u];
+#pragma unroll
+            for (int o = 1; o < 32; o <<= 1) {
+                const uint32_t y = __shfl_up_sync(0xffffffffu, inc, o);
+                if (lane >= o) inc += y;
+            }
+            if (t < e) c[t] = (uint32_t)(carry + inc - x[u]);
+            carry += __shfl_sync(0xffffffffu, inc, 31);
+        }
+    }
+    if (threadIdx.x == 0) totals[bk] = all;
 }
 
 // One block: padded segment starts (segments begin on `align`-element boundaries), the
@@ -225,7 +249,8 @@ __global__ void __launch_bounds__(kThreads, 3)
     s_spl[tid] = (uint32_t)tid + 1 < parts ? splitters[tid] : ~0ull;
     for (uint32_t i = tid; i < kCells / 8; i += kThreads)
         reinterpret_cast<uint4*>(s_cell)[i] = reinterpret_cast<const uint4*>(cells)[i];
-    const uint64_t my_base = (uint32_t)tid < parts ? starts[tid] + offsets[(uint64_t)blockIdx.x * parts + tid] : 0ull;
+    const uint64_t my_base =
+        (uint32_t)tid < parts ? starts[tid] + offsets[(uint64_t)tid * gridDim.x + blockIdx.x] : 0ull;
 #pragma unroll
     for (int w = 0; w < kWarps; ++w) s_whist[w][tid] = 0;
     __syncthreads();
@@ -306,7 +331,7 @@ __global__ void __launch_bounds__(kThreads)
     uint32_t wb = 0;
 #pragma unroll
     for (int w = 0; w < kWarps; ++w) wb += (w < warp) ? s_wt[w] : 0u;
-    uint64_t run = starts[b] + offsets[(uint64_t)blockIdx.x * parts + b] + wb;
+    uint64_t run = starts[b] + offsets[(uint64_t)b * gridDim.x + blockIdx.x] + wb;
     const uint32_t lt = lanemask_lt();
 #pragma unroll
     for (int i = 0; i < kItems; ++i) {

@@ -184,9 +184,18 @@ __global__ void __launch_bounds__(1024)
     const uint32_t b = warp * per;
     const uint32_t e = b + per < tiles ? b + per : tiles;
     uint64_t tot = 0;
-    for (uint32_t t = b; t < e; t += 32) {
-        const uint32_t c = t + lane < e ? counts[t + lane] : 0u;
-        tot += __reduce_add_sync(0xffffffffu, c);
+    constexpr int kU = 8;  // independent loads in flight per lane
+    for (uint32_t t0 = b; t0 < e; t0 += 32 * kU) {
+        uint32_t x[kU];
+#pragma unroll
+        for (int u = 0; u < kU; ++u) {
+            const uint32_t t = t0 + 32 * u + lane;
+            x[u] = t < e ? counts[t] : 0u;
+        }
+        uint32_t sum = 0;
+#pragma unroll
+        for (int u = 0; u < kU; ++u) sum += x[u];
+        tot += __reduce_add_sync(0xffffffffu, sum);
     }
     if (lane == 0) s_tot[warp] = tot;
     __syncthreads();
@@ -195,16 +204,25 @@ __global__ void __launch_bounds__(1024)
         carry += w < warp ? s_tot[w] : 0u;
         all += s_tot[w];
     }
-    for (uint32_t t = b; t < e; t += 32) {
-        const uint32_t c = t + lane < e ? counts[t + lane] : 0u;
-        uint32_t inc = c;
+    for (uint32_t t0 = b; t0 < e; t0 += 32 * kU) {
+        uint32_t x[kU];
 #pragma unroll
-        for (int o = 1; o < 32; o <<= 1) {
-            const uint32_t y = __shfl_up_sync(0xffffffffu, inc, o);
-            if (lane >= o) inc += y;
+        for (int u = 0; u < kU; ++u) {
+            const uint32_t t = t0 + 32 * u + lane;
+            x[u] = t < e ? counts[t] : 0u;
         }
-        if (t + lane < e) offsets[t + lane] = carry + inc - c;
-        carry += __shfl_sync(0xffffffffu, inc, 31);
+#pragma unroll
+        for (int u = 0; u < kU; ++u) {
+            const uint32_t t = t0 + 32 * u + lane;
+            uint32_t inc = x[u];
+#pragma unroll
+            for (int o = 1; o < 32; o <<= 1) {
+                const uint32_t y = __shfl_up_sync(0xffffffffu, inc, o);
+                if (lane >= o) inc += y;
+            }
+            if (t < e) offsets[t] = carry + inc - x[u];
+            carry += __shfl_sync(0xffffffffu, inc, 31);
+        }
     }
     if (threadIdx.x == 0) *n_scale = (d_base ? *d_base : 0ull) + all;
 }
