@@ -6,9 +6,11 @@
 //   grade_i = inclusive_scan(flag)_i                     (1-based, filtration.cpp:32)
 //   D[grade_i - 1] = length_i  for flagged i             (Filtration::scale)
 //
-// Single pass: one 4096-key tile per CTA (dynamic tile ids), warp ballots for the
-// in-tile scan, decoupled look-back for the prefix across tiles.  Column j of M is
-// {u_j, v_j} at grade_j: the sorted (u << 16 | v) array already holds the supports, and
+// Default: a chain-free split over 4096-key tiles — (1) a persistent TMA-staged count pass
+// (run fix-ups of truncated radix plans, per-tile distinct counts and owned ranges), (2) a
+// scan of the tile counts, (3) a persistent TMA-staged pass writing D and the grades.  The
+// single-pass variant with decoupled look-back is kept behind PH0B_UNIQUE=1.  Column j of M
+// is {u_j, v_j} at grade_j: the sorted (u << 16 | v) array already holds the supports, and
 // the grades are written only when requested (parity surfaces); the barcode collect
 // recovers a survivor's grade from D by binary search instead.
 #include <cuda_runtime.h>
@@ -22,155 +24,11 @@
 namespace ph0b {
 namespace {
 
-constexpr int kThreads = 512;
-constexpr int kWarps = kThreads / 32;
-constexpr int kItems = 8;
-constexpr int kTileKeys = kThreads * kItems;
+constexpr int kTileKeys = 4096;  // keys per tile (all unique kernels and the scratch sizing)
 
 constexpr uint32_t kMaxRun = 64;  // longest equal-prefix run fixed up in place
 
-// Three kernels, no look-back: count the distinct lengths of every tile (fixing the
-// equal-prefix runs of a truncated radix plan in shared memory first), scan the tile counts,
-// then write D and the grades.  Keys are read twice (8 B + 8 B) and D written once (8 B);
-// no CTA ever waits on another.
 constexpr int kExt = (int)kMaxRun + 1;  // extension past the tile end (runs crossing it)
-
-__device__ __forceinline__ bool is_run_start(uint64_t p, uint64_t pprev, uint64_t pnext,
-                                             bool has_prev, bool has_next) {
-    return has_next && pnext == p && !(has_prev && pprev == p);
-}
-
-__global__ void __launch_bounds__(kThreads)
-    k3_count(uint64_t* __restrict__ keys, uint32_t* __restrict__ vals, uint64_t count,
-             uint64_t kmin, uint32_t low_bits, uint32_t* __restrict__ counts,
-             int2* __restrict__ own, uint32_t* redo) {
-    extern __shared__ __align__(16) uint64_t u_dyn[];
-    uint64_t* s_k = u_dyn;                                              // [kTileKeys + kExt]
-    __shared__ uint32_t s_warp_tot[kWarps];
-    __shared__ int s_own[2];
-    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-    const uint64_t tile_start = (uint64_t)blockIdx.x * kTileKeys;
-    const uint64_t tile_end = tile_start + kTileKeys < count ? tile_start + kTileKeys : count;
-    const uint64_t wbase = tile_start + (uint64_t)warp * (32 * kItems) + lane;
-    auto pre = [&](uint64_t kk) { return (kk - kmin) >> low_bits; };
-
-    if (low_bits == 0) {
-        uint64_t k[kItems];
-#pragma unroll
-        for (int i = 0; i < kItems; ++i) {  // all loads in flight before any use
-            const uint64_t idx = wbase + 32 * i;
-            k[i] = idx < tile_end ? keys[idx] : 0ull;
-        }
-        const uint64_t k_before = (lane == 0 && wbase > 0) ? keys[wbase - 1] : 0ull;
-        uint32_t total = 0;
-#pragma unroll
-        for (int i = 0; i < kItems; ++i) {
-            const uint64_t idx = wbase + 32 * i;
-            uint64_t prev = __shfl_up_sync(0xffffffffu, k[i], 1);
-            const uint64_t last = __shfl_sync(0xffffffffu, i ? k[i - 1] : 0ull, 31);
-            if (lane == 0) prev = i ? last : k_before;
-            total += __popc(__ballot_sync(0xffffffffu, idx < tile_end && (idx == 0 || k[i] != prev)));
-        }
-        if (lane == 0) s_warp_tot[warp] = total;
-        __syncthreads();
-        if (tid == 0) {
-            uint32_t t = 0;
-            for (int w = 0; w < kWarps; ++w) t += s_warp_tot[w];
-            counts[blockIdx.x] = t;
-            own[blockIdx.x] = make_int2(0, (int)(tile_end - tile_start));
-        }
-        return;
-    }
-
-    // ---- stage the tile (+ extension) in shared memory ------------------------------------
-    const uint64_t ext_end = tile_end + kExt < count ? tile_end + kExt : count;
-    const uint32_t staged = (uint32_t)(ext_end - tile_start);
-    {
-        uint64_t t[kItems];
-#pragma unroll
-        for (int i = 0; i < kItems; ++i) {  // all loads in flight before any store
-            const uint32_t j = i * kThreads + tid;
-            t[i] = j < staged ? keys[tile_start + j] : 0ull;
-        }
-#pragma unroll
-        for (int i = 0; i < kItems; ++i) {
-            const uint32_t j = i * kThreads + tid;
-            if (j < staged) s_k[j] = t[i];
-        }
-        if (tid < kExt && kTileKeys + tid < staged) s_k[kTileKeys + tid] = keys[tile_start + kTileKeys + tid];
-    }
-    __syncthreads();
-    const uint64_t p_before = tile_start > 0 ? pre(keys[tile_start - 1]) : 0ull;
-
-    // ---- phase A: fix the runs that start in this tile (stable insertion sort, smem) -----
-    for (uint32_t i = tid; i < (uint32_t)(tile_end - tile_start); i += kThreads) {
-        const uint64_t g = tile_start + i;
-        if (g + 1 >= count) continue;
-        const uint64_t p = pre(s_k[i]);
-        const bool has_prev = g > 0;
-        const uint64_t pp = i > 0 ? pre(s_k[i - 1]) : p_before;
-        if (!is_run_start(p, pp, i + 1 < staged ? pre(s_k[i + 1]) : ~p, has_prev, i + 1 < staged))
-            continue;
-        uint32_t len = 2;
-        while (i + len < staged && len <= kMaxRun && pre(s_k[i + len]) == p) ++len;
-        if (len > kMaxRun || (i + len == staged && ext_end < count)) {
-            atomicOr(redo, 1u);  // too long to fix here: the caller re-sorts every digit
-            continue;
-        }
-        bool sorted = true;
-        for (uint32_t a = 1; a < len; ++a) sorted = sorted && s_k[i + a - 1] <= s_k[i + a];
-        if (sorted) continue;  // already in (length, u, v) order
-        // stable insertion sort of keys (shared) and their columns (global, rare)
-        for (uint32_t a = 1; a < len; ++a) {
-            const uint64_t k = s_k[i + a];
-            const uint32_t v = vals[g + a];
-            uint32_t j = a;
-            while (j > 0 && s_k[i + j - 1] > k) {
-                s_k[i + j] = s_k[i + j - 1];
-                vals[g + j] = vals[g + j - 1];
-                --j;
-            }
-            s_k[i + j] = k;
-            vals[g + j] = v;
-        }
-        for (uint32_t a = 0; a < len; ++a) keys[g + a] = s_k[i + a];
-    }
-    __syncthreads();
-
-    // ---- ownership: skip a run continuing from the previous tile; extend through the run
-    // that crosses the tile end ---------------------------------------------------------------
-    if (tid == 0) {
-        uint32_t st = 0;
-        if (tile_start > 0)
-            while (st < (uint32_t)(tile_end - tile_start) && pre(s_k[st]) == p_before) ++st;
-        uint32_t e = (uint32_t)(tile_end - tile_start);
-        if (e > st && e < staged) {
-            const uint64_t pl = pre(s_k[e - 1]);
-            while (e < staged && pre(s_k[e]) == pl) ++e;
-        }
-        if (st >= (uint32_t)(tile_end - tile_start)) st = e = (uint32_t)(tile_end - tile_start);
-        s_own[0] = (int)st;
-        s_own[1] = (int)e;
-    }
-    __syncthreads();
-    const uint32_t os = (uint32_t)s_own[0], oe = (uint32_t)s_own[1];
-    uint32_t total = 0;
-    for (uint32_t i0 = 0; i0 < oe; i0 += kThreads) {
-        const uint32_t i = i0 + tid;
-        const bool f = i >= os && i < oe &&
-                       (tile_start + i == 0 || (i > 0 ? s_k[i] != s_k[i - 1]
-                                                      : s_k[0] != keys[tile_start - 1]));
-        total += __popc(__ballot_sync(0xffffffffu, f));
-    }
-    if (lane == 0) s_warp_tot[warp] = total;
-    __syncthreads();
-    if (tid == 0) {
-        uint32_t t = 0;
-        for (int w = 0; w < kWarps; ++w) t += s_warp_tot[w];
-        counts[blockIdx.x] = t;
-        own[blockIdx.x] = make_int2((int)os, (int)oe);
-    }
-}
 
 // Exclusive scan of the per-tile distinct counts by one block of 32 warps: warp w owns a
 // contiguous chunk and walks it 32 counts at a time (coalesced loads, warp scan, running
@@ -225,72 +83,6 @@ __global__ void __launch_bounds__(1024)
         }
     }
     if (threadIdx.x == 0) *n_scale = (d_base ? *d_base : 0ull) + all;
-}
-
-template <int kWT>
-__global__ void __launch_bounds__(kWT)
-    k3_write(const uint64_t* __restrict__ keys, uint64_t count, const int2* __restrict__ own,
-             const uint64_t* __restrict__ offsets, double* __restrict__ scale,
-             uint32_t* __restrict__ grade) {
-    constexpr int kWW = kWT / 32, kWI = kTileKeys / kWT;
-    __shared__ uint32_t s_warp_tot[kWW];
-    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-    const uint64_t tile_start = (uint64_t)blockIdx.x * kTileKeys;
-    const uint64_t tile_end = tile_start + kTileKeys < count ? tile_start + kTileKeys : count;
-    const uint64_t base = offsets[blockIdx.x];  // independent of the keys: issue first
-    const int2 ow = own[blockIdx.x];
-    const uint64_t own_start = tile_start + (uint64_t)ow.x, own_end = tile_start + (uint64_t)ow.y;
-    const uint64_t wbase = tile_start + (uint64_t)warp * (32 * kWI) + lane;
-    uint64_t k[kWI];
-    uint32_t ball[kWI];
-    uint32_t total = 0;
-#pragma unroll
-    for (int i = 0; i < kWI; ++i) {  // all loads in flight before any use
-        const uint64_t idx = wbase + 32 * i;
-        k[i] = idx < tile_end ? keys[idx] : 0ull;
-    }
-    const uint64_t k_before = (lane == 0 && wbase > 0) ? keys[wbase - 1] : 0ull;
-#pragma unroll
-    for (int i = 0; i < kWI; ++i) {
-        const uint64_t idx = wbase + 32 * i;
-        const bool valid = idx < tile_end;
-        uint64_t prev = __shfl_up_sync(0xffffffffu, k[i], 1);
-        const uint64_t last = __shfl_sync(0xffffffffu, i ? k[i - 1] : 0ull, 31);
-        if (lane == 0) prev = i ? last : k_before;
-        const bool owned = valid && idx >= own_start && idx < own_end;
-        ball[i] = __ballot_sync(0xffffffffu, owned && (idx == 0 || k[i] != prev));
-        total += __popc(ball[i]);
-    }
-    if (lane == 0) s_warp_tot[warp] = total;
-    __syncthreads();
-    uint32_t warp_base = 0, main_tot = 0;
-#pragma unroll
-    for (int w = 0; w < kWW; ++w) {
-        warp_base += (w < warp) ? s_warp_tot[w] : 0u;
-        main_tot += s_warp_tot[w];
-    }
-    uint64_t run = base + warp_base;
-    const uint32_t lt = lanemask_lt();
-#pragma unroll
-    for (int i = 0; i < kWI; ++i) {
-        const uint64_t idx = wbase + 32 * i;
-        const bool flag = (ball[i] >> lane) & 1u;
-        const uint64_t before = run + __popc(ball[i] & lt);  // flags strictly before idx
-        if (flag) scale[before] = __longlong_as_double((long long)k[i]);
-        if (grade && idx >= own_start && idx < own_end)
-            grade[idx] = (uint32_t)(before + (flag ? 1u : 0u));
-        run += __popc(ball[i]);
-    }
-    // the extension: elements past the tile end that belong to this tile's last run
-    if (tid == 0 && own_end > tile_end) {
-        uint64_t r = base + main_tot;
-        for (uint64_t g = tile_end; g < own_end; ++g) {
-            const bool f = keys[g] != keys[g - 1];
-            if (f) scale[r] = __longlong_as_double((long long)keys[g]);
-            r += f ? 1u : 0u;
-            if (grade) grade[g] = (uint32_t)r;
-        }
-    }
 }
 
 }  // namespace
@@ -526,31 +318,16 @@ int launch_unique(const UniqueArgs& a, cudaStream_t s) {
         cudaMemsetAsync(a.n_scale, 0, sizeof(uint64_t), s);
         return 0;
     }
-    static const int mode_env = [] {  // PH0B_UNIQUE: 1 single pass, 2 split (default), 3 legacy
+    static const int mode_env = [] {  // PH0B_UNIQUE: 1 single pass, 2 split (default)
         const char* e = getenv("PH0B_UNIQUE");
         return e ? atoi(e) : 2;
     }();
     const uint64_t tiles = (a.count + kUT - 1) / kUT;
-    static_assert(kUT == kTileKeys, "the split and legacy kernels share the tiling");
+    static_assert(kUT == kTileKeys, "scratch sizing uses the same tiling");
     // scratch: counts (u32) | own (int2) | offsets (u64), unique_scratch_words(count) words
     uint32_t* counts = reinterpret_cast<uint32_t*>(a.scratch);
     int2* own = reinterpret_cast<int2*>(a.scratch + (tiles + 1) / 2 + 1);
     uint64_t* offsets = a.scratch + (tiles + 1) / 2 + 1 + tiles + 1;
-    if (mode_env == 3 && !a.d_base) {
-        const size_t smem = a.low_bits ? (size_t)(kTileKeys + kExt) * 8 : 0;
-        static bool configured = false;
-        if (!configured) {
-            cudaFuncSetAttribute(k3_count, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                 (kTileKeys + kExt) * 8);
-            configured = true;
-        }
-        k3_count<<<(unsigned)tiles, kThreads, smem, s>>>(a.keys, a.vals, a.count, a.kmin,
-                                                        a.low_bits, counts, own, a.redo);
-        k3_scan<<<1, 1024, 0, s>>>(counts, (uint32_t)tiles, offsets, a.n_scale, nullptr);
-        k3_write<kThreads><<<(unsigned)tiles, kThreads, 0, s>>>(a.keys, a.count, own, offsets,
-                                                               a.scale, a.grade);
-        return 3;
-    }
     const size_t smem = (size_t)2 * kUStage * 8;
     static int per_sm = 0;
     static int num_sms = 0;
