@@ -177,12 +177,32 @@ __global__ void __launch_bounds__(kUThreads, 3)
         } else if (low_bits) {
             // ---- fix the equal-prefix runs that start in this tile (stable, in smem) -----
             const uint64_t p_before = pre(k_before);
-            for (uint32_t i = tid; i < tn; i += kUThreads) {
+            // run starts, branch-free: each thread checks its kUItems positions of the
+            // warp-interleaved layout (consecutive lanes read consecutive keys: no bank
+            // conflicts, all loads in flight), then handles only the rare starts
+            uint32_t starts = 0;
+            {
+                const uint32_t wofs0 = warp * (32 * kUItems) + lane;
+#pragma unroll
+                for (int j = 0; j < kUItems; ++j) {
+                    const uint32_t i = wofs0 + 32 * j;
+                    const bool in = i < tn && i + 1 < staged;
+                    const uint64_t kc = in ? s_k[i] : 0ull;
+                    const uint64_t kn = in ? s_k[i + 1] : 0ull;
+                    const uint64_t kp = in && i > 0 ? s_k[i - 1] : 0ull;
+                    const uint64_t p = pre(kc);
+                    const bool has_prev = i > 0 || tile_start > 0;
+                    const uint64_t pp = i > 0 ? pre(kp) : p_before;
+                    const bool st = in && pre(kn) == p && !(has_prev && pp == p);
+                    starts |= st ? (1u << j) : 0u;
+                }
+            }
+            while (starts) {
+                const uint32_t j = (uint32_t)(__ffs(starts) - 1);
+                starts &= starts - 1;
+                const uint32_t i = warp * (32 * kUItems) + lane + 32 * j;
                 const uint64_t g = tile_start + i;
-                if (g + 1 >= count || i + 1 >= staged) continue;
                 const uint64_t p = pre(s_k[i]);
-                if (pre(s_k[i + 1]) != p) continue;
-                if (g > 0 && (i > 0 ? pre(s_k[i - 1]) : p_before) == p) continue;
                 uint32_t len = 2;
                 while (i + len < staged && len <= kMaxRun && pre(s_k[i + len]) == p) ++len;
                 if (len > kMaxRun || (i + len == staged && ext_end < count)) {
