@@ -81,6 +81,8 @@ typedef struct ph0b_stage_times {
     uint64_t columns_scanned; /* edge columns streamed by the reduction */
     float sort_passes_ms;     /* the radix passes alone (sort_ms minus the digit histogram) */
     uint32_t reserved0;
+    uint64_t d2h_bytes;       /* host-output calls: bytes actually moved device -> host
+                                 (D is shipped delta-encoded: ~4 B per distinct length) */
 } ph0b_stage_times;
 
 /* Host-side result of ph0b_h0_barcode; arrays are owned by the library. */

@@ -238,6 +238,8 @@ int ph0b_run_host(ph0b_context* ctx, const double* X, uint64_t n, uint64_t d, ui
     rc = copy_out(c, r, s, death_grade, death_length, scale, scale_capacity,
                   scale != nullptr && !overlap);
     if (rc) return rc;
+    r.times.d2h_bytes = (overlap ? r.times.d2h_bytes : (scale ? r.n_scale * 8 : 0)) +
+                        r.n_finite * 16;  // + the bars
     if (n_finite) *n_finite = r.n_finite;
     if (essential_count) *essential_count = r.essential;
     if (n_scale) *n_scale = r.n_scale;

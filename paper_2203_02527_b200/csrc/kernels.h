@@ -108,6 +108,11 @@ struct ReduceStats {
 int run_reduction(ReduceState& st, cudaStream_t s, int num_sms, uint32_t& epoch,
                   ReduceStats* stats);
 
+// ---- K9: compressed D for the host path (d2h_codec.cu) ----------------------------------
+constexpr int kD2HChunk = 4096;  // values per chunk: one u64 base + u32 deltas
+int launch_d2h_encode(const double* d, uint64_t n, uint32_t* deltas, uint64_t* bases,
+                      uint8_t* raw, cudaStream_t s);
+
 // ---- K8: on-device generate_uniform_cloud (generate.cu) --------------------------------
 // returns launches (>0), -1 on a CUDA error, -2 if more than 64 zero draws were met
 int launch_uniform_cloud(uint64_t n, uint64_t dim, uint64_t seed, double* d_out,

@@ -8,6 +8,7 @@
 #include <cstring>
 #include <map>
 #include <memory>
+#include <thread>
 #include <vector>
 
 #include "kernels.h"
@@ -78,6 +79,14 @@ struct Trace {
     }
 };
 
+bool d2h_compress() {
+    static const bool v = [] {
+        const char* e = getenv("PH0B_D2H_COMPRESS");
+        return !(e && e[0] == '0');
+    }();
+    return v;
+}
+
 uint64_t d2h_chunk_elems() {
     static const uint64_t v = [] {
         const char* e = getenv("PH0B_D2H_CHUNK_MB");
@@ -105,9 +114,15 @@ Context::~Context() {
     void* ps[] = {xin_,  xpad_, keys_[0], keys_[1], vals_[0], vals_[1], status_,
                   grade_, comp_, best_, surv_, surv_sorted_, lows_, cand_[0], cand_[1],
                   survkeys_[0], survkeys_[1], death_grade_, death_length_, hist_, counters_,
-                  small_, uscratch_, dbuf_, part_counts_, part_small_};
+                  small_, uscratch_, dbuf_, part_counts_, part_small_, d_delta_, d_cbase_,
+                  d_craw_};
     for (void* p : ps)
         if (p) cudaFree(p);
+    pool_.reset();
+    for (void* p : {(void*)h_delta_, (void*)h_cbase_, (void*)h_craw_})
+        if (p) cudaFreeHost(p);
+    for (auto& e : bucket_ev_)
+        if (e) cudaEventDestroy(e);
     if (h_small_) cudaFreeHost(h_small_);
     if (h_counters_) cudaFreeHost(h_counters_);
     if (h_mapped_) cudaFreeHost(h_mapped_);
@@ -147,6 +162,22 @@ Status Context::init() {
              "cudaHostGetDevicePointer");
     bytes_ += 8 * 256 * 4 + 64 * 4 + 64;
     atomic_rank_ok_ = sort_self_test(stream_);
+    return Status::ok();
+}
+
+Status Context::grow_host(void** p, uint64_t* cap, uint64_t need) {
+    if (need <= *cap) return Status::ok();
+    if (*p) cudaFreeHost(*p);
+    *p = nullptr;
+    *cap = 0;
+    need = (need + 4095) & ~4095ull;
+    const cudaError_t e = cudaHostAlloc(p, need, cudaHostAllocDefault);
+    if (e != cudaSuccess) {
+        cudaGetLastError();
+        return {PH0B_ERR_OUT_OF_MEMORY, "pinned host allocation of " + std::to_string(need) +
+                                            " bytes failed (" + cudaGetErrorString(e) + ")"};
+    }
+    *cap = need;
     return Status::ok();
 }
 
@@ -548,6 +579,28 @@ Status Context::run_host_overlapped(const double* X, uint64_t n, uint64_t d, uin
         return s;
     if (!copy_stream_) PH0B_TRY(cudaStreamCreateWithFlags(&copy_stream_, cudaStreamNonBlocking),
                                 "cudaStreamCreate");
+    const bool compress = host_scale && d2h_compress();
+    if (compress) {
+        const uint64_t chunks = k / kD2HChunk + 64;
+        if (!(s = grow(reinterpret_cast<void**>(&d_delta_), &d_delta_cap_, k * 4 + 64)).good() ||
+            !(s = grow(reinterpret_cast<void**>(&d_cbase_), &d_cbase_cap_, chunks * 8)).good() ||
+            !(s = grow(reinterpret_cast<void**>(&d_craw_), &d_craw_cap_, chunks)).good() ||
+            !(s = grow_host(reinterpret_cast<void**>(&h_delta_), &h_delta_cap_, k * 4 + 64)).good() ||
+            !(s = grow_host(reinterpret_cast<void**>(&h_cbase_), &h_cbase_cap_, chunks * 8)).good() ||
+            !(s = grow_host(reinterpret_cast<void**>(&h_craw_), &h_craw_cap_, chunks)).good())
+            return s;
+        if (!pool_) {
+            const unsigned hw = std::thread::hardware_concurrency();
+            pool_ = std::make_unique<DecodePool>(hw > 2 ? hw - 1 : 1);
+        }
+    }
+    // whatever the exit path, no decode task may still be writing the caller's buffer
+    struct PoolGuard {
+        DecodePool* p;
+        ~PoolGuard() {
+            if (p) p->wait();
+        }
+    } pool_guard{compress ? pool_.get() : nullptr};
     uint64_t* d_spl = part_small_;           // [256]
     uint64_t* d_tot = part_small_ + 256;     // [512]: totals | segment starts
     uint64_t* d_mm = part_small_ + 768;      // [512]: key bounds
@@ -599,11 +652,84 @@ Status Context::run_host_overlapped(const double* X, uint64_t n, uint64_t d, uin
     // D slice [host_base, d_base[b+1]) of a finished bucket -> host, in medium chunks (several
     // medium copies sustain a higher PCIe rate than one large one: 55 vs 52 GB/s for 17 GB,
     // tools/d2h_big.py)
+    // compressed variant: the encoder turns the slice into a u64 base + u32 deltas per
+    // 4096-value chunk (half the PCIe bytes), the copy engine ships that, and the host pool
+    // decodes each bucket as soon as its copy has landed (drain)
+    struct Pending {
+        uint32_t b;
+        uint64_t lo, n, cb, nch;
+    };
+    std::vector<Pending> pending;
+    uint64_t chunk_base = 0;
+    uint64_t d2h_total = 0;  // bytes moved device -> host by this call
+    if (compress && bucket_ev_.size() < B) {
+        bucket_ev_.resize(B, nullptr);
+        for (auto& e : bucket_ev_)
+            if (!e) PH0B_TRY(cudaEventCreateWithFlags(&e, cudaEventDisableTiming), "event");
+    }
+    auto drain = [&](bool wait) -> Status {
+        while (!pending.empty()) {
+            const Pending p = pending.front();
+            if (!wait && cudaEventQuery(bucket_ev_[p.b]) == cudaErrorNotReady) {
+                cudaGetLastError();
+                break;
+            }
+            PH0B_TRY(cudaEventSynchronize(bucket_ev_[p.b]), "D2H bucket");
+            for (uint64_t j = 0; j < p.nch; ++j) {  // a delta did not fit in 32 bits: raw
+                if (!h_craw_[p.cb + j]) continue;
+                const uint64_t s0 = p.lo + j * kD2HChunk;
+                const uint64_t len = std::min<uint64_t>(kD2HChunk, p.lo + p.n - s0);
+                PH0B_TRY(cudaMemcpyAsync(host_scale + s0, dbuf_ + s0, len * 8,
+                                         cudaMemcpyDeviceToHost, copy_stream_), "D2H raw");
+                d2h_total += len * 8;
+            }
+            std::vector<DecodeTask> tasks;
+            constexpr uint64_t kGroup = 64;  // chunks per decode task (256 Ki values)
+            for (uint64_t j0 = 0; j0 < p.nch; j0 += kGroup) {
+                const uint64_t s0 = p.lo + j0 * kD2HChunk;
+                const uint64_t n = std::min<uint64_t>(kGroup * kD2HChunk, p.lo + p.n - s0);
+                tasks.push_back({h_delta_ + s0, h_cbase_ + p.cb + j0, h_craw_ + p.cb + j0,
+                                 reinterpret_cast<uint64_t*>(host_scale + s0), n,
+                                 (uint32_t)kD2HChunk});
+            }
+            pool_->submit(tasks);
+            pending.erase(pending.begin());
+        }
+        return Status::ok();
+    };
     auto ship = [&](uint32_t b) -> Status {
         PH0B_TRY(cudaEventRecord(ev_[6], st), "event");
         PH0B_TRY(cudaEventSynchronize(ev_[6]), "bucket");
         tr.mark("bucket sorted", (long)b);
         const uint64_t next_base = h_base[b + 1];
+        if (compress && next_base > host_base) {
+            if (next_base > scale_capacity)
+                return {PH0B_ERR_CAPACITY, "scale buffer too small: need >= " +
+                                               std::to_string(next_base) + " entries"};
+            const uint64_t n = next_base - host_base;
+            const uint64_t nch = (n + kD2HChunk - 1) / kD2HChunk;
+            launches += launch_d2h_encode(dbuf_ + host_base, n, d_delta_ + host_base,
+                                          d_cbase_ + chunk_base, d_craw_ + chunk_base, st);
+            PH0B_CHECK_LAUNCH("D2H encode");
+            PH0B_TRY(cudaEventRecord(ev_[6], st), "event");
+            PH0B_TRY(cudaStreamWaitEvent(copy_stream_, ev_[6], 0), "wait");
+            for (uint64_t q = 0; q < n; q += 2 * d2h_chunk_elems()) {
+                const uint64_t e = std::min<uint64_t>(n, q + 2 * d2h_chunk_elems());
+                PH0B_TRY(cudaMemcpyAsync(h_delta_ + host_base + q, d_delta_ + host_base + q,
+                                         (e - q) * 4, cudaMemcpyDeviceToHost, copy_stream_),
+                         "D2H deltas");
+            }
+            PH0B_TRY(cudaMemcpyAsync(h_cbase_ + chunk_base, d_cbase_ + chunk_base, nch * 8,
+                                     cudaMemcpyDeviceToHost, copy_stream_), "D2H bases");
+            PH0B_TRY(cudaMemcpyAsync(h_craw_ + chunk_base, d_craw_ + chunk_base, nch,
+                                     cudaMemcpyDeviceToHost, copy_stream_), "D2H flags");
+            PH0B_TRY(cudaEventRecord(bucket_ev_[b], copy_stream_), "event");
+            d2h_total += n * 4 + nch * 9;
+            pending.push_back({b, host_base, n, chunk_base, nch});
+            chunk_base += nch;
+            host_base = next_base;
+            return drain(false);
+        }
         if (host_scale && next_base > host_base) {
             if (next_base > scale_capacity)
                 return {PH0B_ERR_CAPACITY, "scale buffer too small: need >= " +
@@ -614,6 +740,7 @@ Status Context::run_host_overlapped(const double* X, uint64_t n, uint64_t d, uin
                 PH0B_TRY(cudaMemcpyAsync(host_scale + q, dbuf_ + q, (e - q) * 8,
                                          cudaMemcpyDeviceToHost, copy_stream_), "D2H scale");
             }
+            d2h_total += (next_base - host_base) * 8;
         }
         host_base = next_base;
         return Status::ok();
@@ -707,8 +834,14 @@ Status Context::run_host_overlapped(const double* X, uint64_t n, uint64_t d, uin
     PH0B_TRY(cudaEventRecord(ev_[5], st), "event");
     PH0B_TRY(cudaStreamSynchronize(st), "pipeline");
     tr.mark("reduce+collect done");
+    if (compress) {
+        if (!(s = drain(true)).good()) return s;
+        pool_->wait();
+        tr.mark("decode done");
+    }
     PH0B_TRY(cudaStreamSynchronize(copy_stream_), "D2H scale");
     tr.mark("D2H done");
+    r.times.d2h_bytes = d2h_total;
     r.n_scale = host_base;
     r.d_uv_sorted = vals_[cur_];
     r.d_scale = dbuf_;

@@ -4,10 +4,13 @@
 #include <cuda_runtime.h>
 
 #include <cstdint>
+#include <memory>
 #include <mutex>
 #include <string>
+#include <vector>
 
 #include "../../include/ph0b.h"
+#include "host_decode.h"
 #include "kernels.h"
 
 namespace ph0b {
@@ -133,6 +136,16 @@ private:
     double* death_length_ = nullptr;  uint64_t death_length_cap_ = 0;
     uint64_t* uscratch_ = nullptr; uint64_t uscratch_cap_ = 0;
     double* dbuf_ = nullptr;       uint64_t dbuf_cap_ = 0;        // D (overlapped host path)
+    // compressed D for the host path: device deltas/chunk bases/raw flags, pinned mirrors
+    uint32_t* d_delta_ = nullptr;  uint64_t d_delta_cap_ = 0;
+    uint64_t* d_cbase_ = nullptr;  uint64_t d_cbase_cap_ = 0;
+    uint8_t* d_craw_ = nullptr;    uint64_t d_craw_cap_ = 0;
+    uint32_t* h_delta_ = nullptr;  uint64_t h_delta_cap_ = 0;
+    uint64_t* h_cbase_ = nullptr;  uint64_t h_cbase_cap_ = 0;
+    uint8_t* h_craw_ = nullptr;    uint64_t h_craw_cap_ = 0;
+    std::unique_ptr<DecodePool> pool_;
+    std::vector<cudaEvent_t> bucket_ev_;
+    Status grow_host(void** p, uint64_t* cap, uint64_t need);
     uint32_t* part_counts_ = nullptr; uint64_t part_counts_cap_ = 0;
     uint64_t* part_small_ = nullptr;  uint64_t part_small_cap_ = 0;
     cudaStream_t copy_stream_ = nullptr;

@@ -60,7 +60,7 @@ class StageTimes(C.Structure):
                 ("reduce_ms", C.c_float), ("collect_ms", C.c_float), ("total_ms", C.c_float),
                 ("sort_passes", C.c_uint32), ("reduce_rounds", C.c_uint32),
                 ("columns_scanned", C.c_uint64), ("sort_passes_ms", C.c_float),
-                ("reserved0", C.c_uint32)]
+                ("reserved0", C.c_uint32), ("d2h_bytes", C.c_uint64)]
 
     def as_dict(self):
         return {f: getattr(self, f) for f, _ in self._fields_}
