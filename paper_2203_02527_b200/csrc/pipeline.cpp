@@ -87,6 +87,14 @@ bool d2h_compress() {
     return v;
 }
 
+uint32_t d2h_raw_every() {
+    static const uint32_t v = [] {
+        const char* e = getenv("PH0B_D2H_RAW_EVERY");
+        return e ? (uint32_t)atoi(e) : 0u;
+    }();
+    return v;
+}
+
 uint64_t d2h_chunk_elems() {
     static const uint64_t v = [] {
         const char* e = getenv("PH0B_D2H_CHUNK_MB");
@@ -590,8 +598,13 @@ Status Context::run_host_overlapped(const double* X, uint64_t n, uint64_t d, uin
             !(s = grow_host(reinterpret_cast<void**>(&h_craw_), &h_craw_cap_, chunks)).good())
             return s;
         if (!pool_) {
+            static const int env_threads = [] {
+                const char* e = getenv("PH0B_DECODE_THREADS");
+                return e ? atoi(e) : 0;
+            }();
             const unsigned hw = std::thread::hardware_concurrency();
-            pool_ = std::make_unique<DecodePool>(hw > 2 ? hw - 1 : 1);
+            pool_ = std::make_unique<DecodePool>(
+                env_threads > 0 ? (unsigned)env_threads : (hw > 2 ? hw - 1 : 1));
         }
     }
     // whatever the exit path, no decode task may still be writing the caller's buffer
@@ -702,7 +715,10 @@ Status Context::run_host_overlapped(const double* X, uint64_t n, uint64_t d, uin
         PH0B_TRY(cudaEventSynchronize(ev_[6]), "bucket");
         tr.mark("bucket sorted", (long)b);
         const uint64_t next_base = h_base[b + 1];
-        if (compress && next_base > host_base) {
+        // PH0B_D2H_RAW_EVERY=k ships every k-th bucket raw (0, the measured best: none)
+        const bool this_compressed =
+            compress && !(d2h_raw_every() && b % d2h_raw_every() == d2h_raw_every() - 1);
+        if (this_compressed && next_base > host_base) {
             if (next_base > scale_capacity)
                 return {PH0B_ERR_CAPACITY, "scale buffer too small: need >= " +
                                                std::to_string(next_base) + " entries"};
