@@ -2,6 +2,9 @@
 #include "host_decode.h"
 
 #include <immintrin.h>
+#include <sys/resource.h>
+#include <sys/syscall.h>
+#include <unistd.h>
 
 #include <algorithm>
 
@@ -99,6 +102,8 @@ void DecodePool::wait() {
 }
 
 void DecodePool::run() {
+    // below the orchestrating thread: the GPU's next launches must not wait for a core
+    setpriority(PRIO_PROCESS, (id_t)syscall(SYS_gettid), 5);
     for (;;) {
         DecodeTask t;
         {
