@@ -220,6 +220,13 @@ uint64_t ph0b_last_launch_count(void);
 int ph0b_generate_uniform_cloud_device(ph0b_context* ctx, uint64_t n, uint64_t dim,
                                        uint64_t seed, double* d_out, void* stream);
 
+/* Host-side decoder of the delta-encoded D stream the host-output path uses over PCIe
+ * (d2h_codec.cu): chunks of `chunk` values, chunk j = bases[j] followed by 32-bit deltas
+ * (deltas[j*chunk] unused); chunks with raw[j] != 0 are skipped (shipped uncompressed).
+ * Writes out[0..n).  Exposed for callers that move D between processes the same way. */
+int ph0b_decode_deltas(const uint32_t* deltas, const uint64_t* bases, const uint8_t* raw,
+                       uint64_t n, uint32_t chunk, uint64_t* out);
+
 int ph0b_generate_cloud(uint32_t kind, uint64_t n, uint64_t d, uint64_t seed, uint32_t clusters,
                         double sigma, double lo, double hi, uint64_t n_background,
                         double* out_colmajor);

@@ -9,6 +9,7 @@
 #include <vector>
 
 #include "../../include/ph0b.h"
+#include "host_decode.h"
 #include "pipeline.h"
 
 using ph0b::Context;
@@ -211,6 +212,15 @@ int ph0b_generate_uniform_cloud_device(ph0b_context* ctx, uint64_t n, uint64_t d
     g_last_launches = l > 0 ? (uint64_t)l : 0;
     if (l == -2) return fail(PH0B_ERR_INVALID_ARGUMENT, "more than 64 zero draws (impossible in practice)");
     if (l < 0 || cudaGetLastError() != cudaSuccess) return fail(PH0B_ERR_CUDA, "generator kernel");
+    return PH0B_OK;
+}
+
+int ph0b_decode_deltas(const uint32_t* deltas, const uint64_t* bases, const uint8_t* raw,
+                       uint64_t n, uint32_t chunk, uint64_t* out) {
+    if (n == 0) return PH0B_OK;
+    if (!deltas || !bases || !raw || !out || chunk == 0)
+        return fail(PH0B_ERR_INVALID_ARGUMENT, "null argument or zero chunk");
+    ph0b::decode_chunk(ph0b::DecodeTask{deltas, bases, raw, out, n, chunk});
     return PH0B_OK;
 }
 

@@ -36,6 +36,7 @@ EXPORTED_SYMBOLS = [
     "ph0b_last_launch_count", "ph0b_generate_cloud", "ph0b_shard_distances", "ph0b_shard_sample",
     "ph0b_shard_partition", "ph0b_shard_recv", "ph0b_shard_sort_unique", "ph0b_shard_reduce",
     "ph0b_reduce_columns", "ph0b_kruskal_barcode", "ph0b_generate_uniform_cloud_device",
+    "ph0b_decode_deltas",
 ]
 
 
@@ -95,6 +96,7 @@ def lib() -> C.CDLL:
         "ph0b_kruskal_barcode": (C.c_int, [vp, u64, u64, u32, C.POINTER(Options),
                                            C.POINTER(Result)]),
         "ph0b_generate_uniform_cloud_device": (C.c_int, [vp, u64, u64, u64, vp, vp]),
+        "ph0b_decode_deltas": (C.c_int, [vp, vp, vp, u64, u32, vp]),
         "ph0b_h0_barcode_into": (C.c_int, [vp, u64, u64, u32, C.POINTER(Options), vp, vp, u64p,
                                            u64p, vp, u64, u64p, C.POINTER(StageTimes)]),
         "ph0b_pairwise_distances": (C.c_int, [vp, u64, u64, u32, C.POINTER(Options), vp]),

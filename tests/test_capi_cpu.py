@@ -64,3 +64,36 @@ def test_config_clouds_deterministic():
         assert np.array_equal(a, b) and np.isfinite(a).all()
     C5 = pkg.config_cloud("C5", 1000)
     assert C5.shape == (1000, 8)
+
+
+def test_host_delta_decoder_roundtrip():
+    """The host half of the compressed D2H (ph0b_decode_deltas): chunked u64 bases + u32
+    deltas decode back to the exact bit patterns, at any output alignment, skipping raw
+    chunks (which the host path ships uncompressed)."""
+    import ctypes as C
+    rng = np.random.default_rng(7)
+    L = pkg.lib()
+    for n, chunk, off in ((1, 4096, 0), (5000, 4096, 1), (20000, 1024, 3), (4096 * 3, 4096, 0),
+                          (777, 256, 2)):
+        gaps = rng.integers(1, 1 << 31, size=n, dtype=np.uint64)
+        seq = np.cumsum(gaps, dtype=np.uint64) + np.uint64(0x3F00000000000000)
+        nch = (n + chunk - 1) // chunk
+        bases = seq[::chunk].copy()
+        deltas = np.zeros(n, np.uint32)
+        deltas[1:] = (seq[1:] - seq[:-1]).astype(np.uint32)
+        raw = np.zeros(nch, np.uint8)
+        if nch > 1:
+            raw[1] = 1  # a raw chunk: the decoder must leave it alone
+        buf = np.full(n + 8, 0xDEADBEEF, np.uint64)
+        out = buf[off:off + n]
+        rc = L.ph0b_decode_deltas(C.c_void_p(deltas.ctypes.data), C.c_void_p(bases.ctypes.data),
+                                  C.c_void_p(raw.ctypes.data), n, chunk,
+                                  C.c_void_p(out.ctypes.data))
+        assert rc == 0
+        for j in range(nch):
+            s, e = j * chunk, min(n, (j + 1) * chunk)
+            if raw[j]:
+                assert np.all(out[s:e] == 0xDEADBEEF)
+            else:
+                assert np.array_equal(out[s:e], seq[s:e]), (n, chunk, off, j)
+        assert np.all(buf[:off] == 0xDEADBEEF) and np.all(buf[off + n:] == 0xDEADBEEF)
