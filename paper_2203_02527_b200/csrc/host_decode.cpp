@@ -7,6 +7,8 @@
 #include <unistd.h>
 
 #include <algorithm>
+#include <atomic>
+#include <chrono>
 
 namespace ph0b {
 
@@ -49,6 +51,40 @@ __attribute__((target("avx2"))) void decode_avx2(const Chunk& t) {
     _mm_sfence();
 }
 
+// 8 values per step: widen 8 deltas to u64, in-register prefix sum (3 lane shifts), add the
+// running value, one 64-byte non-temporal store.
+__attribute__((target("avx512f"))) void decode_avx512(const Chunk& t) {
+    uint64_t acc = t.base;
+    uint64_t* out = t.out;
+    const uint32_t* d = t.deltas;
+    out[0] = acc;
+    uint32_t i = 1;
+    while (i < t.len && (reinterpret_cast<uintptr_t>(out + i) & 63u)) {
+        acc += d[i];
+        out[i++] = acc;
+    }
+    if (i + 8 <= t.len) {
+        const __m512i z = _mm512_setzero_si512();
+        const __m512i last = _mm512_set1_epi64(7);
+        __m512i run = _mm512_set1_epi64((long long)acc);
+        for (; i + 8 <= t.len; i += 8) {
+            __m512i x = _mm512_cvtepu32_epi64(_mm256_loadu_si256(reinterpret_cast<const __m256i*>(d + i)));
+            x = _mm512_add_epi64(x, _mm512_alignr_epi64(x, z, 7));
+            x = _mm512_add_epi64(x, _mm512_alignr_epi64(x, z, 6));
+            x = _mm512_add_epi64(x, _mm512_alignr_epi64(x, z, 4));
+            x = _mm512_add_epi64(x, run);
+            run = _mm512_permutexvar_epi64(last, x);
+            _mm512_stream_si512(reinterpret_cast<__m512i*>(out + i), x);
+        }
+        acc = (uint64_t)_mm_cvtsi128_si64(_mm512_castsi512_si128(run));
+    }
+    for (; i < t.len; ++i) {
+        acc += d[i];
+        out[i] = acc;
+    }
+    _mm_sfence();
+}
+
 void decode_scalar(const Chunk& t) {
     uint64_t acc = t.base;
     t.out[0] = acc;
@@ -61,16 +97,75 @@ void decode_scalar(const Chunk& t) {
 }  // namespace
 
 void decode_chunk(const DecodeTask& t) {
-    static const bool avx2 = __builtin_cpu_supports("avx2");
+    static const int isa = __builtin_cpu_supports("avx512f") ? 2 : __builtin_cpu_supports("avx2") ? 1 : 0;
     for (uint64_t j = 0, s0 = 0; s0 < t.n; ++j, s0 += t.chunk) {
         if (t.raw[j]) continue;
         const Chunk c{t.deltas + s0, t.bases[j], t.out + s0,
                       (uint32_t)(t.n - s0 < t.chunk ? t.n - s0 : t.chunk)};
-        if (avx2)
+        if (isa == 2)
+            decode_avx512(c);
+        else if (isa == 1)
             decode_avx2(c);
         else
             decode_scalar(c);
     }
+}
+
+std::atomic<uint64_t> g_wait_ns{0}, g_decode_ns{0}, g_pieces{0};
+
+void decode_stats(uint64_t* wait_ns, uint64_t* decode_ns, uint64_t* pieces, bool reset) {
+    *wait_ns = g_wait_ns.load();
+    *decode_ns = g_decode_ns.load();
+    *pieces = g_pieces.load();
+    if (reset) {
+        g_wait_ns = 0;
+        g_decode_ns = 0;
+        g_pieces = 0;
+    }
+}
+
+void decode_piece(const DecodeTask& t) {
+    const auto t0 = std::chrono::steady_clock::now();
+    // the copy engine flags the slot after the piece (and, earlier in the same stream, the
+    // bucket's chunk bases and raw flags) has landed
+    std::chrono::steady_clock::time_point deadline{};
+    for (uint32_t spins = 0; __atomic_load_n(t.ready, __ATOMIC_ACQUIRE) != t.gen; ++spins) {
+        if (spins < 4096) {
+            _mm_pause();
+            continue;
+        }
+        std::this_thread::yield();
+        if ((spins & 1023u) != 0) continue;
+        const auto now = std::chrono::steady_clock::now();
+        if (spins == 4096) {
+            deadline = now + std::chrono::seconds(60);
+        } else if (now > deadline) {  // the copy stream is dead (device fault): give up
+            *t.overflow = 2;
+            if (t.done->fetch_add(1) + 1 == (uint64_t)t.gen * t.nsub)
+                __atomic_store_n(t.freed, t.gen, __ATOMIC_RELEASE);
+            return;
+        }
+    }
+    const auto t1 = std::chrono::steady_clock::now();
+    const uint64_t lo = t.bounds[0], hi = t.bounds[1];
+    const uint64_t nb = hi > lo ? hi - lo : 0;
+    if (t.v0 < nb) {
+        const uint64_t v1 = t.v0 + t.n < nb ? t.v0 + t.n : nb;
+        if (lo + v1 > t.capacity) {
+            *t.overflow = 1;
+        } else {
+            DecodeTask c = t;
+            c.out = t.out + lo + t.v0;
+            c.n = v1 - t.v0;
+            decode_chunk(c);
+        }
+    }
+    if (t.done->fetch_add(1, std::memory_order_acq_rel) + 1 == (uint64_t)t.gen * t.nsub)
+        __atomic_store_n(t.freed, t.gen, __ATOMIC_RELEASE);
+    const auto t2 = std::chrono::steady_clock::now();
+    g_wait_ns += std::chrono::duration_cast<std::chrono::nanoseconds>(t1 - t0).count();
+    g_decode_ns += std::chrono::duration_cast<std::chrono::nanoseconds>(t2 - t1).count();
+    ++g_pieces;
 }
 
 DecodePool::DecodePool(unsigned threads) {
@@ -113,7 +208,10 @@ void DecodePool::run() {
             t = queue_.front();
             queue_.pop_front();
         }
-        decode_chunk(t);
+        if (t.ready)
+            decode_piece(t);
+        else
+            decode_chunk(t);
         {
             std::lock_guard<std::mutex> lk(mu_);
             if (--pending_ == 0) done_cv_.notify_all();

@@ -3,6 +3,7 @@
 // with non-temporal stores.  Internal header.
 #pragma once
 
+#include <atomic>
 #include <condition_variable>
 #include <cstdint>
 #include <deque>
@@ -14,13 +15,32 @@ namespace ph0b {
 
 // A run of consecutive chunks of one bucket: chunk j covers values [j*chunk, ...) of
 // deltas/out; raw chunks (shipped uncompressed) are skipped.
+//
+// Streamed pieces (`ready` set): the deltas sit in a slot of the pinned staging ring, which
+// the copy engine fills and then flags by writing `gen` into *ready (a stream memory
+// operation after the copy).  The worker spins until *ready == gen, decodes, and hands the
+// slot back with *freed = gen (the copy engine's next fill of that slot waits for it).  The
+// value range is only known on the device when the piece is enqueued: it is resolved from
+// the bucket's published D bounds (`bounds[0..1]`, mapped host words) at decode time as
+// values [v0, min(v0 + n, hi - lo)) of the bucket, written to out_base + lo + v0.
 struct DecodeTask {
     const uint32_t* deltas;  // [n] (each chunk's first entry unused)
     const uint64_t* bases;   // [nchunks] pattern of each chunk's first value
     const uint8_t* raw;      // [nchunks] 1 = chunk shipped raw
-    uint64_t* out;           // [n]
-    uint64_t n;              // values covered
+    uint64_t* out;           // [n] (streamed pieces: out_base)
+    uint64_t n;              // values covered (streamed pieces: upper bound)
     uint32_t chunk;          // values per chunk
+    const volatile uint32_t* ready = nullptr;
+    volatile uint32_t* freed = nullptr;
+    uint32_t gen = 0;
+    const volatile uint64_t* bounds = nullptr;
+    uint64_t v0 = 0;
+    uint64_t capacity = 0;   // entries of out_base
+    volatile int* overflow = nullptr;  // set when lo + v1 > capacity (nothing written)
+    // a piece is decoded by `nsub` tasks (sub-ranges of its chunks); the slot's monotone
+    // completion counter reaches gen * nsub when the last one finishes, which frees the slot
+    std::atomic<uint64_t>* done = nullptr;
+    uint32_t nsub = 1;
 };
 
 class DecodePool {
@@ -42,5 +62,9 @@ private:
 };
 
 void decode_chunk(const DecodeTask& t);
+// A streamed piece: wait for its slot, decode the resolved range, release the slot.
+void decode_piece(const DecodeTask& t);
+// diagnostics (PH0B_TRACE): summed wait-for-slot and decode times of streamed pieces
+void decode_stats(uint64_t* wait_ns, uint64_t* decode_ns, uint64_t* pieces, bool reset);
 
 }  // namespace ph0b

@@ -110,6 +110,9 @@ int run_reduction(ReduceState& st, cudaStream_t s, int num_sms, uint32_t& epoch,
 
 // ---- K9: compressed D for the host path (d2h_codec.cu) ----------------------------------
 constexpr int kD2HChunk = 4096;  // values per chunk: one u64 base + u32 deltas
+// Same, for the slice [lohi[0], lohi[1]) of d given by device words; n_upper >= its length.
+int launch_d2h_encode_bucket(const double* d, const uint64_t* lohi, uint64_t n_upper,
+                             uint32_t* deltas, uint64_t* bases, uint8_t* raw, cudaStream_t s);
 int launch_d2h_encode(const double* d, uint64_t n, uint32_t* deltas, uint64_t* bases,
                       uint8_t* raw, cudaStream_t s);
 

@@ -2,6 +2,8 @@
 // proj/src/bench.cpp:45-59 (distances -> filtration -> matrix -> reduce -> barcode).
 #include "pipeline.h"
 
+#include <cuda.h>
+
 #include <algorithm>
 #include <chrono>
 #include <cstdio>
@@ -104,6 +106,66 @@ uint64_t d2h_chunk_elems() {
     return v;
 }
 
+// Streamed D2H ring of the compressed host path: PH0B_RING_SLOTS slots (default 6) of
+// PH0B_RING_CHUNKS 4096-value chunks (u32 deltas: 8 MiB at the default 512), filled on
+// PH0B_RING_STREAMS copy streams (default 2) and decoded by PH0B_RING_SUBTASKS pool tasks
+// per piece (default 32).  8 MiB copies keep the per-copy and stream-memop overheads below
+// 5 % of the PCIe time (tools/ring_bench.cu); the 48 MiB ring replaces a k*4-byte pinned
+// staging buffer (8.6 GB at C5).  Measured sweep: tools/ring_sweep.sh, DESIGN.md.
+uint32_t ring_piece_chunks() {
+    static const uint32_t v = [] {
+        const char* e = getenv("PH0B_RING_CHUNKS");
+        const int x = e ? atoi(e) : 512;
+        return (uint32_t)(x < 1 ? 1 : (x > 4096 ? 4096 : x));
+    }();
+    return v;
+}
+
+uint32_t ring_subtasks() {
+    static const uint32_t v = [] {
+        const char* e = getenv("PH0B_RING_SUBTASKS");
+        const int x = e ? atoi(e) : 32;
+        return (uint32_t)(x < 1 ? 1 : (x > 256 ? 256 : x));
+    }();
+    return v;
+}
+
+uint32_t ring_slots() {
+    static const uint32_t v = [] {
+        const char* e = getenv("PH0B_RING_SLOTS");
+        const int x = e ? atoi(e) : 6;
+        return (uint32_t)(x < 2 ? 2 : (x > 256 ? 256 : x));
+    }();
+    return v;
+}
+
+// Stream memory operations (driver API, resolved through the runtime): the copy stream
+// waits for a slot to be released by the host decoder, and flags a slot as filled, without
+// any CUDA call from the decoder threads.
+using StreamValueFn = CUresult (*)(CUstream, CUdeviceptr, cuuint32_t, unsigned int);
+StreamValueFn stream_fn(const char* name) {
+    void* fn = nullptr;
+    cudaDriverEntryPointQueryResult q{};
+    if (cudaGetDriverEntryPoint(name, &fn, cudaEnableDefault, &q) != cudaSuccess ||
+        q != cudaDriverEntryPointSuccess) {
+        cudaGetLastError();
+        return nullptr;
+    }
+    return reinterpret_cast<StreamValueFn>(fn);
+}
+
+bool stream_wait_u32(cudaStream_t s, uint64_t dptr, uint32_t value) {
+    static const StreamValueFn fn = stream_fn("cuStreamWaitValue32");
+    return fn && fn(reinterpret_cast<CUstream>(s), (CUdeviceptr)dptr, value,
+                    CU_STREAM_WAIT_VALUE_EQ) == CUDA_SUCCESS;
+}
+
+bool stream_write_u32(cudaStream_t s, uint64_t dptr, uint32_t value) {
+    static const StreamValueFn fn = stream_fn("cuStreamWriteValue32");
+    return fn && fn(reinterpret_cast<CUstream>(s), (CUdeviceptr)dptr, value,
+                    CU_STREAM_WRITE_VALUE_DEFAULT) == CUDA_SUCCESS;
+}
+
 uint32_t max_sort_passes() {
     static const uint32_t v = [] {
         const char* e = getenv("PH0B_MAX_PASSES");
@@ -127,13 +189,15 @@ Context::~Context() {
     for (void* p : ps)
         if (p) cudaFree(p);
     pool_.reset();
-    for (void* p : {(void*)h_delta_, (void*)h_cbase_, (void*)h_craw_})
+    for (void* p : {(void*)h_ring_, (void*)h_ringflags_, (void*)h_cbase_, (void*)h_craw_})
         if (p) cudaFreeHost(p);
+    if (enc_ev_) cudaEventDestroy(enc_ev_);
     for (auto& e : bucket_ev_)
         if (e) cudaEventDestroy(e);
     if (h_small_) cudaFreeHost(h_small_);
     if (h_counters_) cudaFreeHost(h_counters_);
     if (h_mapped_) cudaFreeHost(h_mapped_);
+    for (size_t i = 1; i < ring_streams_.size(); ++i) cudaStreamDestroy(ring_streams_[i]);
     if (copy_stream_) cudaStreamDestroy(copy_stream_);
     for (auto& e : ev_)
         if (e) cudaEventDestroy(e);
@@ -170,6 +234,21 @@ Status Context::init() {
              "cudaHostGetDevicePointer");
     bytes_ += 8 * 256 * 4 + 64 * 4 + 64;
     atomic_rank_ok_ = sort_self_test(stream_);
+    return Status::ok();
+}
+
+Status Context::ensure_ring() {
+    const uint64_t need = (uint64_t)ring_slots() * ring_piece_chunks() * kD2HChunk * 4;
+    Status s = grow_host(reinterpret_cast<void**>(&h_ring_), &h_ring_cap_, need);
+    if (!s.good()) return s;
+    if (!h_ringflags_) {
+        // [0, 256) ready, [256, 512) freed; slot generations start at 1, so 0 = never used
+        PH0B_TRY(cudaHostAlloc(&h_ringflags_, 512 * 4, cudaHostAllocMapped), "cudaHostAlloc mapped");
+        std::memset(h_ringflags_, 0, 512 * 4);
+        PH0B_TRY(cudaHostGetDevicePointer(reinterpret_cast<void**>(&d_ringflags_), h_ringflags_, 0),
+                 "cudaHostGetDevicePointer");
+        ring_seq_ = 0;
+    }
     return Status::ok();
 }
 
@@ -362,7 +441,7 @@ Status Context::sort_unique_range(uint64_t* kb0, uint32_t* vb0, uint64_t* kb1, u
                                   uint64_t k, uint64_t kmin, uint64_t kmax, bool raw_hist,
                                   double* scale_out, const uint64_t* d_base, uint64_t* d_count,
                                   uint32_t* grade_out, cudaStream_t st, int* res,
-                                  uint32_t* passes) {
+                                  uint32_t* passes, const std::function<Status()>* after_enqueue) {
     uint64_t* kb[2] = {kb0, kb1};
     uint32_t* vb[2] = {vb0, vb1};
     int src = 0;
@@ -372,7 +451,7 @@ Status Context::sort_unique_range(uint64_t* kb0, uint32_t* vb0, uint64_t* kb1, u
             PH0B_TRY(cudaMemcpyAsync(d_count, d_base, 8, cudaMemcpyDeviceToDevice, st), "copy");
         else
             PH0B_TRY(cudaMemsetAsync(d_count, 0, 8, st), "memset");
-        return Status::ok();
+        return after_enqueue ? (*after_enqueue)() : Status::ok();
     }
     for (int attempt = 0;; ++attempt) {
         SortPlan plan{};
@@ -420,6 +499,10 @@ Status Context::sort_unique_range(uint64_t* kb0, uint32_t* vb0, uint64_t* kb1, u
                       counters_ + 40, d_count, next_epochs(1, st), redo, uscratch_, d_base};
         launches += launch_unique(ua, st);
         PH0B_CHECK_LAUNCH("unique kernel");
+        if (attempt == 0 && after_enqueue) {  // host work that overlaps this range's kernels
+            const Status hs = (*after_enqueue)();
+            if (!hs.good()) return hs;
+        }
         if (low_bits == 0) break;
         PH0B_TRY(cudaEventRecord(ev_[7], st), "event");
         PH0B_TRY(cudaEventSynchronize(ev_[7]), "unique");
@@ -589,14 +672,35 @@ Status Context::run_host_overlapped(const double* X, uint64_t n, uint64_t d, uin
                                 "cudaStreamCreate");
     const bool compress = host_scale && d2h_compress();
     if (compress) {
-        const uint64_t chunks = k / kD2HChunk + 64;
-        if (!(s = grow(reinterpret_cast<void**>(&d_delta_), &d_delta_cap_, k * 4 + 64)).good() ||
+        // per bucket, a chunk-aligned area sized by its edge count (>= its |D|)
+        const uint64_t chunks = k / kD2HChunk + B + 64;
+        if (!(s = grow(reinterpret_cast<void**>(&d_delta_), &d_delta_cap_, chunks * kD2HChunk * 4))
+                 .good() ||
             !(s = grow(reinterpret_cast<void**>(&d_cbase_), &d_cbase_cap_, chunks * 8)).good() ||
             !(s = grow(reinterpret_cast<void**>(&d_craw_), &d_craw_cap_, chunks)).good() ||
-            !(s = grow_host(reinterpret_cast<void**>(&h_delta_), &h_delta_cap_, k * 4 + 64)).good() ||
             !(s = grow_host(reinterpret_cast<void**>(&h_cbase_), &h_cbase_cap_, chunks * 8)).good() ||
-            !(s = grow_host(reinterpret_cast<void**>(&h_craw_), &h_craw_cap_, chunks)).good())
+            !(s = grow_host(reinterpret_cast<void**>(&h_craw_), &h_craw_cap_, chunks)).good() ||
+            !(s = ensure_ring()).good())
             return s;
+        if (bucket_ev_.size() < B) {
+            bucket_ev_.resize(B, nullptr);
+            for (auto& e : bucket_ev_)
+                if (!e) PH0B_TRY(cudaEventCreateWithFlags(&e, cudaEventDisableTiming), "event");
+        }
+        if (!enc_ev_) PH0B_TRY(cudaEventCreateWithFlags(&enc_ev_, cudaEventDisableTiming), "event");
+        if (ring_streams_.empty()) {
+            static const int ns = [] {
+                const char* e = getenv("PH0B_RING_STREAMS");
+                const int x = e ? atoi(e) : 2;
+                return x < 1 ? 1 : (x > 8 ? 8 : x);
+            }();
+            ring_streams_.push_back(copy_stream_);
+            for (int i = 1; i < ns; ++i) {
+                cudaStream_t x;
+                PH0B_TRY(cudaStreamCreateWithFlags(&x, cudaStreamNonBlocking), "cudaStreamCreate");
+                ring_streams_.push_back(x);
+            }
+        }
         if (!pool_) {
             static const int env_threads = [] {
                 const char* e = getenv("PH0B_DECODE_THREADS");
@@ -607,6 +711,7 @@ Status Context::run_host_overlapped(const double* X, uint64_t n, uint64_t d, uin
                 env_threads > 0 ? (unsigned)env_threads : (hw > 2 ? hw - 1 : 1));
         }
     }
+    volatile int overflow = 0;  // decode tasks: 1 = scale buffer too small, 2 = stream stalled
     // whatever the exit path, no decode task may still be writing the caller's buffer
     struct PoolGuard {
         DecodePool* p;
@@ -659,93 +764,134 @@ Status Context::run_host_overlapped(const double* X, uint64_t n, uint64_t d, uin
     PH0B_TRY(cudaStreamSynchronize(st), "partition");
     tr.mark("partition counts done");
     h_base[0] = 0;
-    uint64_t start = 0, host_base = 0;
+    uint64_t start = 0;
     int target = -1;
     auto pad = [&](uint64_t c) { return (c + kAlign - 1) / kAlign * kAlign; };
-    // D slice [host_base, d_base[b+1]) of a finished bucket -> host, in medium chunks (several
-    // medium copies sustain a higher PCIe rate than one large one: 55 vs 52 GB/s for 17 GB,
-    // tools/d2h_big.py)
-    // compressed variant: the encoder turns the slice into a u64 base + u32 deltas per
-    // 4096-value chunk (half the PCIe bytes), the copy engine ships that, and the host pool
-    // decodes each bucket as soon as its copy has landed (drain)
-    struct Pending {
-        uint32_t b;
-        uint64_t lo, n, cb, nch;
-    };
-    std::vector<Pending> pending;
-    uint64_t chunk_base = 0;
-    uint64_t d2h_total = 0;  // bytes moved device -> host by this call
-    if (compress && bucket_ev_.size() < B) {
-        bucket_ev_.resize(B, nullptr);
-        for (auto& e : bucket_ev_)
-            if (!e) PH0B_TRY(cudaEventCreateWithFlags(&e, cudaEventDisableTiming), "event");
+    // D slices of finished buckets -> host.
+    //  * compressed (default): the encoder turns the slice into a u64 base + u32 deltas per
+    //    4096-value chunk (half the PCIe bytes); the copy engine streams the deltas through a
+    //    small pinned ring (LLC-resident: the DMA writes land in the last-level cache and the
+    //    decode reads them from there) and the pool decodes each piece as soon as its ready
+    //    flag flips.  Nothing about a bucket is waited for on the host: the encode reads the
+    //    slice bounds from device words and the copies are sized by the bucket's edge count
+    //    (an upper bound of its |D|), so bucket b's copies are enqueued while bucket b+1 sorts.
+    //  * uncompressed: plain D2H of the slice in medium chunks once the bucket is sorted.
+    const uint32_t G = ring_piece_chunks();
+    const uint32_t R = ring_slots();
+    const uint32_t NS = ring_subtasks();
+    std::vector<uint64_t> nch_ub(B), cb(B + 1, 0);
+    for (uint32_t b = 0; b < B; ++b) {
+        nch_ub[b] = (tot[b] + kD2HChunk - 1) / kD2HChunk;
+        cb[b + 1] = cb[b] + nch_ub[b];
     }
+    uint64_t d2h_total = 0;  // bytes moved device -> host by this call
+    uint64_t enq_ns = 0;     // host time spent enqueuing the pieces (trace)
+    std::vector<uint32_t> pending;  // buckets whose raw chunks are not shipped yet
+    uint64_t* d_lohi = part_small_ + 2304;  // [2B] device copy of each bucket's D bounds
+    auto encode = [&](uint32_t b) -> Status {
+        if (!compress || tot[b] == 0) return Status::ok();
+        PH0B_TRY(cudaMemcpyAsync(d_lohi + 2 * b, d_base + b, 16, cudaMemcpyDefault, st), "copy");
+        launches += launch_d2h_encode_bucket(dbuf_, d_lohi + 2 * b, tot[b],
+                                             d_delta_ + cb[b] * kD2HChunk, d_cbase_ + cb[b],
+                                             d_craw_ + cb[b], st);
+        PH0B_CHECK_LAUNCH("D2H encode");
+        PH0B_TRY(cudaEventRecord(enc_ev_, st), "event");
+        return Status::ok();
+    };
+    // after encode(b): chunk bases + raw flags, then the pieces through the ring
+    auto stream_out = [&](uint32_t b) -> Status {
+        if (!compress || tot[b] == 0) return Status::ok();
+        cudaStream_t cs = copy_stream_;
+        const uint64_t nch = nch_ub[b];
+        PH0B_TRY(cudaStreamWaitEvent(cs, enc_ev_, 0), "wait");
+        PH0B_TRY(cudaMemcpyAsync(h_cbase_ + cb[b], d_cbase_ + cb[b], nch * 8,
+                                 cudaMemcpyDeviceToHost, cs), "D2H bases");
+        PH0B_TRY(cudaMemcpyAsync(h_craw_ + cb[b], d_craw_ + cb[b], nch, cudaMemcpyDeviceToHost,
+                                 cs), "D2H flags");
+        PH0B_TRY(cudaEventRecord(bucket_ev_[b], cs), "event");
+        // extra ring streams: their pieces must not land before the bases and flags
+        for (size_t i = 1; i < ring_streams_.size(); ++i)
+            PH0B_TRY(cudaStreamWaitEvent(ring_streams_[i], bucket_ev_[b], 0), "wait");
+        d2h_total += nch * 9;
+        // each piece's task is handed to the pool right after its copy is enqueued: when the
+        // copy stream's queue is full, the enqueue blocks until earlier pieces are decoded
+        std::vector<DecodeTask> task;
+        for (uint64_t j0 = 0; j0 < nch; j0 += G) {
+            const uint64_t pc = std::min<uint64_t>(G, nch - j0);
+            cs = ring_streams_[ring_seq_ % ring_streams_.size()];
+            const uint32_t slot = (uint32_t)(ring_seq_ % R);
+            const uint32_t gen = (uint32_t)(ring_seq_ / R + 1);
+            ++ring_seq_;
+            uint32_t* ring = h_ring_ + (uint64_t)slot * G * kD2HChunk;
+            const uint64_t dready = reinterpret_cast<uint64_t>(d_ringflags_ + slot);
+            const uint64_t dfreed = reinterpret_cast<uint64_t>(d_ringflags_ + R + slot);
+            const auto e0 = std::chrono::steady_clock::now();
+            if (!stream_wait_u32(cs, dfreed, gen - 1))
+                return {PH0B_ERR_CUDA, "D2H ring: stream wait failed"};
+            PH0B_TRY(cudaMemcpyAsync(ring, d_delta_ + (cb[b] + j0) * kD2HChunk,
+                                     pc * kD2HChunk * 4, cudaMemcpyDeviceToHost, cs), "D2H deltas");
+            if (!stream_write_u32(cs, dready, gen))
+                return {PH0B_ERR_CUDA, "D2H ring: stream write failed"};
+            enq_ns += std::chrono::duration_cast<std::chrono::nanoseconds>(
+                          std::chrono::steady_clock::now() - e0).count();
+            d2h_total += pc * kD2HChunk * 4;
+            // the piece is decoded by NS tasks of G/NS chunks (empty past the piece's end)
+            task.clear();
+            const uint64_t per = (G + NS - 1) / NS;
+            for (uint32_t i = 0; i < NS; ++i) {
+                const uint64_t c0 = std::min<uint64_t>(pc, i * per);
+                const uint64_t c1 = std::min<uint64_t>(pc, c0 + per);
+                DecodeTask t{ring + c0 * kD2HChunk, h_cbase_ + cb[b] + j0 + c0,
+                             h_craw_ + cb[b] + j0 + c0, reinterpret_cast<uint64_t*>(host_scale),
+                             (c1 - c0) * kD2HChunk, (uint32_t)kD2HChunk};
+                t.ready = h_ringflags_ + slot;
+                t.freed = h_ringflags_ + R + slot;
+                t.gen = gen;
+                t.bounds = h_base + b;
+                t.v0 = (j0 + c0) * kD2HChunk;
+                t.capacity = scale_capacity;
+                t.overflow = &overflow;
+                t.done = &ring_done_[slot];
+                t.nsub = NS;
+                task.push_back(t);
+            }
+            pool_->submit(task);
+        }
+        pending.push_back(b);
+        return Status::ok();
+    };
+    // raw chunks (a delta did not fit in 32 bits) of buckets whose flags have landed
     auto drain = [&](bool wait) -> Status {
         while (!pending.empty()) {
-            const Pending p = pending.front();
-            if (!wait && cudaEventQuery(bucket_ev_[p.b]) == cudaErrorNotReady) {
+            const uint32_t b = pending.front();
+            if (!wait && cudaEventQuery(bucket_ev_[b]) == cudaErrorNotReady) {
                 cudaGetLastError();
                 break;
             }
-            PH0B_TRY(cudaEventSynchronize(bucket_ev_[p.b]), "D2H bucket");
-            for (uint64_t j = 0; j < p.nch; ++j) {  // a delta did not fit in 32 bits: raw
-                if (!h_craw_[p.cb + j]) continue;
-                const uint64_t s0 = p.lo + j * kD2HChunk;
-                const uint64_t len = std::min<uint64_t>(kD2HChunk, p.lo + p.n - s0);
+            PH0B_TRY(cudaEventSynchronize(bucket_ev_[b]), "D2H bucket");
+            const uint64_t lo = h_base[b], nb = h_base[b + 1] - lo;
+            for (uint64_t j = 0; j * kD2HChunk < nb; ++j) {
+                if (!h_craw_[cb[b] + j]) continue;
+                const uint64_t s0 = lo + j * kD2HChunk;
+                const uint64_t len = std::min<uint64_t>(kD2HChunk, lo + nb - s0);
+                if (s0 + len > scale_capacity) {
+                    overflow = 1;
+                    continue;
+                }
                 PH0B_TRY(cudaMemcpyAsync(host_scale + s0, dbuf_ + s0, len * 8,
                                          cudaMemcpyDeviceToHost, copy_stream_), "D2H raw");
                 d2h_total += len * 8;
             }
-            std::vector<DecodeTask> tasks;
-            constexpr uint64_t kGroup = 64;  // chunks per decode task (256 Ki values)
-            for (uint64_t j0 = 0; j0 < p.nch; j0 += kGroup) {
-                const uint64_t s0 = p.lo + j0 * kD2HChunk;
-                const uint64_t n = std::min<uint64_t>(kGroup * kD2HChunk, p.lo + p.n - s0);
-                tasks.push_back({h_delta_ + s0, h_cbase_ + p.cb + j0, h_craw_ + p.cb + j0,
-                                 reinterpret_cast<uint64_t*>(host_scale + s0), n,
-                                 (uint32_t)kD2HChunk});
-            }
-            pool_->submit(tasks);
             pending.erase(pending.begin());
         }
         return Status::ok();
     };
-    auto ship = [&](uint32_t b) -> Status {
+    uint64_t host_base = 0;
+    auto ship_plain = [&](uint32_t b) -> Status {
         PH0B_TRY(cudaEventRecord(ev_[6], st), "event");
         PH0B_TRY(cudaEventSynchronize(ev_[6]), "bucket");
         tr.mark("bucket sorted", (long)b);
         const uint64_t next_base = h_base[b + 1];
-        // PH0B_D2H_RAW_EVERY=k ships every k-th bucket raw (0, the measured best: none)
-        const bool this_compressed =
-            compress && !(d2h_raw_every() && b % d2h_raw_every() == d2h_raw_every() - 1);
-        if (this_compressed && next_base > host_base) {
-            if (next_base > scale_capacity)
-                return {PH0B_ERR_CAPACITY, "scale buffer too small: need >= " +
-                                               std::to_string(next_base) + " entries"};
-            const uint64_t n = next_base - host_base;
-            const uint64_t nch = (n + kD2HChunk - 1) / kD2HChunk;
-            launches += launch_d2h_encode(dbuf_ + host_base, n, d_delta_ + host_base,
-                                          d_cbase_ + chunk_base, d_craw_ + chunk_base, st);
-            PH0B_CHECK_LAUNCH("D2H encode");
-            PH0B_TRY(cudaEventRecord(ev_[6], st), "event");
-            PH0B_TRY(cudaStreamWaitEvent(copy_stream_, ev_[6], 0), "wait");
-            for (uint64_t q = 0; q < n; q += 2 * d2h_chunk_elems()) {
-                const uint64_t e = std::min<uint64_t>(n, q + 2 * d2h_chunk_elems());
-                PH0B_TRY(cudaMemcpyAsync(h_delta_ + host_base + q, d_delta_ + host_base + q,
-                                         (e - q) * 4, cudaMemcpyDeviceToHost, copy_stream_),
-                         "D2H deltas");
-            }
-            PH0B_TRY(cudaMemcpyAsync(h_cbase_ + chunk_base, d_cbase_ + chunk_base, nch * 8,
-                                     cudaMemcpyDeviceToHost, copy_stream_), "D2H bases");
-            PH0B_TRY(cudaMemcpyAsync(h_craw_ + chunk_base, d_craw_ + chunk_base, nch,
-                                     cudaMemcpyDeviceToHost, copy_stream_), "D2H flags");
-            PH0B_TRY(cudaEventRecord(bucket_ev_[b], copy_stream_), "event");
-            d2h_total += n * 4 + nch * 9;
-            pending.push_back({b, host_base, n, chunk_base, nch});
-            chunk_base += nch;
-            host_base = next_base;
-            return drain(false);
-        }
         if (host_scale && next_base > host_base) {
             if (next_base > scale_capacity)
                 return {PH0B_ERR_CAPACITY, "scale buffer too small: need >= " +
@@ -775,6 +921,7 @@ Status Context::run_host_overlapped(const double* X, uint64_t n, uint64_t d, uin
                               c0 ? mm[0] : 0, c0 ? mm[B] : 0, false, dbuf_, d_base,
                               d_base + 1, nullptr, st, &res, &passes);
         if (!s.good()) return s;
+        tr.mark("bucket sorted", 0);
         r.times.sort_passes = passes;
         if (c0 && res == 1) {  // sorted data ended in the scratch half, which the scatter
                                // below overwrites: back into segment 0 first
@@ -783,7 +930,11 @@ Status Context::run_host_overlapped(const double* X, uint64_t n, uint64_t d, uin
             PH0B_TRY(cudaMemcpyAsync(vals_[1], vals_[1] + c0p, c0 * 4, cudaMemcpyDeviceToDevice,
                                      st), "D2D");
         }
-        if (!(s = ship(0)).good()) return s;
+        if (compress) {
+            if (!(s = encode(0)).good()) return s;
+        } else if (!(s = ship_plain(0)).good()) {
+            return s;
+        }
         // ---- the rest of the partition (segment 0 is already in place) --------------------
         launches += launch_partition_scatter(keys_[0], vals_[0], k, d_spl, B, part_counts_,
                                              d_tot, keys_[1], vals_[1], st, kmin, kmax, d_table,
@@ -799,6 +950,8 @@ Status Context::run_host_overlapped(const double* X, uint64_t n, uint64_t d, uin
             target = 0;
         }
         start = c0p;
+        // bucket 0's pieces are enqueued while the scatter runs
+        if (!(s = stream_out(0)).good()) return s;
     }
 
     // ---- per bucket: sort + unique into D, then stream that slice of D to the host ---------
@@ -806,10 +959,15 @@ Status Context::run_host_overlapped(const double* X, uint64_t n, uint64_t d, uin
         const uint64_t c = tot[b];
         int res = 0;
         uint32_t passes = 0;
+        // the previous bucket's copies are enqueued once this bucket's kernels are queued
+        const std::function<Status()> after = [&]() -> Status { return stream_out(b - 1); };
+        const bool hook = compress && b > 1;
         s = sort_unique_range(keys_[1] + start, vals_[1] + start, keys_[0] + start,
                               vals_[0] + start, c, c ? mm[b] : 0, c ? mm[B + b] : 0, false,
-                              dbuf_, d_base + b, d_base + b + 1, nullptr, st, &res, &passes);
+                              dbuf_, d_base + b, d_base + b + 1, nullptr, st, &res, &passes,
+                              hook ? &after : nullptr);
         if (!s.good()) return s;
+        if (compress && !hook && b > 1 && !(s = stream_out(b - 1)).good()) return s;
         r.times.sort_passes = std::max(r.times.sort_passes, passes);
         const int buf = res == 0 ? 1 : 0;  // global buffer holding this bucket's sorted data
         if (c && target < 0) target = buf;
@@ -819,9 +977,16 @@ Status Context::run_host_overlapped(const double* X, uint64_t n, uint64_t d, uin
             PH0B_TRY(cudaMemcpyAsync(vals_[target] + start, vals_[buf] + start, c * 4,
                                      cudaMemcpyDeviceToDevice, st), "D2D");
         }
-        if (!(s = ship(b)).good()) return s;
+        if (compress) {
+            tr.mark("bucket sorted", (long)b);
+            if (!(s = encode(b)).good()) return s;
+            if (!(s = drain(false)).good()) return s;
+        } else if (!(s = ship_plain(b)).good()) {
+            return s;
+        }
         start += pad(c);
     }
+    if (compress && B > 1 && !(s = stream_out(B - 1)).good()) return s;
     const uint64_t kpad = start;  // columns incl. the sentinel padding
     if (target < 0) target = 0;
     // padding slots of M hold the cycle column {0, 0} in whichever buffer M ended up
@@ -854,11 +1019,26 @@ Status Context::run_host_overlapped(const double* X, uint64_t n, uint64_t d, uin
         if (!(s = drain(true)).good()) return s;
         pool_->wait();
         tr.mark("decode done");
+        if (tr.on) {
+            uint64_t w, dn, np;
+            decode_stats(&w, &dn, &np, true);
+            fprintf(stderr, "[ph0b trace] pieces %lu: wait %.1f ms, decode %.1f ms (summed over "
+                    "%u threads), enqueue blocked %.1f ms\n", (unsigned long)np, w * 1e-6,
+                    dn * 1e-6, pool_->threads(), enq_ns * 1e-6);
+        }
     }
     PH0B_TRY(cudaStreamSynchronize(copy_stream_), "D2H scale");
+    for (size_t i = 1; i < ring_streams_.size(); ++i)
+        PH0B_TRY(cudaStreamSynchronize(ring_streams_[i]), "D2H scale");
     tr.mark("D2H done");
+    const uint64_t n_scale = h_base[B];
+    if (overflow == 1 || (host_scale && n_scale > scale_capacity))
+        return {PH0B_ERR_CAPACITY,
+                "scale buffer too small: need >= " + std::to_string(n_scale) + " entries"};
+    if (overflow)
+        return {PH0B_ERR_CUDA, "D2H of D stalled (the copy stream made no progress)"};
     r.times.d2h_bytes = d2h_total;
-    r.n_scale = host_base;
+    r.n_scale = n_scale;
     r.d_uv_sorted = vals_[cur_];
     r.d_scale = dbuf_;
     r.d_death_grade = death_grade_;

@@ -3,7 +3,9 @@
 
 #include <cuda_runtime.h>
 
+#include <atomic>
 #include <cstdint>
+#include <functional>
 #include <memory>
 #include <mutex>
 #include <string>
@@ -70,7 +72,8 @@ public:
     Status sort_unique_range(uint64_t* kb0, uint32_t* vb0, uint64_t* kb1, uint32_t* vb1,
                              uint64_t k, uint64_t kmin, uint64_t kmax, bool raw_hist,
                              double* scale_out, const uint64_t* d_base, uint64_t* d_count,
-                             uint32_t* grade_out, cudaStream_t st, int* res, uint32_t* passes);
+                             uint32_t* grade_out, cudaStream_t st, int* res, uint32_t* passes,
+                             const std::function<Status()>* after_enqueue = nullptr);
     // Host-output run with the D2H of D overlapped with the sort: edges are split into
     // key-range buckets (one stable partition pass), each bucket is sorted + deduplicated
     // in turn and its slice of D streams to the host while the next bucket sorts.
@@ -140,7 +143,16 @@ private:
     uint32_t* d_delta_ = nullptr;  uint64_t d_delta_cap_ = 0;
     uint64_t* d_cbase_ = nullptr;  uint64_t d_cbase_cap_ = 0;
     uint8_t* d_craw_ = nullptr;    uint64_t d_craw_cap_ = 0;
-    uint32_t* h_delta_ = nullptr;  uint64_t h_delta_cap_ = 0;
+    // streamed D2H ring: pinned slots the copy engine fills and the decode pool drains; ring
+    // flags in mapped host memory ([0,256) ready, [256,512) freed, by slot)
+    uint32_t* h_ring_ = nullptr;   uint64_t h_ring_cap_ = 0;
+    uint32_t* h_ringflags_ = nullptr;
+    uint32_t* d_ringflags_ = nullptr;
+    uint64_t ring_seq_ = 0;
+    std::atomic<uint64_t> ring_done_[256] = {};  // per slot: decode tasks completed (monotone)
+    cudaEvent_t enc_ev_ = nullptr;
+    std::vector<cudaStream_t> ring_streams_;  // [0] = copy_stream_
+    Status ensure_ring();
     uint64_t* h_cbase_ = nullptr;  uint64_t h_cbase_cap_ = 0;
     uint8_t* h_craw_ = nullptr;    uint64_t h_craw_cap_ = 0;
     std::unique_ptr<DecodePool> pool_;
