@@ -183,6 +183,30 @@ int ph0b_shard_partition(ph0b_context* ctx, const uint64_t* splitters, uint32_t 
                          uint64_t* counts, uint64_t* part_min, uint64_t* part_max);
 /* Device receive buffers for `count` edges (keys u64, columns u32). */
 int ph0b_shard_recv(ph0b_context* ctx, uint64_t count, uint64_t** d_keys, uint32_t** d_vals);
+/* ---- exchange over peer memory (replaces partition + NCCL all-to-all-v): the partition's
+ * counts only, then ONE kernel that scatters every part straight into its destination
+ * rank's receive buffer (NVLink P2P stores through CUDA IPC mappings), in the same stable
+ * order the all-to-all-v would deliver.  Sequence per rank: partition_count -> all-gather
+ * counts -> recv_peer -> all-gather IPC handles -> open peers' handles -> scatter_peers
+ * -> barrier -> sort_unique. */
+/* Counts and key bounds of the stable partition (as ph0b_shard_partition, no scatter). */
+int ph0b_shard_partition_count(ph0b_context* ctx, const uint64_t* splitters, uint32_t parts,
+                               void* stream, uint64_t* counts, uint64_t* part_min,
+                               uint64_t* part_max);
+/* Receive buffers for `count` edges that peers write into (cudaMalloc bases: IPC-exportable;
+ * the local edges stay intact). Synchronizes the device. */
+int ph0b_shard_recv_peer(ph0b_context* ctx, uint64_t count, uint64_t** d_keys,
+                         uint32_t** d_vals);
+/* Scatter of the local edges: part b -> device byte addresses dst_keys[b]/dst_vals[b] (the
+ * receive buffers of rank b, mapped into this process) starting at element dst_offsets[b]
+ * (= edges of part b held by lower ranks).  Returns when the stores are complete. */
+int ph0b_shard_scatter_peers(ph0b_context* ctx, uint32_t parts, const uint64_t* dst_keys,
+                             const uint64_t* dst_vals, const uint64_t* dst_offsets,
+                             void* stream);
+/* CUDA IPC of receive buffers between rank processes (64-byte opaque handles). */
+int ph0b_ipc_get_handle(const void* d_ptr, void* handle_out);
+int ph0b_ipc_open_handle(const void* handle, void** d_ptr);
+int ph0b_ipc_close(void* d_ptr);
 /* Sort + unique of the received slice: local |D| and the device pointer of the D slice. */
 int ph0b_shard_sort_unique(ph0b_context* ctx, uint64_t count, uint64_t kmin, uint64_t kmax,
                            void* stream, uint64_t* n_distinct, const double** d_scale,

@@ -168,7 +168,8 @@ int launch_partition_scatter(const uint64_t* keys, const uint32_t* vals, uint64_
                              const uint32_t* d_counts_scratch, const uint64_t* d_totals,
                              uint64_t* keys_out, uint32_t* vals_out, cudaStream_t s,
                              uint64_t kmin, uint64_t kmax, const uint16_t* d_table,
-                             uint32_t skip_bucket);
+                             uint32_t skip_bucket, const uint64_t* d_peer_k = nullptr,
+                             const uint64_t* d_peer_v = nullptr);
 uint64_t partition_scratch_words(uint64_t count, uint32_t parts);
 int launch_sample(const uint64_t* keys, uint64_t count, uint64_t s, uint64_t* out, cudaStream_t st);
 int launch_gather_u32(const uint32_t* src, const uint32_t* idx, uint64_t m, uint32_t* out,

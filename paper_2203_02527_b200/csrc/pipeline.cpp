@@ -325,11 +325,12 @@ Status Context::reserve(uint64_t n, uint64_t d) {
     return reserve_edges(n * (n - (n > 0)) / 2);
 }
 
-Status Context::reserve_recv(uint64_t k) {
+Status Context::reserve_recv(uint64_t k, int buffer) {
     Status s;
-    if (!(s = grow(reinterpret_cast<void**>(&keys_[0]), &keys_cap_[0], k * 8 + 4096)).good())
+    if (!(s = grow(reinterpret_cast<void**>(&keys_[buffer]), &keys_cap_[buffer], k * 8 + 4096))
+             .good())
         return s;
-    return grow(reinterpret_cast<void**>(&vals_[0]), &vals_cap_[0], k * 4 + 4096);
+    return grow(reinterpret_cast<void**>(&vals_[buffer]), &vals_cap_[buffer], k * 4 + 4096);
 }
 
 Status Context::sort_survivors(uint32_t m, uint64_t count, cudaStream_t st) {
@@ -513,19 +514,19 @@ Status Context::sort_unique_range(uint64_t* kb0, uint32_t* vb0, uint64_t* kb1, u
 }
 
 Status Context::stage_sort_unique(uint64_t k, uint64_t kmin, uint64_t kmax, bool raw_hist,
-                                  bool want_grade, cudaStream_t st, uint32_t* passes) {
+                                  bool want_grade, cudaStream_t st, uint32_t* passes, int src) {
     if (want_grade) {
         Status s = grow(reinterpret_cast<void**>(&grade_), &grade_cap_, std::max<uint64_t>(4, k * 4));
         if (!s.good()) return s;
     }
-    cur_ = 0;
+    cur_ = src;
     *passes = 0;
     int res = 0;
-    Status s = sort_unique_range(keys_[0], vals_[0], keys_[1], vals_[1], k, kmin, kmax, raw_hist,
-                                 nullptr, nullptr, small_ + 2, want_grade ? grade_ : nullptr, st,
-                                 &res, passes);
+    Status s = sort_unique_range(keys_[src], vals_[src], keys_[src ^ 1], vals_[src ^ 1], k, kmin,
+                                 kmax, raw_hist && src == 0, nullptr, nullptr, small_ + 2,
+                                 want_grade ? grade_ : nullptr, st, &res, passes);
     if (!s.good()) return s;
-    cur_ = res;
+    cur_ = src ^ res;
     scale_ = reinterpret_cast<double*>(keys_[cur_ ^ 1]);
     return Status::ok();
 }

@@ -63,7 +63,7 @@ public:
                            uint64_t u_lo, uint64_t u_hi, cudaStream_t st, uint64_t* count,
                            uint64_t* kmin, uint64_t* kmax);
     Status stage_sort_unique(uint64_t count, uint64_t kmin, uint64_t kmax, bool raw_hist,
-                             bool want_grade, cudaStream_t st, uint32_t* passes);
+                             bool want_grade, cudaStream_t st, uint32_t* passes, int src = 0);
     Status stage_reduce(const uint32_t* uv, uint64_t count, uint32_t n, cudaStream_t st,
                         ReduceStats* rst);
     // Sort (kb0, vb0) of k edges (ping-pong with kb1/vb1) and write its distinct lengths to
@@ -86,7 +86,9 @@ public:
     bool kruskal_mode = false;  // set by the C entry points (under mu) for one run
     Status reserve_edges(uint64_t count);  // ping-pong key/column buffers for count edges
     Status reserve_points(uint64_t n, uint64_t d);
-    Status reserve_recv(uint64_t count);   // sharded receive side: buffer 0 only
+    // sharded receive side: one ping-pong buffer only (0: NCCL path, whose send data sits in
+    // buffer 1; 1: peer-memory exchange, while the local scatter still reads buffer 0)
+    Status reserve_recv(uint64_t count, int buffer = 0);
     Status sort_survivors(uint32_t m, uint64_t count, cudaStream_t st);
     // workspace accessors for the sharded C entry points
     uint64_t* keys(int i) { return keys_[i]; }

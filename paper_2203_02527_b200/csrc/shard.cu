@@ -222,8 +222,13 @@ __global__ void __launch_bounds__(kThreads, 3)
                const uint64_t* __restrict__ splitters, uint32_t parts,
                const uint32_t* __restrict__ offsets, const uint64_t* __restrict__ starts,
                uint64_t* __restrict__ keys_out, uint32_t* __restrict__ vals_out,
-               const uint16_t* __restrict__ cells, CellMap cm, uint32_t skip_bucket) {
+               const uint16_t* __restrict__ cells, CellMap cm, uint32_t skip_bucket,
+               const uint64_t* __restrict__ peer_k, const uint64_t* __restrict__ peer_v) {
     __shared__ uint64_t s_spl[kMaxParts];
+    // peer mode (peer_k != null): bucket b goes straight into its destination rank's receive
+    // buffer (NVLink P2P stores through a CUDA IPC mapping); peer_k/peer_v[b] are byte
+    // addresses already offset so that local layout position q lands at q * 8 / q * 4
+    __shared__ uint64_t s_pk[kMaxParts], s_pv[kMaxParts];
     __shared__ uint16_t s_cell[kCells];
     __shared__ uint32_t s_whist[kWarps][kMaxParts];
     __shared__ uint32_t s_tstart[kMaxParts];
@@ -247,6 +252,10 @@ __global__ void __launch_bounds__(kThreads, 3)
     }
     // kThreads == kMaxParts: thread b owns bucket b in the per-bucket steps
     s_spl[tid] = (uint32_t)tid + 1 < parts ? splitters[tid] : ~0ull;
+    if (peer_k) {
+        s_pk[tid] = (uint32_t)tid < parts ? peer_k[tid] : 0ull;
+        s_pv[tid] = (uint32_t)tid < parts ? peer_v[tid] : 0ull;
+    }
     for (uint32_t i = tid; i < kCells / 8; i += kThreads)
         reinterpret_cast<uint4*>(s_cell)[i] = reinterpret_cast<const uint4*>(cells)[i];
     const uint64_t my_base =
@@ -292,9 +301,15 @@ __global__ void __launch_bounds__(kThreads, 3)
     for (int i = 0; i < kItems; ++i) {
         const uint32_t p = (uint32_t)i * kThreads + tid;
         if (p < tn && s_b[p] != skip_bucket) {
-            const uint64_t dst = s_base[s_b[p]] + p;
-            keys_out[dst] = s_k[p];
-            vals_out[dst] = s_v[p];
+            const uint32_t b = s_b[p];
+            const uint64_t dst = s_base[b] + p;
+            if (peer_k) {
+                reinterpret_cast<uint64_t*>(s_pk[b])[dst] = s_k[p];
+                reinterpret_cast<uint32_t*>(s_pv[b])[dst] = s_v[p];
+            } else {
+                keys_out[dst] = s_k[p];
+                vals_out[dst] = s_v[p];
+            }
         }
     }
 }
@@ -437,7 +452,8 @@ int launch_partition_scatter(const uint64_t* keys, const uint32_t* vals, uint64_
                              const uint32_t* d_counts_scratch, const uint64_t* d_totals,
                              uint64_t* keys_out, uint32_t* vals_out, cudaStream_t s,
                              uint64_t kmin, uint64_t kmax, const uint16_t* d_table,
-                             uint32_t skip_bucket) {
+                             uint32_t skip_bucket, const uint64_t* d_peer_k,
+                             const uint64_t* d_peer_v) {
     const uint64_t tiles = (count + kTile - 1) / kTile;
     if (tiles == 0) return 0;
     const uint64_t span = kmax >= kmin ? kmax - kmin : 0;
@@ -452,7 +468,7 @@ int launch_partition_scatter(const uint64_t* keys, const uint32_t* vals, uint64_
     k7_scatter<<<(unsigned)tiles, kThreads, kScSmem, s>>>(keys, vals, count, d_splitters, parts,
                                                           d_counts_scratch, d_totals + parts,
                                                           keys_out, vals_out, d_table, cm,
-                                                          skip_bucket);
+                                                          skip_bucket, d_peer_k, d_peer_v);
     return 1;
 }
 
@@ -473,7 +489,7 @@ int launch_partition(const uint64_t* keys, const uint32_t* vals, uint64_t count,
     if (l < 0) return l;
     return l + launch_partition_scatter(keys, vals, count, d_splitters, parts, d_counts_scratch,
                                         d_totals, keys_out, vals_out, s, kmin, kmax, d_table,
-                                        ~0u);
+                                        ~0u, nullptr, nullptr);
 }
 
 int launch_sample(const uint64_t* keys, uint64_t count, uint64_t s, uint64_t* out, cudaStream_t st) {

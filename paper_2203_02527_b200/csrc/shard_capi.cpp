@@ -41,6 +41,10 @@ struct ShardScratch {
     uint64_t cand_cap = 0;
     uint64_t local_count = 0;       // edges produced by shard_distances
     uint64_t local_kmin = 0, local_kmax = 0;
+    // peer-memory exchange: per-part local layout starts and the received slice's buffer
+    std::vector<uint64_t> starts;   // [parts] from ph0b_shard_partition_count
+    uint64_t* d_peer = nullptr;     // [2][256] adjusted destination byte addresses
+    int recv_buffer = 0;            // ping-pong buffer holding the received slice
 };
 
 std::mutex g_scratch_mu;
@@ -75,6 +79,49 @@ int ensure(void** p, uint64_t* cap, uint64_t bytes) {
     return PH0B_OK;
 }
 
+// Device scratch of the partition stages and the splitters on the device.
+int partition_setup(Context* c, ShardScratch& sc, const uint64_t* splitters, uint32_t parts,
+                    cudaStream_t st) {
+    uint64_t cap = 0;
+    int rc = 0;
+    if (!sc.d_spl) {
+        if ((rc = ensure(reinterpret_cast<void**>(&sc.d_spl), &cap, 256 * 8))) return rc;
+        cap = 0;
+        if ((rc = ensure(reinterpret_cast<void**>(&sc.d_totals), &cap, 512 * 8))) return rc;
+        cap = 0;
+        if ((rc = ensure(reinterpret_cast<void**>(&sc.d_bminmax), &cap, 512 * 8))) return rc;
+        cap = 0;
+        if ((rc = ensure(reinterpret_cast<void**>(&sc.d_table), &cap,
+                         ph0b::partition_table_bytes())))
+            return rc;
+    }
+    const uint64_t words = ph0b::partition_scratch_words(sc.local_count, parts);
+    if ((rc = ensure(reinterpret_cast<void**>(&sc.d_counts), &sc.counts_cap, words * 4 + 4)))
+        return rc;
+    (void)c;
+    if (parts > 1 && cudaMemcpyAsync(sc.d_spl, splitters, (parts - 1) * 8,
+                                     cudaMemcpyHostToDevice, st))
+        return ph0b::capi_fail(PH0B_ERR_CUDA, "H2D splitters");
+    return PH0B_OK;
+}
+
+// Per-part counts and key bounds back to the host; the local layout starts (align 1).
+int read_partition(ShardScratch& sc, uint32_t parts, cudaStream_t st, uint64_t* counts,
+                   uint64_t* part_min, uint64_t* part_max) {
+    std::vector<uint64_t> tot(parts), mm(2 * parts);
+    if (cudaGetLastError() != cudaSuccess ||
+        cudaMemcpyAsync(tot.data(), sc.d_totals, parts * 8, cudaMemcpyDeviceToHost, st) ||
+        cudaMemcpyAsync(mm.data(), sc.d_bminmax, 2 * parts * 8, cudaMemcpyDeviceToHost, st) ||
+        cudaStreamSynchronize(st))
+        return ph0b::capi_fail(PH0B_ERR_CUDA, "shard partition");
+    sc.starts.assign(parts, 0);
+    for (uint32_t b = 1; b < parts; ++b) sc.starts[b] = sc.starts[b - 1] + tot[b - 1];
+    if (counts) std::memcpy(counts, tot.data(), parts * 8);
+    if (part_min) std::memcpy(part_min, mm.data(), parts * 8);
+    if (part_max) std::memcpy(part_max, mm.data() + parts, parts * 8);
+    return PH0B_OK;
+}
+
 inline uint64_t row_base(uint64_t u, uint64_t n) { return u * (2 * n - u - 1) / 2; }
 
 }  // namespace
@@ -89,7 +136,7 @@ void shard_scratch_release(Context* c) {
         ShardScratch& sc = all[i].second;
         cudaSetDevice(c->device());
         void* ps[] = {sc.d_spl, sc.d_totals, sc.d_bminmax, sc.d_table, sc.d_counts,
-                      sc.d_sample, sc.d_cand_uv};
+                      sc.d_sample, sc.d_cand_uv, sc.d_peer};
         for (void* p : ps)
             if (p) cudaFree(p);
         all.erase(all.begin() + (long)i);
@@ -151,40 +198,111 @@ int ph0b_shard_partition(ph0b_context* ctx, const uint64_t* splitters, uint32_t 
         return ph0b::capi_fail(PH0B_ERR_INVALID_ARGUMENT, "parts must be in [1, 256]");
     ShardScratch& sc = scratch(c);
     cudaStream_t st = pick(c, stream);
-    uint64_t cap = 0;
-    int rc = 0;
-    if (!sc.d_spl) {
-        if ((rc = ensure(reinterpret_cast<void**>(&sc.d_spl), &cap, 256 * 8))) return rc;
-        cap = 0;
-        if ((rc = ensure(reinterpret_cast<void**>(&sc.d_totals), &cap, 512 * 8))) return rc;
-        cap = 0;
-        if ((rc = ensure(reinterpret_cast<void**>(&sc.d_bminmax), &cap, 512 * 8))) return rc;
-        cap = 0;
-        if ((rc = ensure(reinterpret_cast<void**>(&sc.d_table), &cap,
-                         ph0b::partition_table_bytes())))
-            return rc;
-    }
-    const uint64_t words = ph0b::partition_scratch_words(sc.local_count, parts);
-    if ((rc = ensure(reinterpret_cast<void**>(&sc.d_counts), &sc.counts_cap, words * 4 + 4)))
-        return rc;
-    if (parts > 1 && cudaMemcpyAsync(sc.d_spl, splitters, (parts - 1) * 8,
-                                     cudaMemcpyHostToDevice, st))
-        return ph0b::capi_fail(PH0B_ERR_CUDA, "H2D splitters");
+    int rc = partition_setup(c, sc, splitters, parts, st);
+    if (rc) return rc;
     c->launches = ph0b::launch_partition(c->keys(0), c->vals(0), sc.local_count, sc.d_spl, parts,
                                          sc.d_counts, sc.d_totals, sc.d_bminmax, c->keys(1),
                                          c->vals(1), st, 1, sc.local_kmin, sc.local_kmax,
                                          splitters, sc.d_table);
     ph0b::capi_set_launches(c->launches);
-    std::vector<uint64_t> mm(2 * parts);
-    if (cudaGetLastError() != cudaSuccess ||
-        cudaMemcpyAsync(counts, sc.d_totals, parts * 8, cudaMemcpyDeviceToHost, st) ||
-        cudaMemcpyAsync(mm.data(), sc.d_bminmax, 2 * parts * 8, cudaMemcpyDeviceToHost, st) ||
-        cudaStreamSynchronize(st))
-        return ph0b::capi_fail(PH0B_ERR_CUDA, "shard partition");
-    if (part_min) std::memcpy(part_min, mm.data(), parts * 8);
-    if (part_max) std::memcpy(part_max, mm.data() + parts, parts * 8);
+    if ((rc = read_partition(sc, parts, st, counts, part_min, part_max))) return rc;
     if (d_keys_send) *d_keys_send = c->keys(1);
     if (d_vals_send) *d_vals_send = c->vals(1);
+    return PH0B_OK;
+}
+
+int ph0b_shard_partition_count(ph0b_context* ctx, const uint64_t* splitters, uint32_t parts,
+                               void* stream, uint64_t* counts, uint64_t* part_min,
+                               uint64_t* part_max) {
+    Context* c = reinterpret_cast<Context*>(ctx);
+    std::lock_guard<std::mutex> lk(c->mu);
+    if (parts < 1 || parts > 256)
+        return ph0b::capi_fail(PH0B_ERR_INVALID_ARGUMENT, "parts must be in [1, 256]");
+    ShardScratch& sc = scratch(c);
+    cudaStream_t st = pick(c, stream);
+    int rc = partition_setup(c, sc, splitters, parts, st);
+    if (rc) return rc;
+    c->launches = ph0b::launch_partition_count(c->keys(0), sc.local_count, sc.d_spl, parts,
+                                               sc.d_counts, sc.d_totals, sc.d_bminmax,
+                                               c->keys(1), c->vals(1), st, 1, sc.local_kmin,
+                                               sc.local_kmax, splitters, sc.d_table);
+    ph0b::capi_set_launches(c->launches);
+    return read_partition(sc, parts, st, counts, part_min, part_max);
+}
+
+int ph0b_shard_recv_peer(ph0b_context* ctx, uint64_t count, uint64_t** d_keys,
+                         uint32_t** d_vals) {
+    Context* c = reinterpret_cast<Context*>(ctx);
+    std::lock_guard<std::mutex> lk(c->mu);
+    Status s = c->reserve_recv(count, 1);  // buffer 0 still holds the local edges
+    if (!s.good()) return ph0b::capi_fail(s);
+    if (cudaDeviceSynchronize() != cudaSuccess)  // peers may write as soon as they see it
+        return ph0b::capi_fail(PH0B_ERR_CUDA, "shard recv");
+    scratch(c).recv_buffer = 1;
+    if (d_keys) *d_keys = c->keys(1);
+    if (d_vals) *d_vals = c->vals(1);
+    return PH0B_OK;
+}
+
+int ph0b_shard_scatter_peers(ph0b_context* ctx, uint32_t parts, const uint64_t* dst_keys,
+                             const uint64_t* dst_vals, const uint64_t* dst_offsets,
+                             void* stream) {
+    Context* c = reinterpret_cast<Context*>(ctx);
+    std::lock_guard<std::mutex> lk(c->mu);
+    ShardScratch& sc = scratch(c);
+    if (parts < 1 || parts > 256 || sc.starts.size() != parts)
+        return ph0b::capi_fail(PH0B_ERR_INVALID_ARGUMENT,
+                               "scatter_peers: call ph0b_shard_partition_count first");
+    cudaStream_t st = pick(c, stream);
+    uint64_t cap = 0;
+    int rc = 0;
+    if (!sc.d_peer && (rc = ensure(reinterpret_cast<void**>(&sc.d_peer), &cap, 512 * 8)))
+        return rc;
+    // part b's local layout position q goes to dst_keys[b] + 8 * (dst_offsets[b] + q - start_b)
+    std::vector<uint64_t> adj(512, 0);
+    for (uint32_t b = 0; b < parts; ++b) {
+        adj[b] = dst_keys[b] + 8 * (dst_offsets[b] - sc.starts[b]);
+        adj[256 + b] = dst_vals[b] + 4 * (dst_offsets[b] - sc.starts[b]);
+    }
+    if (cudaMemcpyAsync(sc.d_peer, adj.data(), 512 * 8, cudaMemcpyHostToDevice, st))
+        return ph0b::capi_fail(PH0B_ERR_CUDA, "H2D peer table");
+    c->launches = ph0b::launch_partition_scatter(
+        c->keys(0), c->vals(0), sc.local_count, sc.d_spl, parts, sc.d_counts, sc.d_totals,
+        nullptr, nullptr, st, sc.local_kmin, sc.local_kmax, sc.d_table, ~0u, sc.d_peer,
+        sc.d_peer + 256);
+    ph0b::capi_set_launches(c->launches);
+    // the stores into peer memory are complete when the kernel is; the caller's barrier
+    // then publishes them to the receiving ranks
+    if (cudaGetLastError() != cudaSuccess || cudaStreamSynchronize(st))
+        return ph0b::capi_fail(PH0B_ERR_CUDA, "shard scatter to peers");
+    return PH0B_OK;
+}
+
+int ph0b_ipc_get_handle(const void* d_ptr, void* handle_out) {
+    cudaIpcMemHandle_t h;
+    if (cudaIpcGetMemHandle(&h, const_cast<void*>(d_ptr)) != cudaSuccess) {
+        cudaGetLastError();
+        return ph0b::capi_fail(PH0B_ERR_CUDA, "cudaIpcGetMemHandle");
+    }
+    std::memcpy(handle_out, &h, sizeof(h));
+    return PH0B_OK;
+}
+
+int ph0b_ipc_open_handle(const void* handle, void** d_ptr) {
+    cudaIpcMemHandle_t h;
+    std::memcpy(&h, handle, sizeof(h));
+    if (cudaIpcOpenMemHandle(d_ptr, h, cudaIpcMemLazyEnablePeerAccess) != cudaSuccess) {
+        cudaGetLastError();
+        return ph0b::capi_fail(PH0B_ERR_CUDA, "cudaIpcOpenMemHandle");
+    }
+    return PH0B_OK;
+}
+
+int ph0b_ipc_close(void* d_ptr) {
+    if (cudaIpcCloseMemHandle(d_ptr) != cudaSuccess) {
+        cudaGetLastError();
+        return ph0b::capi_fail(PH0B_ERR_CUDA, "cudaIpcCloseMemHandle");
+    }
     return PH0B_OK;
 }
 
@@ -193,6 +311,7 @@ int ph0b_shard_recv(ph0b_context* ctx, uint64_t count, uint64_t** d_keys, uint32
     std::lock_guard<std::mutex> lk(c->mu);
     Status s = c->reserve_recv(count);  // grows buffer 0 only: buffer 1 holds the send data
     if (!s.good()) return ph0b::capi_fail(s);
+    scratch(c).recv_buffer = 0;
     if (d_keys) *d_keys = c->keys(0);
     if (d_vals) *d_vals = c->vals(0);
     return PH0B_OK;
@@ -209,7 +328,9 @@ int ph0b_shard_sort_unique(ph0b_context* ctx, uint64_t count, uint64_t kmin, uin
     c->launches = 0;
     uint32_t passes = 0;
     if (kmax < kmin) kmax = kmin;
-    s = c->stage_sort_unique(count, kmin, kmax, false, false, st, &passes);
+    s = c->stage_sort_unique(count, kmin, kmax, false, false, st, &passes,
+                             scratch(c).recv_buffer);
+    scratch(c).recv_buffer = 0;
     ph0b::capi_set_launches(c->launches);
     if (!s.good()) return ph0b::capi_fail(s);
     if (cudaMemcpyAsync(c->small_host() + 2, c->small_dev() + 2, 8, cudaMemcpyDeviceToHost, st) ||

@@ -74,6 +74,8 @@ class ShardResult:
 class TorchComm:
     """torch.distributed transport (NCCL for device tensors, gloo for CPU tensors)."""
 
+    same_process = False  # peer buffers are shared through IPC handles
+
     def __init__(self, group=None):
         import torch.distributed as dist
         self.dist = dist
@@ -99,6 +101,8 @@ class TorchComm:
 
 class ThreadComm:
     """P virtual ranks as threads of one process (single-GPU multi-rank parity tests)."""
+
+    same_process = True  # peer buffers are plain device pointers of this process
 
     class _Shared:
         def __init__(self, size):
@@ -182,6 +186,11 @@ class DeviceBackend:
                                                  C.POINTER(C.c_uint32)]),
             ("ph0b_shard_reduce", C.c_int, [vp, u64, u64, u64, vp, u64p, C.POINTER(vp), C.POINTER(vp), C.POINTER(vp)]),
             ("ph0b_reduce_columns", C.c_int, [vp, vp, u64, u64, vp, vp, u64p]),
+            ("ph0b_shard_partition_count", C.c_int, [vp, vp, u32, vp, vp, vp, vp]),
+            ("ph0b_shard_recv_peer", C.c_int, [vp, u64, C.POINTER(vp), C.POINTER(vp)]),
+            ("ph0b_shard_scatter_peers", C.c_int, [vp, u32, vp, vp, vp, vp]),
+            ("ph0b_ipc_get_handle", C.c_int, [vp, vp]),
+            ("ph0b_ipc_open_handle", C.c_int, [vp, C.POINTER(vp)]),
         ]:
             fn = getattr(L, name)
             fn.restype, fn.argtypes = res, args
@@ -234,6 +243,56 @@ class DeviceBackend:
         self._count()
         return nd.value, _dev_view(sp.value, nd.value, "<f8", self.device)
 
+    # ---- exchange over peer memory (NVLink P2P stores; replaces partition + all-to-all-v)
+    def partition_count(self, splitters, parts):
+        spl = np.ascontiguousarray(splitters, np.uint64)
+        counts = np.zeros(parts, np.uint64)
+        pmin = np.zeros(parts, np.uint64)
+        pmax = np.zeros(parts, np.uint64)
+        _b._check(self.L.ph0b_shard_partition_count(
+            self.h, C.c_void_p(spl.ctypes.data) if spl.size else None, parts, None,
+            C.c_void_p(counts.ctypes.data), C.c_void_p(pmin.ctypes.data),
+            C.c_void_p(pmax.ctypes.data)))
+        self._count()
+        return counts, pmin, pmax
+
+    def recv_peer(self, count, same_process):
+        """Receive buffers peers write into; returns what the peers need to reach them."""
+        kp, vp_ = C.c_void_p(), C.c_void_p()
+        _b._check(self.L.ph0b_shard_recv_peer(self.h, count, C.byref(kp), C.byref(vp_)))
+        self._recv = (int(kp.value or 0), int(vp_.value or 0))
+        if same_process:
+            return self._recv
+        hk, hv = (C.c_char * 64)(), (C.c_char * 64)()
+        _b._check(self.L.ph0b_ipc_get_handle(C.c_void_p(self._recv[0]), hk))
+        _b._check(self.L.ph0b_ipc_get_handle(C.c_void_p(self._recv[1]), hv))
+        return (bytes(hk), bytes(hv))
+
+    def open_peer(self, desc, is_self, same_process):
+        """Device addresses (in this process) of a peer's receive buffers."""
+        if is_self:
+            return self._recv
+        if same_process:
+            return desc
+        cache = self.__dict__.setdefault("_ipc", {})
+        if desc not in cache:  # buffers are reused across calls: map each handle once
+            ptrs = []
+            for h in desc:
+                p = C.c_void_p()
+                _b._check(self.L.ph0b_ipc_open_handle(C.c_char_p(h), C.byref(p)))
+                ptrs.append(int(p.value))
+            cache[desc] = tuple(ptrs)
+        return cache[desc]
+
+    def scatter_peers(self, parts, dst, offsets):
+        kd = np.array([d[0] for d in dst], np.uint64)
+        vd = np.array([d[1] for d in dst], np.uint64)
+        off = np.ascontiguousarray(offsets, np.uint64)
+        _b._check(self.L.ph0b_shard_scatter_peers(
+            self.h, parts, C.c_void_p(kd.ctypes.data), C.c_void_p(vd.ctypes.data),
+            C.c_void_p(off.ctypes.data), None))
+        self._count()
+
     def reduce(self, n, count, grade_offset):
         m, up, gp, lp = C.c_uint64(), C.c_void_p(), C.c_void_p(), C.c_void_p()
         _b._check(self.L.ph0b_shard_reduce(self.h, n, count, grade_offset, None, C.byref(m),
@@ -261,6 +320,17 @@ class DeviceBackend:
 
 
 # ---- the SPMD driver -------------------------------------------------------------------------
+def exchange_mode(comm, backend) -> str:
+    """'peer': one partition kernel stores every part straight into its destination rank's
+    receive buffer (peer memory over NVLink); 'collective': partition into a send buffer,
+    then all-to-all-v (NCCL).  PH0B_EXCHANGE=collective|peer overrides the default (peer
+    when the backend supports it)."""
+    import os
+    want = os.environ.get("PH0B_EXCHANGE", "peer")
+    ok = hasattr(backend, "scatter_peers") and hasattr(comm, "same_process")
+    return "peer" if want == "peer" and ok else "collective"
+
+
 def h0_barcode_sharded(x_ptr, n: int, d: int, comm, backend, layout=_b.COL_MAJOR) -> ShardResult:
     """Run on every rank (same X on every rank: it is <= 4 MiB, replicated)."""
     P, r = comm.size, comm.rank
@@ -269,7 +339,11 @@ def h0_barcode_sharded(x_ptr, n: int, d: int, comm, backend, layout=_b.COL_MAJOR
     if P > 1:
         samples = np.concatenate(comm.allgather_obj(backend.sample(SAMPLES_PER_RANK, count)))
         spl = choose_splitters(samples, P)
-        send_k, send_v, counts, pmin, pmax = backend.partition(spl, P)
+        peer = exchange_mode(comm, backend) == "peer"
+        if peer:
+            counts, pmin, pmax = backend.partition_count(spl, P)
+        else:
+            send_k, send_v, counts, pmin, pmax = backend.partition(spl, P)
         allc = np.array(comm.allgather_obj(counts), np.uint64)          # [src][dst]
         allmin = np.array(comm.allgather_obj(pmin), np.uint64)
         allmax = np.array(comm.allgather_obj(pmax), np.uint64)
@@ -278,9 +352,19 @@ def h0_barcode_sharded(x_ptr, n: int, d: int, comm, backend, layout=_b.COL_MAJOR
         have = recv_counts > 0
         kmin = int(allmin[have, r].min()) if have.any() else 0
         kmax = int(allmax[have, r].max()) if have.any() else 0
-        recv_k, recv_v = backend.recv(total)
-        comm.alltoallv(send_k, counts, recv_k, recv_counts)
-        comm.alltoallv(send_v, counts, recv_v, recv_counts)
+        if peer:
+            # every rank's receive buffer exists before anyone learns where it is; part b of
+            # this rank lands after the parts of lower ranks (source-rank order, as the
+            # all-to-all-v delivers it, so the received slice is u-major)
+            descs = comm.allgather_obj(backend.recv_peer(total, comm.same_process))
+            dst = [backend.open_peer(descs[b], b == r, comm.same_process) for b in range(P)]
+            offsets = [int(allc[:r, b].sum()) for b in range(P)]
+            backend.scatter_peers(P, dst, offsets)
+            comm.barrier()  # all stores into every receive buffer are complete
+        else:
+            recv_k, recv_v = backend.recv(total)
+            comm.alltoallv(send_k, counts, recv_k, recv_counts)
+            comm.alltoallv(send_v, counts, recv_v, recv_counts)
         count = total
     n_distinct, scale = backend.sort_unique(count, kmin, kmax)
     nds = comm.allgather_obj(int(n_distinct)) if P > 1 else [int(n_distinct)]

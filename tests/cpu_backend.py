@@ -68,13 +68,66 @@ class NumpyBackend:
         sv = torch.from_numpy(self.vals[order].view(np.int32).copy())
         return sk, sv, counts, pmin, pmax
 
+    # ---- peer-memory exchange, emulated with POSIX shared memory between rank processes
+    def partition_count(self, spl, parts):
+        self._part = np.searchsorted(np.asarray(spl, np.uint64), self.keys, side="right")
+        counts = np.bincount(self._part, minlength=parts).astype(np.uint64)
+        pmin = np.full(parts, np.iinfo(np.uint64).max, np.uint64)
+        pmax = np.zeros(parts, np.uint64)
+        for j in range(parts):
+            sel = self.keys[self._part == j]
+            if len(sel):
+                pmin[j], pmax[j] = sel.min(), sel.max()
+        return counts, pmin, pmax
+
+    def recv_peer(self, count, same_process):
+        from multiprocessing import shared_memory
+        self._own = [shared_memory.SharedMemory(create=True, size=max(8, 8 * count)),
+                     shared_memory.SharedMemory(create=True, size=max(4, 4 * count))]
+        self._count_recv = count
+        return (self._own[0].name, self._own[1].name)
+
+    def open_peer(self, desc, is_self, same_process):
+        from multiprocessing import resource_tracker, shared_memory
+        if is_self:
+            shms = self._own
+        else:
+            shms = [shared_memory.SharedMemory(name=nm) for nm in desc]
+            for m in shms:  # the owner unlinks it; this process only maps it
+                resource_tracker.unregister(m._name, "shared_memory")
+            self.__dict__.setdefault("_attached", []).extend(shms)
+        return (np.ndarray(shms[0].size // 8, np.uint64, buffer=shms[0].buf),
+                np.ndarray(shms[1].size // 4, np.uint32, buffer=shms[1].buf))
+
+    def scatter_peers(self, parts, dst, offsets):
+        order = np.argsort(self._part, kind="stable")
+        ks, vs, bs = self.keys[order], self.vals[order], self._part[order]
+        for b in range(parts):
+            sel = bs == b
+            c, o = int(sel.sum()), int(offsets[b])
+            dst[b][0][o:o + c] = ks[sel]
+            dst[b][1][o:o + c] = vs[sel]
+
+    def _take_peer_recv(self):
+        n = self._count_recv
+        self.keys = np.ndarray(n, np.uint64, buffer=self._own[0].buf).copy()
+        self.vals = np.ndarray(n, np.uint32, buffer=self._own[1].buf).copy()
+        for m in self.__dict__.pop("_attached", []):
+            m.close()
+        for m in self._own:
+            m.close()
+            m.unlink()
+        del self._own
+
     def recv(self, count):
         self.rk = torch.empty(count, dtype=torch.int64)
         self.rv = torch.empty(count, dtype=torch.int32)
         return self.rk, self.rv
 
     def sort_unique(self, count, kmin, kmax):
-        if hasattr(self, "rk"):
+        if hasattr(self, "_own"):
+            self._take_peer_recv()
+        elif hasattr(self, "rk"):
             self.keys = self.rk.numpy().view(np.uint64).copy()
             self.vals = self.rv.numpy().view(np.uint32).copy()
         order = np.argsort(self.keys, kind="stable")

@@ -21,10 +21,10 @@ def _free_port():
     return p
 
 
-def _worker(rank, world, port, X, out):
+def _worker(rank, world, port, X, out, exchange="peer"):
     sys.path.insert(0, str(ROOT))
     sys.path.insert(0, str(ROOT / "tests"))
-    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port), PH0B_EXCHANGE=exchange)
     import torch.distributed as dist
 
     from cpu_backend import NumpyBackend
@@ -39,11 +39,12 @@ def _worker(rank, world, port, X, out):
     dist.destroy_process_group()
 
 
-def run_world(X, world):
+def run_world(X, world, exchange="peer"):
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port = _free_port()
-    procs = [ctx.Process(target=_worker, args=(r, world, port, X, q)) for r in range(world)]
+    procs = [ctx.Process(target=_worker, args=(r, world, port, X, q, exchange))
+             for r in range(world)]
     for p in procs:
         p.start()
     res = sorted([q.get(timeout=300) for _ in range(world)], key=lambda t: t[0])
@@ -53,14 +54,18 @@ def run_world(X, world):
     return res
 
 
-@pytest.mark.parametrize("world", [2, 3])
-def test_sharded_orchestration_matches_oracle(world):
+@pytest.mark.parametrize("world,exchange", [(2, "peer"), (3, "peer"), (2, "collective"),
+                                            (3, "collective")])
+def test_sharded_orchestration_matches_oracle(world, exchange):
+    """exchange='peer': every rank stores its parts straight into the receive buffers of the
+    other ranks (shared memory here, NVLink P2P through CUDA IPC on GPUs); 'collective': send
+    buffer + all-to-all-v."""
     import oracle_bridge as ob
 
     rng = np.random.default_rng(world)
     X = np.vstack([rng.normal(0, 0.1, size=(60, 3)), rng.normal(3, 0.1, size=(50, 3)),
                    rng.integers(0, 4, size=(40, 3)).astype(np.float64)])  # clusters + ties
-    res = run_world(X, world)
+    res = run_world(X, world, exchange)
     ref = ob.oracle_filtration_and_bars(X)
     D = np.concatenate([r[2] for r in res])
     assert [r[1] for r in res] == list(np.cumsum([0] + [len(r[2]) for r in res])[:-1])

@@ -1,8 +1,8 @@
 """GPU: the sharded (multi-GPU) pipeline of sharded.py, run as P virtual ranks (threads, one
 ph0b context each) on the single B200 available to the tests: every stage kernel of the
-multi-rank path (row-range distances, splitter partition, received-slice sort/unique, local
-and final column reductions) is exercised; the transport is a device-to-device copy instead
-of NCCL.  Bit-exact D (concatenated slices) and ordered bars vs the oracle."""
+multi-rank path (row-range distances, splitter partition — including the scatter straight into
+the peers' receive buffers — received-slice sort/unique, local and final column reductions) is
+exercised; the collective transport is a device-to-device copy instead of NCCL.  Bit-exact D (concatenated slices) and ordered bars vs the oracle."""
 import threading
 
 import numpy as np
@@ -44,9 +44,14 @@ def run_virtual(X, parts):
     return out
 
 
+@pytest.mark.parametrize("exchange", ["peer", "collective"])
 @pytest.mark.parametrize("parts", [1, 2, 3, 4])
 @pytest.mark.parametrize("cloud", ["C2", "lattice", "C1"])
-def test_virtual_ranks_match_oracle(parts, cloud):
+def test_virtual_ranks_match_oracle(parts, cloud, exchange, monkeypatch):
+    """exchange='peer': the partition kernel of each virtual rank stores its parts straight
+    into the other ranks' receive buffers (the peer-memory path; here all on one device);
+    'collective': send buffer + all-to-all-v emulated by device copies."""
+    monkeypatch.setenv("PH0B_EXCHANGE", exchange)
     if cloud == "lattice":
         X = np.array([[x, y] for x in range(24) for y in range(24)], np.float64)
     elif cloud == "C2":
