@@ -187,14 +187,17 @@ def load_traffic():
 
 def run_sharded(args, cfg_name):
     """N > 1 (torchrun, one rank per GPU): the sharded pipeline of sharded.py — rows split
-    across ranks, splitter partition + one NCCL all-to-all-v, D sharded, local + final column
-    reductions.  Total work fixed as N grows (strong scaling of the C5 problem)."""
+    across ranks, splitter partition whose kernel stores each part straight into its
+    destination rank's receive buffer over NVLink (CUDA IPC; PH0B_EXCHANGE=collective: send
+    buffer + NCCL all-to-all-v instead), D sharded, local + final column reductions.  Total
+    work fixed as N grows (strong scaling of the C5 problem)."""
     import numpy as np
     import torch
     import torch.distributed as dist
 
     import paper_2203_02527_b200 as pkg
-    from paper_2203_02527_b200.sharded import DeviceBackend, TorchComm, h0_barcode_sharded
+    from paper_2203_02527_b200.sharded import (DeviceBackend, TorchComm, exchange_mode,
+                                               h0_barcode_sharded)
 
     ws, rank, local = dist_env()
     torch.cuda.set_device(local)
@@ -265,7 +268,8 @@ def run_sharded(args, cfg_name):
             "warmup": args.warmup, "ms_per_step": ms / args.steps, "higher_is_better": True,
             "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
             "config": {"workload": f"{cfg_name}: {WORKLOADS[cfg_name]}", "n": n, "d": d,
-                       "edges": k, "parallelism": f"dp{ws} (row shards + splitter all-to-all)",
+                       "edges": k, "parallelism": f"dp{ws} (row shards + splitter exchange)",
+                       "exchange": exchange_mode(comm, be),
                        "l2": "inputs larger than L2", "n_scale": res.n_scale_total,
                        "bars": int(len(res.death_grade))},
             "e2e": {"value": k * e2e_steps / (e2e_ms / 1e3), "unit": UNIT,
