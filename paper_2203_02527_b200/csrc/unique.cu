@@ -177,32 +177,53 @@ __global__ void __launch_bounds__(kUThreads, 3)
         } else if (low_bits) {
             // ---- fix the equal-prefix runs that start in this tile (stable, in smem) -----
             const uint64_t p_before = pre(k_before);
-            // run starts, branch-free: each thread checks its kUItems positions of the
-            // warp-interleaved layout (consecutive lanes read consecutive keys: no bank
-            // conflicts, all loads in flight), then handles only the rare starts
+            // Work is only needed where a run is out of order, and an out-of-order adjacent
+            // pair can only lie inside an equal-prefix run (pre() is monotone, the array is
+            // sorted by it): so the scan is one 64-bit compare per position (consecutive
+            // lanes read consecutive keys).  Each out-of-order run is claimed by the thread
+            // holding its first inversion, if the run starts in this tile; claims are made
+            // read-only, before any thread reorders anything.
+            // item j < kUItems: position wofs0 + 32 j of the tile; item kUItems: position
+            // kUT + tid of the extension (a run starting here may be out of order only there)
+            const uint32_t wofs0 = warp * (32 * kUItems) + lane;
+            auto item_pos = [&](uint32_t j) {
+                return j < (uint32_t)kUItems ? wofs0 + 32 * j : (uint32_t)kUT + tid;
+            };
             uint32_t starts = 0;
             {
-                const uint32_t wofs0 = warp * (32 * kUItems) + lane;
 #pragma unroll
-                for (int j = 0; j < kUItems; ++j) {
-                    const uint32_t i = wofs0 + 32 * j;
-                    const bool in = i < tn && i + 1 < staged;
-                    const uint64_t kc = in ? s_k[i] : 0ull;
-                    const uint64_t kn = in ? s_k[i + 1] : 0ull;
-                    const uint64_t kp = in && i > 0 ? s_k[i - 1] : 0ull;
-                    const uint64_t p = pre(kc);
-                    const bool has_prev = i > 0 || tile_start > 0;
-                    const uint64_t pp = i > 0 ? pre(kp) : p_before;
-                    const bool st = in && pre(kn) == p && !(has_prev && pp == p);
-                    starts |= st ? (1u << j) : 0u;
+                for (int j = 0; j <= kUItems; ++j) {
+                    const uint32_t i = item_pos(j);
+                    const bool in = i > 0 && i < staged;
+                    const bool inv = in && s_k[i] < s_k[i - 1];
+                    starts |= inv ? (1u << j) : 0u;
                 }
+                uint32_t claims = 0;
+                while (starts) {
+                    const uint32_t j = (uint32_t)(__ffs(starts) - 1);
+                    starts &= starts - 1;
+                    const uint32_t i = item_pos(j);
+                    const uint64_t p = pre(s_k[i]);
+                    uint32_t st = i - 1;  // run start within the staged window
+                    bool first = true;
+                    while (st > 0 && pre(s_k[st - 1]) == p) {
+                        first = first && !(s_k[st] < s_k[st - 1]);
+                        --st;
+                    }
+                    const bool from_prev = st == 0 && tile_start > 0 && p == p_before;
+                    if (first && !from_prev && st < tn) claims |= 1u << j;
+                }
+                starts = claims;
             }
+            __syncthreads();  // every claim is made before any run is reordered
             while (starts) {
                 const uint32_t j = (uint32_t)(__ffs(starts) - 1);
                 starts &= starts - 1;
-                const uint32_t i = warp * (32 * kUItems) + lane + 32 * j;
+                const uint32_t inv = item_pos(j);
+                const uint64_t p = pre(s_k[inv]);
+                uint32_t i = inv - 1;  // prefixes never change: safe to re-walk while others fix
+                while (i > 0 && pre(s_k[i - 1]) == p) --i;
                 const uint64_t g = tile_start + i;
-                const uint64_t p = pre(s_k[i]);
                 uint32_t len = 2;
                 while (i + len < staged && len <= kMaxRun && pre(s_k[i + len]) == p) ++len;
                 if (len > kMaxRun || (i + len == staged && ext_end < count)) {
@@ -243,6 +264,9 @@ __global__ void __launch_bounds__(kUThreads, 3)
                     const uint64_t pl = pre(s_k[e - 1]);
                     while (e < staged && pre(s_k[e]) == pl) ++e;
                 }
+                // this tile's last run runs past the staged window: its end (and the next
+                // tile's first owned position) is not visible here — sorted or not, redo
+                if (st < tn && e == staged && ext_end < count) atomicOr(redo, 1u);
                 if (st >= tn) st = e = tn;
                 uint32_t ext = 0;
                 for (uint32_t g = tn; g < e; ++g) ext += s_k[g] != s_k[g - 1] ? 1u : 0u;
