@@ -143,6 +143,9 @@ __global__ void __launch_bounds__(kUThreads, 3)
     };
     uint32_t tile = blockIdx.x;
     if (tid == 0 && tile < num_tiles) issue(tile, 0);
+    // the key before each tile is loaded one tile ahead (its latency hides behind a tile)
+    uint64_t k_before_next =
+        tile < num_tiles && tile > 0 ? keys[(uint64_t)tile * kUT - 1] : 0ull;
     const uint64_t base0 = d_base ? *d_base : 0ull;  // D index of this range's first length
     uint32_t phase[2] = {0, 0};
     int b = 0;
@@ -167,7 +170,12 @@ __global__ void __launch_bounds__(kUThreads, 3)
         __syncthreads();  // everyone is done with the other buffer: prefetch into it
         const uint32_t next = tile + gridDim.x;
         if (tid == 0 && next < num_tiles) issue(next, b ^ 1);
-        const uint64_t k_before = tile_start > 0 ? keys[tile_start - 1] : 0ull;
+        const uint64_t k_before = k_before_next;
+        // (run fix-ups of earlier tiles may rewrite keys[next*kUT - 1] — only in order
+        // within an equal-prefix run, and only the prefix of k_before is used for run
+        // bookkeeping; its exact value matters for the first flag only when the run
+        // fix-ups are off, i.e. when nothing rewrites it)
+        if (next < num_tiles) k_before_next = keys[(uint64_t)next * kUT - 1];
 
         uint32_t os = 0, oe = tn;
         if (kMode == 2) {
