@@ -250,6 +250,13 @@ int ph0b_generate_uniform_cloud_device(ph0b_context* ctx, uint64_t n, uint64_t d
  * Writes out[0..n).  Exposed for callers that move D between processes the same way. */
 int ph0b_decode_deltas(const uint32_t* deltas, const uint64_t* bases, const uint8_t* raw,
                        uint64_t n, uint32_t chunk, uint64_t* out);
+/* The packed stream ph0b_run_host ships D in (d2h_codec.cu): chunks of `chunk` values (1024
+ * on the host path), chunk j = bases[j] followed by deltas of widths[j] bytes each (3 or 4,
+ * little-endian, the first one unused) at packed + offs[j]; widths[j] == 0: the chunk was
+ * shipped raw and is skipped.  `packed` must have 8 readable bytes past the last chunk's
+ * data.  Writes out[0..n). */
+int ph0b_decode_packed(const uint8_t* packed, const uint64_t* bases, const uint8_t* widths,
+                       const uint32_t* offs, uint64_t n, uint32_t chunk, uint64_t* out);
 
 int ph0b_generate_cloud(uint32_t kind, uint64_t n, uint64_t d, uint64_t seed, uint32_t clusters,
                         double sigma, double lo, double hi, uint64_t n_background,

@@ -224,6 +224,23 @@ int ph0b_decode_deltas(const uint32_t* deltas, const uint64_t* bases, const uint
     return PH0B_OK;
 }
 
+int ph0b_decode_packed(const uint8_t* packed, const uint64_t* bases, const uint8_t* widths,
+                       const uint32_t* offs, uint64_t n, uint32_t chunk, uint64_t* out) {
+    if (n == 0) return PH0B_OK;
+    if (!packed || !bases || !widths || !offs || !out || chunk == 0)
+        return fail(PH0B_ERR_INVALID_ARGUMENT, "null argument or zero chunk");
+    const uint64_t nch = (n + chunk - 1) / chunk;
+    for (uint64_t j = 0; j < nch; ++j)
+        if (widths[j] != 0 && widths[j] != 3 && widths[j] != 4)
+            return fail(PH0B_ERR_INVALID_ARGUMENT, "chunk width must be 0, 3 or 4");
+    ph0b::DecodeTask t{nullptr, bases, nullptr, out, n, chunk};
+    t.widths = widths;
+    t.poff = offs;
+    t.packed = packed;
+    ph0b::decode_chunk(t);
+    return PH0B_OK;
+}
+
 int ph0b_run_host(ph0b_context* ctx, const double* X, uint64_t n, uint64_t d, uint32_t layout,
                   void* stream, uint64_t* death_grade, double* death_length, uint64_t* n_finite,
                   uint64_t* essential_count, double* scale, uint64_t scale_capacity,

@@ -9,6 +9,7 @@
 #include <algorithm>
 #include <atomic>
 #include <chrono>
+#include <cstring>
 
 namespace ph0b {
 
@@ -85,6 +86,62 @@ __attribute__((target("avx512f"))) void decode_avx512(const Chunk& t) {
     _mm_sfence();
 }
 
+// 3-byte deltas (packed chunks): 8 per step, widened to 32-bit lanes with one byte permute,
+// then the same prefix sum as decode_avx512.  Reads up to 8 bytes past the chunk's data
+// (the ring slots carry slack).
+inline uint32_t load24(const uint8_t* p) {
+    uint32_t x;
+    std::memcpy(&x, p, 4);
+    return x & 0xFFFFFFu;
+}
+
+__attribute__((target("avx512f,avx512vl,avx512vbmi"))) void decode3_avx512(const uint8_t* d,
+                                                                           uint64_t base,
+                                                                           uint64_t* out,
+                                                                           uint32_t len) {
+    uint64_t acc = base;
+    out[0] = acc;
+    uint32_t i = 1;
+    while (i < len && (reinterpret_cast<uintptr_t>(out + i) & 63u)) {
+        acc += load24(d + 3 * i);
+        out[i++] = acc;
+    }
+    if (i + 8 <= len) {
+        const __m512i z = _mm512_setzero_si512();
+        const __m512i last = _mm512_set1_epi64(7);
+        const __m256i idx = _mm256_setr_epi8(0, 1, 2, 0, 3, 4, 5, 0, 6, 7, 8, 0, 9, 10, 11, 0, 12,
+                                             13, 14, 0, 15, 16, 17, 0, 18, 19, 20, 0, 21, 22, 23, 0);
+        const __m256i m24 = _mm256_set1_epi32(0xFFFFFF);
+        __m512i run = _mm512_set1_epi64((long long)acc);
+        for (; i + 8 <= len; i += 8) {
+            const __m256i raw = _mm256_loadu_si256(reinterpret_cast<const __m256i*>(d + 3 * i));
+            const __m256i x32 = _mm256_and_si256(_mm256_permutexvar_epi8(idx, raw), m24);
+            __m512i x = _mm512_cvtepu32_epi64(x32);
+            x = _mm512_add_epi64(x, _mm512_alignr_epi64(x, z, 7));
+            x = _mm512_add_epi64(x, _mm512_alignr_epi64(x, z, 6));
+            x = _mm512_add_epi64(x, _mm512_alignr_epi64(x, z, 4));
+            x = _mm512_add_epi64(x, run);
+            run = _mm512_permutexvar_epi64(last, x);
+            _mm512_stream_si512(reinterpret_cast<__m512i*>(out + i), x);
+        }
+        acc = (uint64_t)_mm_cvtsi128_si64(_mm512_castsi512_si128(run));
+    }
+    for (; i < len; ++i) {
+        acc += load24(d + 3 * i);
+        out[i] = acc;
+    }
+    _mm_sfence();
+}
+
+void decode3_scalar(const uint8_t* d, uint64_t base, uint64_t* out, uint32_t len) {
+    uint64_t acc = base;
+    out[0] = acc;
+    for (uint32_t i = 1; i < len; ++i) {
+        acc += load24(d + 3 * i);
+        out[i] = acc;
+    }
+}
+
 void decode_scalar(const Chunk& t) {
     uint64_t acc = t.base;
     t.out[0] = acc;
@@ -98,6 +155,31 @@ void decode_scalar(const Chunk& t) {
 
 void decode_chunk(const DecodeTask& t) {
     static const int isa = __builtin_cpu_supports("avx512f") ? 2 : __builtin_cpu_supports("avx2") ? 1 : 0;
+    static const bool vbmi = __builtin_cpu_supports("avx512vbmi") &&
+                             __builtin_cpu_supports("avx512vl");
+    if (t.widths) {  // packed chunks
+        for (uint64_t j = 0, s0 = 0; s0 < t.n; ++j, s0 += t.chunk) {
+            const uint32_t w = t.widths[j];
+            if (w == 0) continue;
+            const uint32_t len = (uint32_t)(t.n - s0 < t.chunk ? t.n - s0 : t.chunk);
+            const uint8_t* src = t.packed + t.poff[j];
+            if (w == 3) {
+                if (vbmi)
+                    decode3_avx512(src, t.bases[j], t.out + s0, len);
+                else
+                    decode3_scalar(src, t.bases[j], t.out + s0, len);
+                continue;
+            }
+            const Chunk c{reinterpret_cast<const uint32_t*>(src), t.bases[j], t.out + s0, len};
+            if (isa == 2)
+                decode_avx512(c);
+            else if (isa == 1)
+                decode_avx2(c);
+            else
+                decode_scalar(c);
+        }
+        return;
+    }
     for (uint64_t j = 0, s0 = 0; s0 < t.n; ++j, s0 += t.chunk) {
         if (t.raw[j]) continue;
         const Chunk c{t.deltas + s0, t.bases[j], t.out + s0,

@@ -41,6 +41,11 @@ struct DecodeTask {
     // completion counter reaches gen * nsub when the last one finishes, which frees the slot
     std::atomic<uint64_t>* done = nullptr;
     uint32_t nsub = 1;
+    // packed chunks (widths != null): chunk j's deltas are widths[j] bytes each (3 or 4; 0 =
+    // raw, skipped) at packed + poff[j]; `deltas` and `raw` are unused
+    const uint8_t* widths = nullptr;
+    const uint32_t* poff = nullptr;
+    const uint8_t* packed = nullptr;
 };
 
 class DecodePool {

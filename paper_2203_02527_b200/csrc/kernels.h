@@ -109,12 +109,16 @@ int run_reduction(ReduceState& st, cudaStream_t s, int num_sms, uint32_t& epoch,
                   ReduceStats* stats);
 
 // ---- K9: compressed D for the host path (d2h_codec.cu) ----------------------------------
-constexpr int kD2HChunk = 4096;  // values per chunk: one u64 base + u32 deltas
-// Same, for the slice [lohi[0], lohi[1]) of d given by device words; n_upper >= its length.
-int launch_d2h_encode_bucket(const double* d, const uint64_t* lohi, uint64_t n_upper,
-                             uint32_t* deltas, uint64_t* bases, uint8_t* raw, cudaStream_t s);
-int launch_d2h_encode(const double* d, uint64_t n, uint32_t* deltas, uint64_t* bases,
-                      uint8_t* raw, cudaStream_t s);
+// Packed stream of the slice [lohi[0], lohi[1]) of d (device words; n_upper >= its length):
+// kPackChunk-value chunks of 3- or 4-byte deltas (width 0 = raw: not in the stream), the
+// chunks' bases, widths, absolute byte offsets (device) and offsets within their piece of
+// piece_chunks chunks; piece_off[p] = byte offset of piece p, piece_off[#pieces] = total
+// (mapped host memory: the host sizes the copies from it).  Returns launches.
+constexpr int kPackChunk = 1024;
+int launch_d2h_pack_bucket(const double* d, const uint64_t* lohi, uint64_t n_upper,
+                           uint64_t* bases, uint8_t* widths, uint64_t* offs, uint32_t* poff,
+                           uint64_t* piece_off, uint32_t piece_chunks, uint8_t* out,
+                           cudaStream_t s);
 
 // ---- K8: on-device generate_uniform_cloud (generate.cu) --------------------------------
 // returns launches (>0), -1 on a CUDA error, -2 if more than 64 zero draws were met

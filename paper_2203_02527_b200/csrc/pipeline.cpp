@@ -107,18 +107,22 @@ uint64_t d2h_chunk_elems() {
 }
 
 // Streamed D2H ring of the compressed host path: PH0B_RING_SLOTS slots (default 6) of
-// PH0B_RING_CHUNKS 4096-value chunks (u32 deltas: 8 MiB at the default 512), filled on
+// PH0B_RING_CHUNKS 1024-value packed chunks (<= 8 MiB at the default 2048), filled on
 // PH0B_RING_STREAMS copy streams (default 2) and decoded by PH0B_RING_SUBTASKS pool tasks
 // per piece (default 32).  8 MiB copies keep the per-copy and stream-memop overheads below
 // 5 % of the PCIe time (tools/ring_bench.cu); the 48 MiB ring replaces a k*4-byte pinned
 // staging buffer (8.6 GB at C5).  Measured sweep: tools/ring_sweep.sh, DESIGN.md.
-uint32_t ring_piece_chunks() {
+uint32_t ring_piece_chunks() {  // 1024-value packed chunks per piece
     static const uint32_t v = [] {
         const char* e = getenv("PH0B_RING_CHUNKS");
-        const int x = e ? atoi(e) : 512;
-        return (uint32_t)(x < 1 ? 1 : (x > 4096 ? 4096 : x));
+        const int x = e ? atoi(e) : 2048;
+        return (uint32_t)(x < 1 ? 1 : (x > 16384 ? 16384 : x));
     }();
     return v;
+}
+
+uint64_t ring_slot_bytes() {  // a piece at 4 bytes per value + slack for the decoder's reads
+    return (uint64_t)ring_piece_chunks() * kPackChunk * 4 + 128;
 }
 
 uint32_t ring_subtasks() {
@@ -189,8 +193,11 @@ Context::~Context() {
     for (void* p : ps)
         if (p) cudaFree(p);
     pool_.reset();
-    for (void* p : {(void*)h_ring_, (void*)h_ringflags_, (void*)h_cbase_, (void*)h_craw_})
+    for (void* p : {(void*)h_ring_, (void*)h_ringflags_, (void*)h_cbase_, (void*)h_craw_,
+                    (void*)h_cpoff_, (void*)h_pieceoff_})
         if (p) cudaFreeHost(p);
+    for (void* p : {(void*)d_coff_, (void*)d_cpoff_})
+        if (p) cudaFree(p);
     if (enc_ev_) cudaEventDestroy(enc_ev_);
     for (auto& e : bucket_ev_)
         if (e) cudaEventDestroy(e);
@@ -238,7 +245,7 @@ Status Context::init() {
 }
 
 Status Context::ensure_ring() {
-    const uint64_t need = (uint64_t)ring_slots() * ring_piece_chunks() * kD2HChunk * 4;
+    const uint64_t need = (uint64_t)ring_slots() * ring_slot_bytes();
     Status s = grow_host(reinterpret_cast<void**>(&h_ring_), &h_ring_cap_, need);
     if (!s.good()) return s;
     if (!h_ringflags_) {
@@ -673,16 +680,32 @@ Status Context::run_host_overlapped(const double* X, uint64_t n, uint64_t d, uin
                                 "cudaStreamCreate");
     const bool compress = host_scale && d2h_compress();
     if (compress) {
-        // per bucket, a chunk-aligned area sized by its edge count (>= its |D|)
-        const uint64_t chunks = k / kD2HChunk + B + 64;
-        if (!(s = grow(reinterpret_cast<void**>(&d_delta_), &d_delta_cap_, chunks * kD2HChunk * 4))
-                 .good() ||
+        // per bucket, a chunk-aligned area sized by its edge count (>= its |D|): packed bytes
+        // (<= 4 per value + slack), chunk bases, widths, offsets (device) and offsets within
+        // a piece; pinned mirrors of the per-chunk metadata; mapped piece boundaries
+        const uint64_t chunks = k / kPackChunk + B + 64;
+        const uint64_t pieces = chunks / ring_piece_chunks() + B + 2;
+        if (!(s = grow(reinterpret_cast<void**>(&d_delta_), &d_delta_cap_,
+                       chunks * kPackChunk * 4 + 64 * B)).good() ||
             !(s = grow(reinterpret_cast<void**>(&d_cbase_), &d_cbase_cap_, chunks * 8)).good() ||
             !(s = grow(reinterpret_cast<void**>(&d_craw_), &d_craw_cap_, chunks)).good() ||
+            !(s = grow(reinterpret_cast<void**>(&d_coff_), &d_coff_cap_, chunks * 8)).good() ||
+            !(s = grow(reinterpret_cast<void**>(&d_cpoff_), &d_cpoff_cap_, chunks * 4)).good() ||
             !(s = grow_host(reinterpret_cast<void**>(&h_cbase_), &h_cbase_cap_, chunks * 8)).good() ||
             !(s = grow_host(reinterpret_cast<void**>(&h_craw_), &h_craw_cap_, chunks)).good() ||
+            !(s = grow_host(reinterpret_cast<void**>(&h_cpoff_), &h_cpoff_cap_, chunks * 4)).good() ||
             !(s = ensure_ring()).good())
             return s;
+        if (pieces > h_pieceoff_cap_) {
+            if (h_pieceoff_) cudaFreeHost(h_pieceoff_);
+            h_pieceoff_ = nullptr;
+            h_pieceoff_cap_ = 0;
+            PH0B_TRY(cudaHostAlloc(&h_pieceoff_, pieces * 8, cudaHostAllocMapped),
+                     "cudaHostAlloc mapped");
+            PH0B_TRY(cudaHostGetDevicePointer(reinterpret_cast<void**>(&d_pieceoff_), h_pieceoff_,
+                                              0), "cudaHostGetDevicePointer");
+            h_pieceoff_cap_ = pieces;
+        }
         if (bucket_ev_.size() < B) {
             bucket_ev_.resize(B, nullptr);
             for (auto& e : bucket_ev_)
@@ -780,76 +803,94 @@ Status Context::run_host_overlapped(const double* X, uint64_t n, uint64_t d, uin
     const uint32_t G = ring_piece_chunks();
     const uint32_t R = ring_slots();
     const uint32_t NS = ring_subtasks();
-    std::vector<uint64_t> nch_ub(B), cb(B + 1, 0);
+    std::vector<uint64_t> nch_ub(B), cb(B + 1, 0), rb(B + 1, 0);
     for (uint32_t b = 0; b < B; ++b) {
-        nch_ub[b] = (tot[b] + kD2HChunk - 1) / kD2HChunk;
+        nch_ub[b] = (tot[b] + kPackChunk - 1) / kPackChunk;
         cb[b + 1] = cb[b] + nch_ub[b];
+        rb[b + 1] = rb[b] + nch_ub[b] * kPackChunk * 4 + 64;  // packed bytes + store slack
     }
     uint64_t d2h_total = 0;  // bytes moved device -> host by this call
     uint64_t enq_ns = 0;     // host time spent enqueuing the pieces (trace)
     std::vector<uint32_t> pending;  // buckets whose raw chunks are not shipped yet
     uint64_t* d_lohi = part_small_ + 2304;  // [2B] device copy of each bucket's D bounds
+    uint8_t* d_pack = reinterpret_cast<uint8_t*>(d_delta_);
     auto encode = [&](uint32_t b) -> Status {
         if (!compress || tot[b] == 0) return Status::ok();
         PH0B_TRY(cudaMemcpyAsync(d_lohi + 2 * b, d_base + b, 16, cudaMemcpyDefault, st), "copy");
-        launches += launch_d2h_encode_bucket(dbuf_, d_lohi + 2 * b, tot[b],
-                                             d_delta_ + cb[b] * kD2HChunk, d_cbase_ + cb[b],
-                                             d_craw_ + cb[b], st);
+        launches += launch_d2h_pack_bucket(dbuf_, d_lohi + 2 * b, tot[b], d_cbase_ + cb[b],
+                                           d_craw_ + cb[b], d_coff_ + cb[b], d_cpoff_ + cb[b],
+                                           d_pieceoff_, G, d_pack + rb[b], st);
         PH0B_CHECK_LAUNCH("D2H encode");
         PH0B_TRY(cudaEventRecord(enc_ev_, st), "event");
         return Status::ok();
     };
-    // after encode(b): chunk bases + raw flags, then the pieces through the ring
+    // after encode(b) (the last one enqueued): per-chunk metadata, then the packed pieces
+    // through the ring, each copy sized by the piece boundaries the encoder published
     auto stream_out = [&](uint32_t b) -> Status {
         if (!compress || tot[b] == 0) return Status::ok();
+        PH0B_TRY(cudaEventSynchronize(enc_ev_), "D2H encode");
+        const uint64_t nb = h_base[b + 1] - h_base[b];
+        const uint64_t nch = (nb + kPackChunk - 1) / kPackChunk;
+        if (nch == 0) return Status::ok();
+        const uint64_t npieces = (nch + G - 1) / G;
+        std::vector<uint64_t> poffs(npieces + 1);
+        for (uint64_t p = 0; p <= npieces; ++p) poffs[p] = h_pieceoff_[p];
         cudaStream_t cs = copy_stream_;
-        const uint64_t nch = nch_ub[b];
         PH0B_TRY(cudaStreamWaitEvent(cs, enc_ev_, 0), "wait");
         PH0B_TRY(cudaMemcpyAsync(h_cbase_ + cb[b], d_cbase_ + cb[b], nch * 8,
                                  cudaMemcpyDeviceToHost, cs), "D2H bases");
         PH0B_TRY(cudaMemcpyAsync(h_craw_ + cb[b], d_craw_ + cb[b], nch, cudaMemcpyDeviceToHost,
-                                 cs), "D2H flags");
+                                 cs), "D2H widths");
+        PH0B_TRY(cudaMemcpyAsync(h_cpoff_ + cb[b], d_cpoff_ + cb[b], nch * 4,
+                                 cudaMemcpyDeviceToHost, cs), "D2H offsets");
         PH0B_TRY(cudaEventRecord(bucket_ev_[b], cs), "event");
-        // extra ring streams: their pieces must not land before the bases and flags
+        // extra ring streams: their pieces must not land before the chunk metadata
         for (size_t i = 1; i < ring_streams_.size(); ++i)
             PH0B_TRY(cudaStreamWaitEvent(ring_streams_[i], bucket_ev_[b], 0), "wait");
-        d2h_total += nch * 9;
-        // each piece's task is handed to the pool right after its copy is enqueued: when the
-        // copy stream's queue is full, the enqueue blocks until earlier pieces are decoded
+        d2h_total += nch * 13;
+        // each piece's tasks are handed to the pool right after its copy is enqueued: when
+        // the copy stream's queue is full, the enqueue blocks until earlier pieces are decoded
         std::vector<DecodeTask> task;
-        for (uint64_t j0 = 0; j0 < nch; j0 += G) {
+        for (uint64_t p = 0; p < npieces; ++p) {
+            const uint64_t j0 = p * G;
             const uint64_t pc = std::min<uint64_t>(G, nch - j0);
+            const uint64_t bytes = poffs[p + 1] - poffs[p];
             cs = ring_streams_[ring_seq_ % ring_streams_.size()];
             const uint32_t slot = (uint32_t)(ring_seq_ % R);
             const uint32_t gen = (uint32_t)(ring_seq_ / R + 1);
             ++ring_seq_;
-            uint32_t* ring = h_ring_ + (uint64_t)slot * G * kD2HChunk;
+            uint8_t* ring = reinterpret_cast<uint8_t*>(h_ring_) + (uint64_t)slot * ring_slot_bytes();
             const uint64_t dready = reinterpret_cast<uint64_t>(d_ringflags_ + slot);
             const uint64_t dfreed = reinterpret_cast<uint64_t>(d_ringflags_ + R + slot);
             const auto e0 = std::chrono::steady_clock::now();
             if (!stream_wait_u32(cs, dfreed, gen - 1))
                 return {PH0B_ERR_CUDA, "D2H ring: stream wait failed"};
-            PH0B_TRY(cudaMemcpyAsync(ring, d_delta_ + (cb[b] + j0) * kD2HChunk,
-                                     pc * kD2HChunk * 4, cudaMemcpyDeviceToHost, cs), "D2H deltas");
+            if (bytes)
+                PH0B_TRY(cudaMemcpyAsync(ring, d_pack + rb[b] + poffs[p], bytes,
+                                         cudaMemcpyDeviceToHost, cs), "D2H packed D");
             if (!stream_write_u32(cs, dready, gen))
                 return {PH0B_ERR_CUDA, "D2H ring: stream write failed"};
             enq_ns += std::chrono::duration_cast<std::chrono::nanoseconds>(
                           std::chrono::steady_clock::now() - e0).count();
-            d2h_total += pc * kD2HChunk * 4;
+            d2h_total += bytes;
             // the piece is decoded by NS tasks of G/NS chunks (empty past the piece's end)
             task.clear();
             const uint64_t per = (G + NS - 1) / NS;
             for (uint32_t i = 0; i < NS; ++i) {
                 const uint64_t c0 = std::min<uint64_t>(pc, i * per);
                 const uint64_t c1 = std::min<uint64_t>(pc, c0 + per);
-                DecodeTask t{ring + c0 * kD2HChunk, h_cbase_ + cb[b] + j0 + c0,
-                             h_craw_ + cb[b] + j0 + c0, reinterpret_cast<uint64_t*>(host_scale),
-                             (c1 - c0) * kD2HChunk, (uint32_t)kD2HChunk};
+                const uint64_t c = cb[b] + j0 + c0;
+                DecodeTask t{nullptr, h_cbase_ + c, nullptr,
+                             reinterpret_cast<uint64_t*>(host_scale), (c1 - c0) * kPackChunk,
+                             (uint32_t)kPackChunk};
+                t.widths = h_craw_ + c;
+                t.poff = h_cpoff_ + c;
+                t.packed = ring;
                 t.ready = h_ringflags_ + slot;
                 t.freed = h_ringflags_ + R + slot;
                 t.gen = gen;
                 t.bounds = h_base + b;
-                t.v0 = (j0 + c0) * kD2HChunk;
+                t.v0 = (j0 + c0) * kPackChunk;
                 t.capacity = scale_capacity;
                 t.overflow = &overflow;
                 t.done = &ring_done_[slot];
@@ -861,7 +902,7 @@ Status Context::run_host_overlapped(const double* X, uint64_t n, uint64_t d, uin
         pending.push_back(b);
         return Status::ok();
     };
-    // raw chunks (a delta did not fit in 32 bits) of buckets whose flags have landed
+    // raw chunks (a delta did not fit in 32 bits) of buckets whose metadata has landed
     auto drain = [&](bool wait) -> Status {
         while (!pending.empty()) {
             const uint32_t b = pending.front();
@@ -871,10 +912,10 @@ Status Context::run_host_overlapped(const double* X, uint64_t n, uint64_t d, uin
             }
             PH0B_TRY(cudaEventSynchronize(bucket_ev_[b]), "D2H bucket");
             const uint64_t lo = h_base[b], nb = h_base[b + 1] - lo;
-            for (uint64_t j = 0; j * kD2HChunk < nb; ++j) {
-                if (!h_craw_[cb[b] + j]) continue;
-                const uint64_t s0 = lo + j * kD2HChunk;
-                const uint64_t len = std::min<uint64_t>(kD2HChunk, lo + nb - s0);
+            for (uint64_t j = 0; j * kPackChunk < nb; ++j) {
+                if (h_craw_[cb[b] + j]) continue;
+                const uint64_t s0 = lo + j * kPackChunk;
+                const uint64_t len = std::min<uint64_t>(kPackChunk, lo + nb - s0);
                 if (s0 + len > scale_capacity) {
                     overflow = 1;
                     continue;

@@ -156,6 +156,11 @@ private:
     std::vector<cudaStream_t> ring_streams_;  // [0] = copy_stream_
     Status ensure_ring();
     uint64_t* h_cbase_ = nullptr;  uint64_t h_cbase_cap_ = 0;
+    uint64_t* d_coff_ = nullptr;   uint64_t d_coff_cap_ = 0;    // packed: chunk byte offsets
+    uint32_t* d_cpoff_ = nullptr;  uint64_t d_cpoff_cap_ = 0;   // packed: offsets in the piece
+    uint32_t* h_cpoff_ = nullptr;  uint64_t h_cpoff_cap_ = 0;
+    uint64_t* h_pieceoff_ = nullptr;  uint64_t* d_pieceoff_ = nullptr;  // mapped
+    uint64_t h_pieceoff_cap_ = 0;
     uint8_t* h_craw_ = nullptr;    uint64_t h_craw_cap_ = 0;
     std::unique_ptr<DecodePool> pool_;
     std::vector<cudaEvent_t> bucket_ev_;

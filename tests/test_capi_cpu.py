@@ -97,3 +97,65 @@ def test_host_delta_decoder_roundtrip():
             else:
                 assert np.array_equal(out[s:e], seq[s:e]), (n, chunk, off, j)
         assert np.all(buf[:off] == 0xDEADBEEF) and np.all(buf[off + n:] == 0xDEADBEEF)
+
+
+def _pack_stream(seq, chunk, rng):
+    """numpy restatement of the device encoder (d2h_codec.cu k9p_*): per chunk the narrowest
+    of 3 / 4 bytes holding every delta (0 = raw), chunks concatenated."""
+    n = len(seq)
+    nch = (n + chunk - 1) // chunk
+    bases = seq[::chunk].copy()
+    widths = np.zeros(nch, np.uint8)
+    offs = np.zeros(nch, np.uint32)
+    parts = []
+    pos = 0
+    for j in range(nch):
+        s, e = j * chunk, min(n, (j + 1) * chunk)
+        d = np.zeros(e - s, np.uint64)
+        d[1:] = seq[s + 1:e] - seq[s:e - 1]
+        mx = int(d.max()) if len(d) else 0
+        w = 0 if mx >> 32 else (4 if mx >> 24 else 3)
+        widths[j], offs[j] = w, pos
+        if w:
+            b = d.astype("<u4").view(np.uint8).reshape(-1, 4)[:, :w].ravel()
+            parts.append(b)
+            pos += len(b)
+    stream = np.concatenate(parts + [np.zeros(16, np.uint8)])  # + the 8-byte read slack
+    return stream, bases, widths, offs
+
+
+def test_host_packed_decoder_roundtrip():
+    """The host half of the streamed D2H (ph0b_decode_packed): 1024-value chunks of 3- or
+    4-byte deltas (or raw) decode back to the exact bit patterns, at any output alignment."""
+    import ctypes as C
+    rng = np.random.default_rng(11)
+    L = pkg.lib()
+    for n, chunk, off in ((1, 1024, 0), (3000, 1024, 1), (20000, 1024, 3), (1024 * 5, 1024, 0),
+                          (777, 256, 2)):
+        # gap sizes vary by chunk: some fit 24 bits, some 32, one chunk has a >= 2^32 gap
+        hi = np.where((np.arange(n) // chunk) % 3 == 0, 1 << 23, 1 << 31).astype(np.uint64)
+        gaps = (rng.random(n) * hi).astype(np.uint64) + np.uint64(1)
+        if n > 2 * chunk:
+            gaps[2 * chunk + 5] = np.uint64(1 << 40)  # chunk 2 goes raw
+        seq = np.cumsum(gaps, dtype=np.uint64) + np.uint64(0x3F00000000000000)
+        stream, bases, widths, offs = _pack_stream(seq, chunk, rng)
+        assert set(widths.tolist()) <= {0, 3, 4}
+        buf = np.full(n + 8, 0xDEADBEEF, np.uint64)
+        out = buf[off:off + n]
+        rc = L.ph0b_decode_packed(C.c_void_p(stream.ctypes.data), C.c_void_p(bases.ctypes.data),
+                                  C.c_void_p(widths.ctypes.data), C.c_void_p(offs.ctypes.data),
+                                  n, chunk, C.c_void_p(out.ctypes.data))
+        assert rc == 0
+        for j in range(len(widths)):
+            s, e = j * chunk, min(n, (j + 1) * chunk)
+            if widths[j] == 0:
+                assert np.all(out[s:e] == 0xDEADBEEF)
+            else:
+                assert np.array_equal(out[s:e], seq[s:e]), (n, chunk, off, j, widths[j])
+        assert np.all(buf[:off] == 0xDEADBEEF) and np.all(buf[off + n:] == 0xDEADBEEF)
+    bad = np.array([5], np.uint8)
+    one = np.zeros(1, np.uint64)
+    rc = L.ph0b_decode_packed(C.c_void_p(one.ctypes.data), C.c_void_p(one.ctypes.data),
+                              C.c_void_p(bad.ctypes.data), C.c_void_p(one.ctypes.data), 1, 1024,
+                              C.c_void_p(one.ctypes.data))
+    assert rc == pkg.ph0b.PH0B_ERR_INVALID_ARGUMENT
