@@ -414,7 +414,7 @@ def main():
     e2e_value = ws * k * e2e_steps / (e2e_ms / 1e3)
     h2d = n * d * 8
     # bytes actually moved device -> host per step, as counted by the library (D goes out
-    # delta-encoded: a u64 base + u32 deltas per 4096-value chunk; bars 16 B each)
+    # delta-encoded: a u64 base + 3- or 4-byte deltas per 1024-value chunk; bars 16 B each)
     d2h = int(_t.get("d2h_bytes", 0)) or (ns_ * 8 + nf * 16)
     e2e_check = {
         "bars_equal_device_path": bool(nf == n_finite and

@@ -82,7 +82,7 @@ typedef struct ph0b_stage_times {
     float sort_passes_ms;     /* the radix passes alone (sort_ms minus the digit histogram) */
     uint32_t reserved0;
     uint64_t d2h_bytes;       /* host-output calls: bytes actually moved device -> host
-                                 (D is shipped delta-encoded: ~4 B per distinct length) */
+                                 (D is shipped delta-encoded: 3-4 B per distinct length) */
 } ph0b_stage_times;
 
 /* Host-side result of ph0b_h0_barcode; arrays are owned by the library. */
@@ -244,8 +244,8 @@ uint64_t ph0b_last_launch_count(void);
 int ph0b_generate_uniform_cloud_device(ph0b_context* ctx, uint64_t n, uint64_t dim,
                                        uint64_t seed, double* d_out, void* stream);
 
-/* Host-side decoder of the delta-encoded D stream the host-output path uses over PCIe
- * (d2h_codec.cu): chunks of `chunk` values, chunk j = bases[j] followed by 32-bit deltas
+/* Host-side decoder of a delta-encoded D stream with fixed 32-bit deltas: chunks of `chunk`
+ * values, chunk j = bases[j] followed by 32-bit deltas
  * (deltas[j*chunk] unused); chunks with raw[j] != 0 are skipped (shipped uncompressed).
  * Writes out[0..n).  Exposed for callers that move D between processes the same way. */
 int ph0b_decode_deltas(const uint32_t* deltas, const uint64_t* bases, const uint8_t* raw,
