@@ -68,3 +68,30 @@ def test_virtual_ranks_match_oracle(parts, cloud, exchange, monkeypatch):
     assert np.array_equal(r0.death_grade, ref["death_grade"])
     assert np.array_equal(r0.death_length.view(np.uint64), ref["death_length"].view(np.uint64))
     assert r0.essential_count == ref["essential"]
+
+
+@pytest.mark.parametrize("exchange", ["peer", "collective"])
+def test_virtual_ranks_c4_scale(exchange, monkeypatch):
+    """C4 (N=32768, d=3, 5.4e8 edges) as 2 virtual ranks: the multi-rank path at scale (each
+    rank ~2.7e8 edges, full 5-pass sorts, peer-memory scatter of ~4 GB) equals the single-GPU
+    device path: ordered bars bit for bit, D slices concatenated = D."""
+    import torch
+    monkeypatch.setenv("PH0B_EXCHANGE", exchange)
+    X = pkg.config_cloud("C4")
+    n, d = X.shape
+    out = run_virtual(X, 2)
+    D = np.concatenate([o[1] for o in out])
+    ctx = pkg.Context(0)
+    xt = torch.from_numpy(np.asfortranarray(X).ravel(order="F").copy()).cuda()
+    r = ctx.run_device(xt.data_ptr(), n, d)
+    assert len(D) == r.n_scale
+    ref_D = torch.as_tensor(type("C", (), {"__cuda_array_interface__": {
+        "shape": (r.n_scale,), "typestr": "<i8", "data": (r.d_scale, False), "version": 3,
+        "strides": None}})(), device="cuda")
+    assert torch.equal(torch.from_numpy(D.view(np.int64)).cuda(), ref_D)
+    bc = pkg.h0_barcode(X)
+    r0 = out[0][0]
+    assert np.array_equal(r0.death_grade, bc.death_grade)
+    assert np.array_equal(r0.death_length.view(np.uint64), bc.death_length.view(np.uint64))
+    assert r0.essential_count == bc.essential_count
+    ctx.close()
