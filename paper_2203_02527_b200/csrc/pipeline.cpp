@@ -89,14 +89,6 @@ bool d2h_compress() {
     return v;
 }
 
-uint32_t d2h_raw_every() {
-    static const uint32_t v = [] {
-        const char* e = getenv("PH0B_D2H_RAW_EVERY");
-        return e ? (uint32_t)atoi(e) : 0u;
-    }();
-    return v;
-}
-
 uint64_t d2h_chunk_elems() {
     static const uint64_t v = [] {
         const char* e = getenv("PH0B_D2H_CHUNK_MB");
@@ -666,9 +658,25 @@ Status Context::run_host_overlapped(const double* X, uint64_t n, uint64_t d, uin
     // sorted before the rest is partitioned, so its D slice (~19 ms on PCIe) covers the
     // partition; then small buckets (1/256 .. 1/32) so the copy engine never starves, then
     // buckets of 1/16
-    static constexpr uint32_t kCum[] = {16, 17, 19, 23, 31, 47, 63, 79, 95, 111, 127,
-                                        143, 159, 175, 191, 207, 223, 239};
-    constexpr uint32_t B = sizeof(kCum) / sizeof(kCum[0]) + 1;
+    // (PH0B_BUCKETS="c1,c2,...": another schedule, strictly increasing values in (0, 256))
+    static const std::vector<uint32_t> kCum = [] {
+        std::vector<uint32_t> v = {16, 17, 19, 23, 31, 47, 63, 79, 95, 111, 127,
+                                   143, 159, 175, 191, 207, 223, 239};
+        if (const char* e = getenv("PH0B_BUCKETS")) {
+            std::vector<uint32_t> w;
+            for (const char* q = e; *q;) {
+                char* end = nullptr;
+                const long x = strtol(q, &end, 10);
+                if (end == q) break;
+                if (x > 0 && x < 256 && (w.empty() || (uint32_t)x > w.back()))
+                    w.push_back((uint32_t)x);
+                q = *end ? end + 1 : end;
+            }
+            if (!w.empty() && w.size() < 100) v = w;
+        }
+        return v;
+    }();
+    const uint32_t B = (uint32_t)kCum.size() + 1;
     if (!(s = grow(reinterpret_cast<void**>(&dbuf_), &dbuf_cap_, k * 8 + 256)).good()) return s;
     const uint64_t part_words = partition_scratch_words(k, B);
     if (!(s = grow(reinterpret_cast<void**>(&part_counts_), &part_counts_cap_, part_words * 4 + 16))
