@@ -251,6 +251,30 @@ Status Context::ensure_ring() {
     return Status::ok();
 }
 
+bool Context::stream_memops_ok() {
+    if (memops_probe_ == 0) {
+        memops_probe_ = -1;
+        uint32_t* h = nullptr;
+        uint32_t* dp = nullptr;
+        cudaStream_t s = nullptr;
+        if (cudaHostAlloc(reinterpret_cast<void**>(&h), 8, cudaHostAllocMapped) == cudaSuccess &&
+            cudaHostGetDevicePointer(reinterpret_cast<void**>(&dp), h, 0) == cudaSuccess &&
+            cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking) == cudaSuccess) {
+            h[0] = 7;
+            h[1] = 0;
+            const uint64_t d0 = reinterpret_cast<uint64_t>(dp);
+            if (stream_wait_u32(s, d0, 7) && stream_write_u32(s, d0 + 4, 42) &&
+                cudaStreamSynchronize(s) == cudaSuccess &&
+                __atomic_load_n(&h[1], __ATOMIC_ACQUIRE) == 42)
+                memops_probe_ = 1;
+        }
+        if (s) cudaStreamDestroy(s);
+        if (h) cudaFreeHost(h);
+        cudaGetLastError();
+    }
+    return memops_probe_ == 1;
+}
+
 Status Context::grow_host(void** p, uint64_t* cap, uint64_t need) {
     if (need <= *cap) return Status::ok();
     if (*p) cudaFreeHost(*p);
@@ -686,7 +710,9 @@ Status Context::run_host_overlapped(const double* X, uint64_t n, uint64_t d, uin
         return s;
     if (!copy_stream_) PH0B_TRY(cudaStreamCreateWithFlags(&copy_stream_, cudaStreamNonBlocking),
                                 "cudaStreamCreate");
-    const bool compress = host_scale && d2h_compress();
+    // the compressed stream needs stream memory operations on mapped host memory (probed
+    // once per context); without them D goes back uncompressed
+    const bool compress = host_scale && d2h_compress() && stream_memops_ok();
     if (compress) {
         // per bucket, a chunk-aligned area sized by its edge count (>= its |D|): packed bytes
         // (<= 4 per value + slack), chunk bases, widths, offsets (device) and offsets within

@@ -155,6 +155,8 @@ private:
     cudaEvent_t enc_ev_ = nullptr;
     std::vector<cudaStream_t> ring_streams_;  // [0] = copy_stream_
     Status ensure_ring();
+    bool stream_memops_ok();  // cuStreamWait/WriteValue32 on mapped host memory work here
+    int memops_probe_ = 0;    // 0 = not probed, 1 = ok, -1 = unavailable
     uint64_t* h_cbase_ = nullptr;  uint64_t h_cbase_cap_ = 0;
     uint64_t* d_coff_ = nullptr;   uint64_t d_coff_cap_ = 0;    // packed: chunk byte offsets
     uint32_t* d_cpoff_ = nullptr;  uint64_t d_cpoff_cap_ = 0;   // packed: offsets in the piece
