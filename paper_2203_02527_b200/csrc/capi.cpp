@@ -31,7 +31,14 @@ int fail(int code, const std::string& msg) {
     return code;
 }
 
-constexpr uint64_t kOverlapEdges = 1ull << 26;
+// smallest edge count taking the bucketed, D-streaming host path (PH0B_OVERLAP_MIN_EDGES)
+uint64_t overlap_min_edges() {
+    static const uint64_t v = [] {
+        const char* e = getenv("PH0B_OVERLAP_MIN_EDGES");
+        return e ? (uint64_t)strtoull(e, nullptr, 10) : (1ull << 26);
+    }();
+    return v;
+}
 
 bool overlap_disabled() {
     static const bool v = [] {
@@ -257,7 +264,7 @@ int ph0b_run_host(ph0b_context* ctx, const double* X, uint64_t n, uint64_t d, ui
     RunOutputs r;
     const uint64_t k = n * (n - (n > 0)) / 2;
     // Large clouds returning D: overlap the D2H of D with the sort (key-range buckets).
-    const bool overlap = scale && k >= kOverlapEdges && !overlap_disabled();
+    const bool overlap = scale && k >= overlap_min_edges() && !overlap_disabled();
     Status st = overlap ? c->run_host_overlapped(X, n, d, layout, s, scale, scale_capacity, &r)
                         : c->run_host_input(X, n, d, layout, s, StopAfter::Barcode, false, &r);
     g_last_launches = c->launches;

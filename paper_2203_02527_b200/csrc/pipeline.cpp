@@ -682,7 +682,8 @@ Status Context::run_host_overlapped(const double* X, uint64_t n, uint64_t d, uin
     // sorted before the rest is partitioned, so its D slice (~19 ms on PCIe) covers the
     // partition; then small buckets (1/256 .. 1/32) so the copy engine never starves, then
     // buckets of 1/16
-    // (PH0B_BUCKETS="c1,c2,...": another schedule, strictly increasing values in (0, 256))
+    // (PH0B_BUCKETS="c1,c2,...": another schedule, strictly increasing values in (0, 256),
+    // c1 <= 64)
     static const std::vector<uint32_t> kCum = [] {
         std::vector<uint32_t> v = {16, 17, 19, 23, 31, 47, 63, 79, 95, 111, 127,
                                    143, 159, 175, 191, 207, 223, 239};
@@ -696,7 +697,8 @@ Status Context::run_host_overlapped(const double* X, uint64_t n, uint64_t d, uin
                     w.push_back((uint32_t)x);
                 q = *end ? end + 1 : end;
             }
-            if (!w.empty() && w.size() < 100) v = w;
+            // the first bucket is sorted inside buffer 1 before the partition: <= 1/4
+            if (!w.empty() && w.size() < 100 && w[0] <= 64) v = w;
         }
         return v;
     }();
@@ -993,6 +995,12 @@ Status Context::run_host_overlapped(const double* X, uint64_t n, uint64_t d, uin
         int res = 0;
         uint32_t passes = 0;
         const uint64_t c0p = pad(c0);
+        // bucket 0 ping-pongs with the space right after it in buffer 1: it must fit twice
+        // (<= 1/16 of the edges by construction: keys strictly below the 1/16 sample quantile)
+        if ((2 * c0p + 4) * 8 > keys_cap_[1] || (2 * c0p + 4) * 4 > vals_cap_[1])
+            return {PH0B_ERR_CUDA, "internal error: first key-range bucket holds " +
+                                       std::to_string(c0) + " of " + std::to_string(k) +
+                                       " edges (more than half)"};
         s = sort_unique_range(keys_[1], vals_[1], keys_[1] + c0p, vals_[1] + c0p, c0,
                               c0 ? mm[0] : 0, c0 ? mm[B] : 0, false, dbuf_, d_base,
                               d_base + 1, nullptr, st, &res, &passes);
