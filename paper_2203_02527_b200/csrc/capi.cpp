@@ -31,6 +31,9 @@ int fail(int code, const std::string& msg) {
     return code;
 }
 
+// below the bucketed path, a D of at least this many values is still shipped compressed
+constexpr uint64_t kStreamMinValues = 1ull << 21;
+
 // smallest edge count taking the bucketed, D-streaming host path (PH0B_OVERLAP_MIN_EDGES)
 uint64_t overlap_min_edges() {
     static const uint64_t v = [] {
@@ -269,10 +272,19 @@ int ph0b_run_host(ph0b_context* ctx, const double* X, uint64_t n, uint64_t d, ui
                         : c->run_host_input(X, n, d, layout, s, StopAfter::Barcode, false, &r);
     g_last_launches = c->launches;
     if (!st.good()) return fail(st);
+    // mid-size D (not bucketed): still shipped compressed through the ring when possible
+    const bool streamed = scale && !overlap && r.n_scale >= kStreamMinValues &&
+                          c->compressed_d2h_ok();
     rc = copy_out(c, r, s, death_grade, death_length, scale, scale_capacity,
-                  scale != nullptr && !overlap);
+                  scale != nullptr && !overlap && !streamed);
     if (rc) return rc;
-    r.times.d2h_bytes = (overlap ? r.times.d2h_bytes : (scale ? r.n_scale * 8 : 0)) +
+    uint64_t moved = 0;
+    if (streamed) {
+        st = c->stream_scale(r.d_scale, r.n_scale, scale, scale_capacity, s, &moved);
+        if (!st.good()) return fail(st);
+    }
+    r.times.d2h_bytes = (overlap ? r.times.d2h_bytes
+                                 : (streamed ? moved : (scale ? r.n_scale * 8 : 0))) +
                         r.n_finite * 16;  // + the bars
     if (n_finite) *n_finite = r.n_finite;
     if (essential_count) *essential_count = r.essential;

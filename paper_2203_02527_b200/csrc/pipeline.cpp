@@ -251,6 +251,8 @@ Status Context::ensure_ring() {
     return Status::ok();
 }
 
+bool Context::compressed_d2h_ok() { return d2h_compress() && stream_memops_ok(); }
+
 bool Context::stream_memops_ok() {
     if (memops_probe_ == 0) {
         memops_probe_ = -1;
@@ -672,6 +674,175 @@ Status Context::run(const double* dX, uint64_t n, uint64_t d, uint32_t layout,
     return Status::ok();
 }
 
+// Device/pinned buffers, ring, events, copy streams and decode pool of the compressed D
+// stream, for k values split over B buckets.
+Status Context::prepare_stream(uint64_t k, uint32_t B) {
+    Status s;
+    // per bucket, a chunk-aligned area sized by its edge count (>= its |D|): packed bytes
+    // (<= 4 per value + slack), chunk bases, widths, offsets (device) and offsets within
+    // a piece; pinned mirrors of the per-chunk metadata; mapped piece boundaries
+    const uint64_t chunks = k / kPackChunk + B + 64;
+    const uint64_t pieces = chunks / ring_piece_chunks() + B + 2;
+    if (!(s = grow(reinterpret_cast<void**>(&d_delta_), &d_delta_cap_,
+                   chunks * kPackChunk * 4 + 64 * B)).good() ||
+        !(s = grow(reinterpret_cast<void**>(&d_cbase_), &d_cbase_cap_, chunks * 8)).good() ||
+        !(s = grow(reinterpret_cast<void**>(&d_craw_), &d_craw_cap_, chunks)).good() ||
+        !(s = grow(reinterpret_cast<void**>(&d_coff_), &d_coff_cap_, chunks * 8)).good() ||
+        !(s = grow(reinterpret_cast<void**>(&d_cpoff_), &d_cpoff_cap_, chunks * 4)).good() ||
+        !(s = grow_host(reinterpret_cast<void**>(&h_cbase_), &h_cbase_cap_, chunks * 8)).good() ||
+        !(s = grow_host(reinterpret_cast<void**>(&h_craw_), &h_craw_cap_, chunks)).good() ||
+        !(s = grow_host(reinterpret_cast<void**>(&h_cpoff_), &h_cpoff_cap_, chunks * 4)).good() ||
+        !(s = ensure_ring()).good())
+        return s;
+    if (pieces > h_pieceoff_cap_) {
+        if (h_pieceoff_) cudaFreeHost(h_pieceoff_);
+        h_pieceoff_ = nullptr;
+        h_pieceoff_cap_ = 0;
+        PH0B_TRY(cudaHostAlloc(&h_pieceoff_, pieces * 8, cudaHostAllocMapped),
+                 "cudaHostAlloc mapped");
+        PH0B_TRY(cudaHostGetDevicePointer(reinterpret_cast<void**>(&d_pieceoff_), h_pieceoff_,
+                                          0), "cudaHostGetDevicePointer");
+        h_pieceoff_cap_ = pieces;
+    }
+    if (bucket_ev_.size() < B) {
+        bucket_ev_.resize(B, nullptr);
+        for (auto& e : bucket_ev_)
+            if (!e) PH0B_TRY(cudaEventCreateWithFlags(&e, cudaEventDisableTiming), "event");
+    }
+    if (!enc_ev_) PH0B_TRY(cudaEventCreateWithFlags(&enc_ev_, cudaEventDisableTiming), "event");
+    if (ring_streams_.empty()) {
+        static const int ns = [] {
+            const char* e = getenv("PH0B_RING_STREAMS");
+            const int x = e ? atoi(e) : 2;
+            return x < 1 ? 1 : (x > 8 ? 8 : x);
+        }();
+        ring_streams_.push_back(copy_stream_);
+        for (int i = 1; i < ns; ++i) {
+            cudaStream_t x;
+            PH0B_TRY(cudaStreamCreateWithFlags(&x, cudaStreamNonBlocking), "cudaStreamCreate");
+            ring_streams_.push_back(x);
+        }
+    }
+    if (!pool_) {
+        static const int env_threads = [] {
+            const char* e = getenv("PH0B_DECODE_THREADS");
+            return e ? atoi(e) : 0;
+        }();
+        const unsigned hw = std::thread::hardware_concurrency();
+        pool_ = std::make_unique<DecodePool>(
+            env_threads > 0 ? (unsigned)env_threads : (hw > 2 ? hw - 1 : 1));
+    }
+    return Status::ok();
+}
+
+Status Context::stream_scale(const double* d_scale, uint64_t n, double* host_scale,
+                             uint64_t capacity, cudaStream_t st, uint64_t* moved) {
+    *moved = 0;
+    if (n == 0) return Status::ok();
+    if (n > capacity)
+        return {PH0B_ERR_CAPACITY, "scale buffer too small: need " + std::to_string(n) +
+                                       " entries"};
+    if (!copy_stream_) PH0B_TRY(cudaStreamCreateWithFlags(&copy_stream_, cudaStreamNonBlocking),
+                                "cudaStreamCreate");
+    Trace tr;
+    Status s = prepare_stream(n, 1);
+    if (!s.good()) return s;
+    tr.mark("stream_scale: prepared");
+    const uint32_t G = ring_piece_chunks(), R = ring_slots(), NS = ring_subtasks();
+    volatile int overflow = 0;
+    struct PoolGuard {
+        DecodePool* p;
+        ~PoolGuard() { p->wait(); }
+    } pool_guard{pool_.get()};
+    // the slice's bounds: device words for the encoder, pinned host words for the decoders
+    h_small_[4] = 0;
+    h_small_[5] = n;
+    volatile uint64_t* bounds = h_small_ + 4;
+    PH0B_TRY(cudaMemcpyAsync(small_ + 4, h_small_ + 4, 16, cudaMemcpyHostToDevice, st), "H2D");
+    uint8_t* d_pack = reinterpret_cast<uint8_t*>(d_delta_);
+    launches += launch_d2h_pack_bucket(d_scale, small_ + 4, n, d_cbase_, d_craw_, d_coff_,
+                                       d_cpoff_, d_pieceoff_, G, d_pack, st);
+    PH0B_CHECK_LAUNCH("D2H encode");
+    PH0B_TRY(cudaEventRecord(enc_ev_, st), "event");
+    PH0B_TRY(cudaEventSynchronize(enc_ev_), "D2H encode");
+    tr.mark("stream_scale: encoded");
+    const uint64_t nch = (n + kPackChunk - 1) / kPackChunk;
+    const uint64_t npieces = (nch + G - 1) / G;
+    std::vector<uint64_t> poffs(npieces + 1);
+    for (uint64_t p = 0; p <= npieces; ++p) poffs[p] = h_pieceoff_[p];
+    cudaStream_t cs = copy_stream_;
+    PH0B_TRY(cudaMemcpyAsync(h_cbase_, d_cbase_, nch * 8, cudaMemcpyDeviceToHost, cs), "D2H");
+    PH0B_TRY(cudaMemcpyAsync(h_craw_, d_craw_, nch, cudaMemcpyDeviceToHost, cs), "D2H");
+    PH0B_TRY(cudaMemcpyAsync(h_cpoff_, d_cpoff_, nch * 4, cudaMemcpyDeviceToHost, cs), "D2H");
+    PH0B_TRY(cudaEventRecord(bucket_ev_[0], cs), "event");
+    for (size_t i = 1; i < ring_streams_.size(); ++i)
+        PH0B_TRY(cudaStreamWaitEvent(ring_streams_[i], bucket_ev_[0], 0), "wait");
+    *moved += nch * 13;
+    std::vector<DecodeTask> task;
+    for (uint64_t p = 0; p < npieces; ++p) {
+        const uint64_t j0 = p * G;
+        const uint64_t pc = std::min<uint64_t>(G, nch - j0);
+        const uint64_t bytes = poffs[p + 1] - poffs[p];
+        cs = ring_streams_[ring_seq_ % ring_streams_.size()];
+        const uint32_t slot = (uint32_t)(ring_seq_ % R);
+        const uint32_t gen = (uint32_t)(ring_seq_ / R + 1);
+        ++ring_seq_;
+        uint8_t* ring = reinterpret_cast<uint8_t*>(h_ring_) + (uint64_t)slot * ring_slot_bytes();
+        if (!stream_wait_u32(cs, reinterpret_cast<uint64_t>(d_ringflags_ + R + slot), gen - 1))
+            return {PH0B_ERR_CUDA, "D2H ring: stream wait failed"};
+        if (bytes)
+            PH0B_TRY(cudaMemcpyAsync(ring, d_pack + poffs[p], bytes, cudaMemcpyDeviceToHost, cs),
+                     "D2H packed D");
+        if (!stream_write_u32(cs, reinterpret_cast<uint64_t>(d_ringflags_ + slot), gen))
+            return {PH0B_ERR_CUDA, "D2H ring: stream write failed"};
+        *moved += bytes;
+        task.clear();
+        const uint64_t per = (G + NS - 1) / NS;
+        for (uint32_t i = 0; i < NS; ++i) {
+            const uint64_t c0 = std::min<uint64_t>(pc, i * per);
+            const uint64_t c1 = std::min<uint64_t>(pc, c0 + per);
+            const uint64_t c = j0 + c0;
+            DecodeTask t{nullptr, h_cbase_ + c, nullptr, reinterpret_cast<uint64_t*>(host_scale),
+                         (c1 - c0) * kPackChunk, (uint32_t)kPackChunk};
+            t.widths = h_craw_ + c;
+            t.poff = h_cpoff_ + c;
+            t.packed = ring;
+            t.ready = h_ringflags_ + slot;
+            t.freed = h_ringflags_ + R + slot;
+            t.gen = gen;
+            t.bounds = bounds;
+            t.v0 = c * kPackChunk;
+            t.capacity = capacity;
+            t.overflow = &overflow;
+            t.done = &ring_done_[slot];
+            t.nsub = NS;
+            task.push_back(t);
+        }
+        pool_->submit(task);
+    }
+    tr.mark("stream_scale: enqueued");
+    // raw chunks (a gap >= 2^32) straight from the device D
+    PH0B_TRY(cudaEventSynchronize(bucket_ev_[0]), "D2H metadata");
+    for (uint64_t j = 0; j < nch;) {  // runs of consecutive raw chunks: one copy each
+        if (h_craw_[j]) {
+            ++j;
+            continue;
+        }
+        uint64_t j1 = j + 1;
+        while (j1 < nch && !h_craw_[j1]) ++j1;
+        const uint64_t s0 = j * kPackChunk, s1 = std::min<uint64_t>(j1 * kPackChunk, n);
+        PH0B_TRY(cudaMemcpyAsync(host_scale + s0, d_scale + s0, (s1 - s0) * 8,
+                                 cudaMemcpyDeviceToHost, copy_stream_), "D2H raw");
+        *moved += (s1 - s0) * 8;
+        j = j1;
+    }
+    pool_->wait();
+    tr.mark("stream_scale: decoded");
+    for (cudaStream_t x : ring_streams_) PH0B_TRY(cudaStreamSynchronize(x), "D2H scale");
+    if (overflow) return {PH0B_ERR_CUDA, "D2H of D stalled (the copy stream made no progress)"};
+    return Status::ok();
+}
+
 Status Context::run_host_overlapped(const double* X, uint64_t n, uint64_t d, uint32_t layout,
                                     cudaStream_t st, double* host_scale, uint64_t scale_capacity,
                                     RunOutputs* out) {
@@ -716,60 +887,7 @@ Status Context::run_host_overlapped(const double* X, uint64_t n, uint64_t d, uin
     // once per context); without them D goes back uncompressed
     const bool compress = host_scale && d2h_compress() && stream_memops_ok();
     if (compress) {
-        // per bucket, a chunk-aligned area sized by its edge count (>= its |D|): packed bytes
-        // (<= 4 per value + slack), chunk bases, widths, offsets (device) and offsets within
-        // a piece; pinned mirrors of the per-chunk metadata; mapped piece boundaries
-        const uint64_t chunks = k / kPackChunk + B + 64;
-        const uint64_t pieces = chunks / ring_piece_chunks() + B + 2;
-        if (!(s = grow(reinterpret_cast<void**>(&d_delta_), &d_delta_cap_,
-                       chunks * kPackChunk * 4 + 64 * B)).good() ||
-            !(s = grow(reinterpret_cast<void**>(&d_cbase_), &d_cbase_cap_, chunks * 8)).good() ||
-            !(s = grow(reinterpret_cast<void**>(&d_craw_), &d_craw_cap_, chunks)).good() ||
-            !(s = grow(reinterpret_cast<void**>(&d_coff_), &d_coff_cap_, chunks * 8)).good() ||
-            !(s = grow(reinterpret_cast<void**>(&d_cpoff_), &d_cpoff_cap_, chunks * 4)).good() ||
-            !(s = grow_host(reinterpret_cast<void**>(&h_cbase_), &h_cbase_cap_, chunks * 8)).good() ||
-            !(s = grow_host(reinterpret_cast<void**>(&h_craw_), &h_craw_cap_, chunks)).good() ||
-            !(s = grow_host(reinterpret_cast<void**>(&h_cpoff_), &h_cpoff_cap_, chunks * 4)).good() ||
-            !(s = ensure_ring()).good())
-            return s;
-        if (pieces > h_pieceoff_cap_) {
-            if (h_pieceoff_) cudaFreeHost(h_pieceoff_);
-            h_pieceoff_ = nullptr;
-            h_pieceoff_cap_ = 0;
-            PH0B_TRY(cudaHostAlloc(&h_pieceoff_, pieces * 8, cudaHostAllocMapped),
-                     "cudaHostAlloc mapped");
-            PH0B_TRY(cudaHostGetDevicePointer(reinterpret_cast<void**>(&d_pieceoff_), h_pieceoff_,
-                                              0), "cudaHostGetDevicePointer");
-            h_pieceoff_cap_ = pieces;
-        }
-        if (bucket_ev_.size() < B) {
-            bucket_ev_.resize(B, nullptr);
-            for (auto& e : bucket_ev_)
-                if (!e) PH0B_TRY(cudaEventCreateWithFlags(&e, cudaEventDisableTiming), "event");
-        }
-        if (!enc_ev_) PH0B_TRY(cudaEventCreateWithFlags(&enc_ev_, cudaEventDisableTiming), "event");
-        if (ring_streams_.empty()) {
-            static const int ns = [] {
-                const char* e = getenv("PH0B_RING_STREAMS");
-                const int x = e ? atoi(e) : 2;
-                return x < 1 ? 1 : (x > 8 ? 8 : x);
-            }();
-            ring_streams_.push_back(copy_stream_);
-            for (int i = 1; i < ns; ++i) {
-                cudaStream_t x;
-                PH0B_TRY(cudaStreamCreateWithFlags(&x, cudaStreamNonBlocking), "cudaStreamCreate");
-                ring_streams_.push_back(x);
-            }
-        }
-        if (!pool_) {
-            static const int env_threads = [] {
-                const char* e = getenv("PH0B_DECODE_THREADS");
-                return e ? atoi(e) : 0;
-            }();
-            const unsigned hw = std::thread::hardware_concurrency();
-            pool_ = std::make_unique<DecodePool>(
-                env_threads > 0 ? (unsigned)env_threads : (hw > 2 ? hw - 1 : 1));
-        }
+        if (!(s = prepare_stream(k, B)).good()) return s;
     }
     volatile int overflow = 0;  // decode tasks: 1 = scale buffer too small, 2 = stream stalled
     // whatever the exit path, no decode task may still be writing the caller's buffer
@@ -948,17 +1066,24 @@ Status Context::run_host_overlapped(const double* X, uint64_t n, uint64_t d, uin
             }
             PH0B_TRY(cudaEventSynchronize(bucket_ev_[b]), "D2H bucket");
             const uint64_t lo = h_base[b], nb = h_base[b + 1] - lo;
-            for (uint64_t j = 0; j * kPackChunk < nb; ++j) {
-                if (h_craw_[cb[b] + j]) continue;
+            const uint64_t nchb = (nb + kPackChunk - 1) / kPackChunk;
+            for (uint64_t j = 0; j < nchb;) {  // runs of consecutive raw chunks: one copy each
+                if (h_craw_[cb[b] + j]) {
+                    ++j;
+                    continue;
+                }
+                uint64_t j1 = j + 1;
+                while (j1 < nchb && !h_craw_[cb[b] + j1]) ++j1;
                 const uint64_t s0 = lo + j * kPackChunk;
-                const uint64_t len = std::min<uint64_t>(kPackChunk, lo + nb - s0);
-                if (s0 + len > scale_capacity) {
+                const uint64_t s1 = lo + std::min<uint64_t>(j1 * kPackChunk, nb);
+                j = j1;
+                if (s1 > scale_capacity) {
                     overflow = 1;
                     continue;
                 }
-                PH0B_TRY(cudaMemcpyAsync(host_scale + s0, dbuf_ + s0, len * 8,
+                PH0B_TRY(cudaMemcpyAsync(host_scale + s0, dbuf_ + s0, (s1 - s0) * 8,
                                          cudaMemcpyDeviceToHost, copy_stream_), "D2H raw");
-                d2h_total += len * 8;
+                d2h_total += (s1 - s0) * 8;
             }
             pending.erase(pending.begin());
         }

@@ -155,7 +155,17 @@ private:
     cudaEvent_t enc_ev_ = nullptr;
     std::vector<cudaStream_t> ring_streams_;  // [0] = copy_stream_
     Status ensure_ring();
-    bool stream_memops_ok();  // cuStreamWait/WriteValue32 on mapped host memory work here
+    Status prepare_stream(uint64_t k, uint32_t buckets);
+  public:
+    // D (device, n values) -> host_scale through the compressed ring (one slice); *moved =
+    // bytes that crossed PCIe.  Requires stream_memops_ok().
+    Status stream_scale(const double* d_scale, uint64_t n, double* host_scale, uint64_t capacity,
+                        cudaStream_t st, uint64_t* moved);
+    // the compressed D stream is available (PH0B_D2H_COMPRESS != 0 and stream memory
+    // operations on mapped host memory work here; probed once)
+    bool compressed_d2h_ok();
+  private:
+    bool stream_memops_ok();
     int memops_probe_ = 0;    // 0 = not probed, 1 = ok, -1 = unavailable
     uint64_t* h_cbase_ = nullptr;  uint64_t h_cbase_cap_ = 0;
     uint64_t* d_coff_ = nullptr;   uint64_t d_coff_cap_ = 0;    // packed: chunk byte offsets

@@ -1,5 +1,5 @@
-"""Subprocess helper for tests/test_gpu_variants.py: the overlapped host path (ph0b_run_host,
-K >= 2^26) under the D2H knobs set in the environment (ring size / piece size of the
+"""Subprocess helper for tests/test_gpu_variants.py: the host-output paths of ph0b_run_host
+(bucketed at K >= 2^26, one compressed slice below) under the D2H knobs set in the environment (ring size / piece size of the
 streamed compressed D, or uncompressed D) must equal the library-allocated path bit for bit,
 including raw chunks (gaps >= 2^32 between consecutive lengths) and a too-small D buffer."""
 import sys
@@ -20,7 +20,11 @@ def main():
     rng = np.random.default_rng(11)
     far = rng.normal(size=(12000, 3))
     far[:6000] += 1e6  # one huge gap in D: a raw chunk
-    clouds = [pkg.config_cloud("C4", 12000), far]
+    far_mid = rng.normal(size=(4000, 3))
+    far_mid[:2000] += 1e6
+    # K >= 2^26: bucketed path; C3 (3.4e7) and far_mid (8e6): one compressed slice after the
+    # pipeline
+    clouds = [pkg.config_cloud("C4", 12000), far, pkg.config_cloud("C3"), far_mid]
     ctx = pkg.Context(0)
     for X in clouds:
         n = X.shape[0]
