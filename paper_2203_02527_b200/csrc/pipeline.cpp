@@ -98,12 +98,12 @@ uint64_t d2h_chunk_elems() {
     return v;
 }
 
-// Streamed D2H ring of the compressed host path: PH0B_RING_SLOTS slots (default 6) of
+// Streamed D2H ring of the compressed host path: PH0B_RING_SLOTS slots (default 10) of
 // PH0B_RING_CHUNKS 1024-value packed chunks (<= 8 MiB at the default 2048), filled on
 // PH0B_RING_STREAMS copy streams (default 2) and decoded by PH0B_RING_SUBTASKS pool tasks
 // per piece (default 32).  8 MiB copies keep the per-copy and stream-memop overheads below
-// 5 % of the PCIe time (tools/ring_bench.cu); the 48 MiB ring replaces a k*4-byte pinned
-// staging buffer (8.6 GB at C5).  Measured sweep: tools/ring_sweep.sh, DESIGN.md.
+// 5 % of the PCIe time (tools/ring_bench.cu); the 80 MiB ring replaces a k*4-byte pinned
+// staging buffer (8.6 GB at C5).  Measured sweeps: tools/ring_sweep.sh, DESIGN.md.
 uint32_t ring_piece_chunks() {  // 1024-value packed chunks per piece
     static const uint32_t v = [] {
         const char* e = getenv("PH0B_RING_CHUNKS");
@@ -129,7 +129,7 @@ uint32_t ring_subtasks() {
 uint32_t ring_slots() {
     static const uint32_t v = [] {
         const char* e = getenv("PH0B_RING_SLOTS");
-        const int x = e ? atoi(e) : 6;
+        const int x = e ? atoi(e) : 10;
         return (uint32_t)(x < 2 ? 2 : (x > 256 ? 256 : x));
     }();
     return v;
