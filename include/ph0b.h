@@ -166,6 +166,14 @@ int ph0b_run_host(ph0b_context* ctx, const double* X, uint64_t n, uint64_t d, ui
                   uint64_t* n_finite, uint64_t* essential_count, double* scale,
                   uint64_t scale_capacity, uint64_t* n_scale, ph0b_stage_times* times);
 
+/* A device-resident D (e.g. a sharded rank's slice, or ph0b_device_result::d_scale) -> host,
+ * shipped like ph0b_run_host ships it: 3/4-byte deltas per 1024-value chunk through the
+ * pinned ring and decoded by the context's host threads (plain copy for small n or where
+ * stream memory operations are unavailable).  Blocks until host_scale holds the exact bit
+ * patterns.  *bytes_moved (optional): bytes that crossed PCIe. */
+int ph0b_scale_to_host(ph0b_context* ctx, const double* d_scale, uint64_t n, double* host_scale,
+                       uint64_t capacity, void* stream, uint64_t* bytes_moved);
+
 /* ---- sharded (multi-GPU) stages: one context per rank; the caller exchanges data between
  * ranks (NCCL).  SURVEY.md §8(e); orchestration in paper_2203_02527_b200/sharded.py. ----- */
 /* K1 over rows [u_lo, u_hi): their edges in u-major order, into the context workspace. */

@@ -251,6 +251,32 @@ int ph0b_decode_packed(const uint8_t* packed, const uint64_t* bases, const uint8
     return PH0B_OK;
 }
 
+int ph0b_scale_to_host(ph0b_context* ctx, const double* d_scale, uint64_t n, double* host_scale,
+                       uint64_t capacity, void* stream, uint64_t* bytes_moved) {
+    if (bytes_moved) *bytes_moved = 0;
+    if (n == 0) return PH0B_OK;
+    if (!ctx || !d_scale || !host_scale)
+        return fail(PH0B_ERR_INVALID_ARGUMENT, "null context or buffer");
+    if (capacity < n)
+        return fail(PH0B_ERR_CAPACITY, "scale buffer too small: need " + std::to_string(n) +
+                                           " entries");
+    Context* c = reinterpret_cast<Context*>(ctx);
+    std::lock_guard<std::mutex> lk(c->mu);
+    cudaStream_t s = stream ? static_cast<cudaStream_t>(stream) : c->own_stream();
+    uint64_t moved = n * 8;
+    if (n >= kStreamMinValues && c->compressed_d2h_ok()) {
+        const Status st = c->stream_scale(d_scale, n, host_scale, capacity, s, &moved);
+        if (!st.good()) return fail(st);
+    } else {
+        if (cudaMemcpyAsync(host_scale, d_scale, n * 8, cudaMemcpyDeviceToHost, s) != cudaSuccess ||
+            cudaStreamSynchronize(s) != cudaSuccess)
+            return fail(PH0B_ERR_CUDA, std::string("D2H scale: ") +
+                                           cudaGetErrorString(cudaGetLastError()));
+    }
+    if (bytes_moved) *bytes_moved = moved;
+    return PH0B_OK;
+}
+
 int ph0b_run_host(ph0b_context* ctx, const double* X, uint64_t n, uint64_t d, uint32_t layout,
                   void* stream, uint64_t* death_grade, double* death_length, uint64_t* n_finite,
                   uint64_t* essential_count, double* scale, uint64_t scale_capacity,

@@ -36,7 +36,8 @@ EXPORTED_SYMBOLS = [
     "ph0b_last_launch_count", "ph0b_generate_cloud", "ph0b_shard_distances", "ph0b_shard_sample",
     "ph0b_shard_partition", "ph0b_shard_recv", "ph0b_shard_sort_unique", "ph0b_shard_reduce",
     "ph0b_reduce_columns", "ph0b_kruskal_barcode", "ph0b_generate_uniform_cloud_device",
-    "ph0b_decode_deltas", "ph0b_decode_packed", "ph0b_shard_partition_count", "ph0b_shard_recv_peer",
+    "ph0b_decode_deltas", "ph0b_decode_packed", "ph0b_scale_to_host",
+    "ph0b_shard_partition_count", "ph0b_shard_recv_peer",
     "ph0b_shard_scatter_peers", "ph0b_ipc_get_handle", "ph0b_ipc_open_handle", "ph0b_ipc_close",
 ]
 

@@ -191,6 +191,7 @@ class DeviceBackend:
             ("ph0b_shard_scatter_peers", C.c_int, [vp, u32, vp, vp, vp, vp]),
             ("ph0b_ipc_get_handle", C.c_int, [vp, vp]),
             ("ph0b_ipc_open_handle", C.c_int, [vp, C.POINTER(vp)]),
+            ("ph0b_scale_to_host", C.c_int, [vp, vp, u64, vp, u64, vp, u64p]),
         ]:
             fn = getattr(L, name)
             fn.restype, fn.argtypes = res, args
@@ -292,6 +293,15 @@ class DeviceBackend:
             self.h, parts, C.c_void_p(kd.ctypes.data), C.c_void_p(vd.ctypes.data),
             C.c_void_p(off.ctypes.data), None))
         self._count()
+
+    def scale_to_host(self, d_ptr, n, out: np.ndarray) -> int:
+        """This rank's D slice (device) -> out (host, ideally pinned), shipped compressed
+        through the context's ring like ph0b_run_host; returns the bytes that crossed PCIe."""
+        moved = C.c_uint64()
+        _b._check(self.L.ph0b_scale_to_host(self.h, C.c_void_p(d_ptr), n,
+                                            C.c_void_p(out.ctypes.data), out.size, None,
+                                            C.byref(moved)))
+        return int(moved.value)
 
     def reduce(self, n, count, grade_offset):
         m, up, gp, lp = C.c_uint64(), C.c_void_p(), C.c_void_p(), C.c_void_p()

@@ -306,3 +306,35 @@ def test_pathological_large(kind):
     assert np.array_equal(bits(dl[:nf]), bits(bc.death_length))
     assert np.array_equal(bits(sc), bits(bc.scale))
     ctx.close()
+
+
+@pytest.mark.parametrize("cfg", ["C2", "C3", "C4"])
+def test_scale_to_host_matches_device_d(cfg):
+    """ph0b_scale_to_host (a device D -> host, compressed through the ring above 2^21 values,
+    plain copy below; used for the sharded ranks' slices) reproduces the device D bit for
+    bit, including raw (>= 2^32 gap) chunks (C3 is mostly raw)."""
+    import ctypes as C
+    torch = pytest.importorskip("torch")
+    X = pkg.config_cloud(cfg)
+    n, d = X.shape
+    ctx = pkg.Context(0)
+    xt = torch.from_numpy(np.asfortranarray(X).ravel(order="F").copy()).cuda()
+    r = ctx.run_device(xt.data_ptr(), n, d)
+    dev = torch.as_tensor(type("C", (), {"__cuda_array_interface__": {
+        "shape": (r.n_scale,), "typestr": "<i8", "data": (r.d_scale, False), "version": 3,
+        "strides": None}})(), device="cuda").cpu().numpy()
+    out = pkg.PinnedArray(r.n_scale + 3)
+    out.array[:] = -1.0
+    moved = C.c_uint64()
+    L = pkg.lib()
+    L.ph0b_scale_to_host.argtypes = [C.c_void_p, C.c_void_p, C.c_uint64, C.c_void_p, C.c_uint64,
+                                     C.c_void_p, C.POINTER(C.c_uint64)]
+    rc = L.ph0b_scale_to_host(ctx._h, C.c_void_p(r.d_scale), r.n_scale,
+                              C.c_void_p(out.array.ctypes.data), out.array.size, None,
+                              C.byref(moved))
+    assert rc == 0
+    assert np.array_equal(out.array[:r.n_scale].view(np.int64), dev)
+    assert np.all(out.array[r.n_scale:] == -1.0)
+    assert 0 < moved.value <= r.n_scale * 8 + (r.n_scale // 1024 + 1) * 13
+    out.free()
+    ctx.close()
