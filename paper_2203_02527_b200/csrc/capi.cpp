@@ -366,7 +366,16 @@ int ph0b_h0_barcode(const double* X, uint64_t n, uint64_t d, uint32_t layout,
         ph0b_result_free(out);
         return fail(PH0B_ERR_OUT_OF_MEMORY, "host allocation of the result failed");
     }
-    rc = copy_out(c, r, s, out->death_grade, out->death_length, out->scale, r.n_scale, want_scale);
+    // a large D goes compressed through the pinned ring and is decoded by host threads into
+    // the (pageable) result, instead of one pageable-memory DMA
+    const bool streamed = want_scale && r.n_scale >= kStreamMinValues && c->compressed_d2h_ok();
+    rc = copy_out(c, r, s, out->death_grade, out->death_length, out->scale, r.n_scale,
+                  want_scale && !streamed);
+    if (!rc && streamed) {
+        uint64_t moved = 0;
+        const Status ss = c->stream_scale(r.d_scale, r.n_scale, out->scale, r.n_scale, s, &moved);
+        if (!ss.good()) rc = fail(ss);
+    }
     if (rc) {
         ph0b_result_free(out);
         return rc;
