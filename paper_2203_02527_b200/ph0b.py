@@ -7,6 +7,7 @@ calls raise.  numpy arrays are the host containers; device runs take raw device 
 from __future__ import annotations
 
 import ctypes as C
+import weakref
 from dataclasses import dataclass, field
 from pathlib import Path
 
@@ -169,6 +170,26 @@ class Barcode:
         return [(0.0, int(g), float(x)) for g, x in zip(self.death_grade, self.death_length)]
 
 
+_libc = None
+
+
+def _take_scale(res) -> np.ndarray:
+    """D of a ph0b_result as a numpy array that takes over the library's malloc'd buffer
+    (freed with the array) instead of copying it; res.scale is cleared so ph0b_result_free
+    leaves it alone."""
+    global _libc
+    if not res.n_scale:
+        return np.zeros(0)
+    if _libc is None:
+        _libc = C.CDLL(None)
+        _libc.free.argtypes = [C.c_void_p]
+    ptr = C.cast(res.scale, C.c_void_p).value
+    arr = np.ctypeslib.as_array(res.scale, (res.n_scale,))
+    weakref.finalize(arr, _libc.free, ptr)
+    res.scale = None
+    return arr
+
+
 def h0_barcode(X, *, device: int = 0, return_scale: bool = True, workers: int = 1,
                pivoting: bool = True, kruskal: bool = False) -> Barcode:
     """pairwise_distances ∘ build_filtration ∘ build_boundary_matrix ∘ reduce ∘ extract_barcode
@@ -184,10 +205,7 @@ def h0_barcode(X, *, device: int = 0, return_scale: bool = True, workers: int = 
         m = res.n_finite
         g = np.ctypeslib.as_array(res.death_grade, (m,)).copy() if m else np.zeros(0, np.uint64)
         ln = np.ctypeslib.as_array(res.death_length, (m,)).copy() if m else np.zeros(0)
-        sc = None
-        if return_scale:
-            sc = (np.ctypeslib.as_array(res.scale, (res.n_scale,)).copy() if res.n_scale
-                  else np.zeros(0))
+        sc = _take_scale(res) if return_scale else None
         return Barcode(g, ln, int(res.essential_count), sc, res.times.as_dict())
     finally:
         L.ph0b_result_free(C.byref(res))
@@ -205,10 +223,7 @@ def kruskal_barcode(X, *, device: int = 0, return_scale: bool = True) -> Barcode
         m = res.n_finite
         g = np.ctypeslib.as_array(res.death_grade, (m,)).copy() if m else np.zeros(0, np.uint64)
         ln = np.ctypeslib.as_array(res.death_length, (m,)).copy() if m else np.zeros(0)
-        sc = None
-        if return_scale:
-            sc = (np.ctypeslib.as_array(res.scale, (res.n_scale,)).copy() if res.n_scale
-                  else np.zeros(0))
+        sc = _take_scale(res) if return_scale else None
         return Barcode(g, ln, int(res.essential_count), sc, res.times.as_dict())
     finally:
         L.ph0b_result_free(C.byref(res))
