@@ -28,7 +28,9 @@
 extern "C" {
 #endif
 
-#define PH0B_ABI_VERSION 2u
+/* 3: + peer-memory exchange (ph0b_shard_partition_count/recv_peer/scatter_peers, ph0b_ipc_*),
+ *    ph0b_scale_to_host, ph0b_decode_packed */
+#define PH0B_ABI_VERSION 3u
 
 /* Return codes.  The message of ph0b_last_error() repeats the reference's exception text
  * where the reference has one. */
