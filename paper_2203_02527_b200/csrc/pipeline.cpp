@@ -735,6 +735,79 @@ Status Context::prepare_stream(uint64_t k, uint32_t B) {
     return Status::ok();
 }
 
+// One packed slice -> host: its chunk metadata [cbase, cbase + nch) (pinned mirrors; meta_ev
+// recorded after it), then its pieces (byte ranges poffs[p] .. poffs[p+1] of d_src) through
+// the ring, each handed to the pool as ring_subtasks() decode tasks right after its copy is
+// enqueued (when a copy stream's queue is full the enqueue blocks until earlier pieces are
+// decoded).  Must follow the slice's encode (enc_ev_) in stream order.
+Status Context::enqueue_stream(uint64_t cbase, uint64_t nch, const std::vector<uint64_t>& poffs,
+                               const uint8_t* d_src, const volatile uint64_t* bounds,
+                               cudaEvent_t meta_ev, double* host_scale, uint64_t capacity,
+                               volatile int* overflow, uint64_t* moved, uint64_t* enq_ns) {
+    const uint32_t G = ring_piece_chunks(), R = ring_slots(), NS = ring_subtasks();
+    const uint64_t npieces = poffs.size() - 1;
+    cudaStream_t cs = copy_stream_;
+    PH0B_TRY(cudaStreamWaitEvent(cs, enc_ev_, 0), "wait");
+    PH0B_TRY(cudaMemcpyAsync(h_cbase_ + cbase, d_cbase_ + cbase, nch * 8, cudaMemcpyDeviceToHost,
+                             cs), "D2H bases");
+    PH0B_TRY(cudaMemcpyAsync(h_craw_ + cbase, d_craw_ + cbase, nch, cudaMemcpyDeviceToHost, cs),
+             "D2H widths");
+    PH0B_TRY(cudaMemcpyAsync(h_cpoff_ + cbase, d_cpoff_ + cbase, nch * 4, cudaMemcpyDeviceToHost,
+                             cs), "D2H offsets");
+    PH0B_TRY(cudaEventRecord(meta_ev, cs), "event");
+    // extra ring streams: their pieces must not land before the chunk metadata
+    for (size_t i = 1; i < ring_streams_.size(); ++i)
+        PH0B_TRY(cudaStreamWaitEvent(ring_streams_[i], meta_ev, 0), "wait");
+    *moved += nch * 13;
+    std::vector<DecodeTask> task;
+    for (uint64_t p = 0; p < npieces; ++p) {
+        const uint64_t j0 = p * G;
+        const uint64_t pc = std::min<uint64_t>(G, nch - j0);
+        const uint64_t bytes = poffs[p + 1] - poffs[p];
+        cs = ring_streams_[ring_seq_ % ring_streams_.size()];
+        const uint32_t slot = (uint32_t)(ring_seq_ % R);
+        const uint32_t gen = (uint32_t)(ring_seq_ / R + 1);
+        ++ring_seq_;
+        uint8_t* ring = reinterpret_cast<uint8_t*>(h_ring_) + (uint64_t)slot * ring_slot_bytes();
+        const auto e0 = std::chrono::steady_clock::now();
+        if (!stream_wait_u32(cs, reinterpret_cast<uint64_t>(d_ringflags_ + R + slot), gen - 1))
+            return {PH0B_ERR_CUDA, "D2H ring: stream wait failed"};
+        if (bytes)
+            PH0B_TRY(cudaMemcpyAsync(ring, d_src + poffs[p], bytes, cudaMemcpyDeviceToHost, cs),
+                     "D2H packed D");
+        if (!stream_write_u32(cs, reinterpret_cast<uint64_t>(d_ringflags_ + slot), gen))
+            return {PH0B_ERR_CUDA, "D2H ring: stream write failed"};
+        *enq_ns += std::chrono::duration_cast<std::chrono::nanoseconds>(
+                       std::chrono::steady_clock::now() - e0).count();
+        *moved += bytes;
+        // the piece is decoded by NS tasks of G/NS chunks (empty past the piece's end)
+        task.clear();
+        const uint64_t per = (G + NS - 1) / NS;
+        for (uint32_t i = 0; i < NS; ++i) {
+            const uint64_t c0 = std::min<uint64_t>(pc, i * per);
+            const uint64_t c1 = std::min<uint64_t>(pc, c0 + per);
+            const uint64_t c = cbase + j0 + c0;
+            DecodeTask t{nullptr, h_cbase_ + c, nullptr, reinterpret_cast<uint64_t*>(host_scale),
+                         (c1 - c0) * kPackChunk, (uint32_t)kPackChunk};
+            t.widths = h_craw_ + c;
+            t.poff = h_cpoff_ + c;
+            t.packed = ring;
+            t.ready = h_ringflags_ + slot;
+            t.freed = h_ringflags_ + R + slot;
+            t.gen = gen;
+            t.bounds = bounds;
+            t.v0 = (j0 + c0) * kPackChunk;
+            t.capacity = capacity;
+            t.overflow = overflow;
+            t.done = &ring_done_[slot];
+            t.nsub = NS;
+            task.push_back(t);
+        }
+        pool_->submit(task);
+    }
+    return Status::ok();
+}
+
 Status Context::stream_scale(const double* d_scale, uint64_t n, double* host_scale,
                              uint64_t capacity, cudaStream_t st, uint64_t* moved) {
     *moved = 0;
@@ -748,7 +821,7 @@ Status Context::stream_scale(const double* d_scale, uint64_t n, double* host_sca
     Status s = prepare_stream(n, 1);
     if (!s.good()) return s;
     tr.mark("stream_scale: prepared");
-    const uint32_t G = ring_piece_chunks(), R = ring_slots(), NS = ring_subtasks();
+    const uint32_t G = ring_piece_chunks();
     volatile int overflow = 0;
     struct PoolGuard {
         DecodePool* p;
@@ -770,56 +843,10 @@ Status Context::stream_scale(const double* d_scale, uint64_t n, double* host_sca
     const uint64_t npieces = (nch + G - 1) / G;
     std::vector<uint64_t> poffs(npieces + 1);
     for (uint64_t p = 0; p <= npieces; ++p) poffs[p] = h_pieceoff_[p];
-    cudaStream_t cs = copy_stream_;
-    PH0B_TRY(cudaMemcpyAsync(h_cbase_, d_cbase_, nch * 8, cudaMemcpyDeviceToHost, cs), "D2H");
-    PH0B_TRY(cudaMemcpyAsync(h_craw_, d_craw_, nch, cudaMemcpyDeviceToHost, cs), "D2H");
-    PH0B_TRY(cudaMemcpyAsync(h_cpoff_, d_cpoff_, nch * 4, cudaMemcpyDeviceToHost, cs), "D2H");
-    PH0B_TRY(cudaEventRecord(bucket_ev_[0], cs), "event");
-    for (size_t i = 1; i < ring_streams_.size(); ++i)
-        PH0B_TRY(cudaStreamWaitEvent(ring_streams_[i], bucket_ev_[0], 0), "wait");
-    *moved += nch * 13;
-    std::vector<DecodeTask> task;
-    for (uint64_t p = 0; p < npieces; ++p) {
-        const uint64_t j0 = p * G;
-        const uint64_t pc = std::min<uint64_t>(G, nch - j0);
-        const uint64_t bytes = poffs[p + 1] - poffs[p];
-        cs = ring_streams_[ring_seq_ % ring_streams_.size()];
-        const uint32_t slot = (uint32_t)(ring_seq_ % R);
-        const uint32_t gen = (uint32_t)(ring_seq_ / R + 1);
-        ++ring_seq_;
-        uint8_t* ring = reinterpret_cast<uint8_t*>(h_ring_) + (uint64_t)slot * ring_slot_bytes();
-        if (!stream_wait_u32(cs, reinterpret_cast<uint64_t>(d_ringflags_ + R + slot), gen - 1))
-            return {PH0B_ERR_CUDA, "D2H ring: stream wait failed"};
-        if (bytes)
-            PH0B_TRY(cudaMemcpyAsync(ring, d_pack + poffs[p], bytes, cudaMemcpyDeviceToHost, cs),
-                     "D2H packed D");
-        if (!stream_write_u32(cs, reinterpret_cast<uint64_t>(d_ringflags_ + slot), gen))
-            return {PH0B_ERR_CUDA, "D2H ring: stream write failed"};
-        *moved += bytes;
-        task.clear();
-        const uint64_t per = (G + NS - 1) / NS;
-        for (uint32_t i = 0; i < NS; ++i) {
-            const uint64_t c0 = std::min<uint64_t>(pc, i * per);
-            const uint64_t c1 = std::min<uint64_t>(pc, c0 + per);
-            const uint64_t c = j0 + c0;
-            DecodeTask t{nullptr, h_cbase_ + c, nullptr, reinterpret_cast<uint64_t*>(host_scale),
-                         (c1 - c0) * kPackChunk, (uint32_t)kPackChunk};
-            t.widths = h_craw_ + c;
-            t.poff = h_cpoff_ + c;
-            t.packed = ring;
-            t.ready = h_ringflags_ + slot;
-            t.freed = h_ringflags_ + R + slot;
-            t.gen = gen;
-            t.bounds = bounds;
-            t.v0 = c * kPackChunk;
-            t.capacity = capacity;
-            t.overflow = &overflow;
-            t.done = &ring_done_[slot];
-            t.nsub = NS;
-            task.push_back(t);
-        }
-        pool_->submit(task);
-    }
+    uint64_t enq = 0;
+    s = enqueue_stream(0, nch, poffs, d_pack, bounds, bucket_ev_[0], host_scale, capacity,
+                       &overflow, moved, &enq);
+    if (!s.good()) return s;
     tr.mark("stream_scale: enqueued");
     // raw chunks (a gap >= 2^32) straight from the device D
     PH0B_TRY(cudaEventSynchronize(bucket_ev_[0]), "D2H metadata");
@@ -955,8 +982,6 @@ Status Context::run_host_overlapped(const double* X, uint64_t n, uint64_t d, uin
     //    (an upper bound of its |D|), so bucket b's copies are enqueued while bucket b+1 sorts.
     //  * uncompressed: plain D2H of the slice in medium chunks once the bucket is sorted.
     const uint32_t G = ring_piece_chunks();
-    const uint32_t R = ring_slots();
-    const uint32_t NS = ring_subtasks();
     std::vector<uint64_t> nch_ub(B), cb(B + 1, 0), rb(B + 1, 0);
     for (uint32_t b = 0; b < B; ++b) {
         nch_ub[b] = (tot[b] + kPackChunk - 1) / kPackChunk;
@@ -989,70 +1014,12 @@ Status Context::run_host_overlapped(const double* X, uint64_t n, uint64_t d, uin
         const uint64_t npieces = (nch + G - 1) / G;
         std::vector<uint64_t> poffs(npieces + 1);
         for (uint64_t p = 0; p <= npieces; ++p) poffs[p] = h_pieceoff_[p];
-        cudaStream_t cs = copy_stream_;
-        PH0B_TRY(cudaStreamWaitEvent(cs, enc_ev_, 0), "wait");
-        PH0B_TRY(cudaMemcpyAsync(h_cbase_ + cb[b], d_cbase_ + cb[b], nch * 8,
-                                 cudaMemcpyDeviceToHost, cs), "D2H bases");
-        PH0B_TRY(cudaMemcpyAsync(h_craw_ + cb[b], d_craw_ + cb[b], nch, cudaMemcpyDeviceToHost,
-                                 cs), "D2H widths");
-        PH0B_TRY(cudaMemcpyAsync(h_cpoff_ + cb[b], d_cpoff_ + cb[b], nch * 4,
-                                 cudaMemcpyDeviceToHost, cs), "D2H offsets");
-        PH0B_TRY(cudaEventRecord(bucket_ev_[b], cs), "event");
-        // extra ring streams: their pieces must not land before the chunk metadata
-        for (size_t i = 1; i < ring_streams_.size(); ++i)
-            PH0B_TRY(cudaStreamWaitEvent(ring_streams_[i], bucket_ev_[b], 0), "wait");
-        d2h_total += nch * 13;
-        // each piece's tasks are handed to the pool right after its copy is enqueued: when
-        // the copy stream's queue is full, the enqueue blocks until earlier pieces are decoded
-        std::vector<DecodeTask> task;
-        for (uint64_t p = 0; p < npieces; ++p) {
-            const uint64_t j0 = p * G;
-            const uint64_t pc = std::min<uint64_t>(G, nch - j0);
-            const uint64_t bytes = poffs[p + 1] - poffs[p];
-            cs = ring_streams_[ring_seq_ % ring_streams_.size()];
-            const uint32_t slot = (uint32_t)(ring_seq_ % R);
-            const uint32_t gen = (uint32_t)(ring_seq_ / R + 1);
-            ++ring_seq_;
-            uint8_t* ring = reinterpret_cast<uint8_t*>(h_ring_) + (uint64_t)slot * ring_slot_bytes();
-            const uint64_t dready = reinterpret_cast<uint64_t>(d_ringflags_ + slot);
-            const uint64_t dfreed = reinterpret_cast<uint64_t>(d_ringflags_ + R + slot);
-            const auto e0 = std::chrono::steady_clock::now();
-            if (!stream_wait_u32(cs, dfreed, gen - 1))
-                return {PH0B_ERR_CUDA, "D2H ring: stream wait failed"};
-            if (bytes)
-                PH0B_TRY(cudaMemcpyAsync(ring, d_pack + rb[b] + poffs[p], bytes,
-                                         cudaMemcpyDeviceToHost, cs), "D2H packed D");
-            if (!stream_write_u32(cs, dready, gen))
-                return {PH0B_ERR_CUDA, "D2H ring: stream write failed"};
-            enq_ns += std::chrono::duration_cast<std::chrono::nanoseconds>(
-                          std::chrono::steady_clock::now() - e0).count();
-            d2h_total += bytes;
-            // the piece is decoded by NS tasks of G/NS chunks (empty past the piece's end)
-            task.clear();
-            const uint64_t per = (G + NS - 1) / NS;
-            for (uint32_t i = 0; i < NS; ++i) {
-                const uint64_t c0 = std::min<uint64_t>(pc, i * per);
-                const uint64_t c1 = std::min<uint64_t>(pc, c0 + per);
-                const uint64_t c = cb[b] + j0 + c0;
-                DecodeTask t{nullptr, h_cbase_ + c, nullptr,
-                             reinterpret_cast<uint64_t*>(host_scale), (c1 - c0) * kPackChunk,
-                             (uint32_t)kPackChunk};
-                t.widths = h_craw_ + c;
-                t.poff = h_cpoff_ + c;
-                t.packed = ring;
-                t.ready = h_ringflags_ + slot;
-                t.freed = h_ringflags_ + R + slot;
-                t.gen = gen;
-                t.bounds = h_base + b;
-                t.v0 = (j0 + c0) * kPackChunk;
-                t.capacity = scale_capacity;
-                t.overflow = &overflow;
-                t.done = &ring_done_[slot];
-                t.nsub = NS;
-                task.push_back(t);
-            }
-            pool_->submit(task);
-        }
+        uint64_t moved = 0;
+        const Status es = enqueue_stream(cb[b], nch, poffs, d_pack + rb[b], h_base + b,
+                                         bucket_ev_[b], host_scale, scale_capacity, &overflow,
+                                         &moved, &enq_ns);
+        if (!es.good()) return es;
+        d2h_total += moved;
         pending.push_back(b);
         return Status::ok();
     };

@@ -156,6 +156,10 @@ private:
     std::vector<cudaStream_t> ring_streams_;  // [0] = copy_stream_
     Status ensure_ring();
     Status prepare_stream(uint64_t k, uint32_t buckets);
+    Status enqueue_stream(uint64_t cbase, uint64_t nch, const std::vector<uint64_t>& poffs,
+                          const uint8_t* d_src, const volatile uint64_t* bounds,
+                          cudaEvent_t meta_ev, double* host_scale, uint64_t capacity,
+                          volatile int* overflow, uint64_t* moved, uint64_t* enq_ns);
   public:
     // D (device, n values) -> host_scale through the compressed ring (one slice); *moved =
     // bytes that crossed PCIe.  Requires stream_memops_ok().
