@@ -68,3 +68,27 @@ def test_ipc_peer_exchange_matches_oracle(world):
     assert np.array_equal(res[0][3], ref["death_grade"])
     assert np.array_equal(res[0][4].view(np.uint64), ref["death_length"].view(np.uint64))
     assert res[0][5] == ref["essential"]
+
+
+def test_ipc_peer_exchange_c4_scale():
+    """C4 (5.4e8 edges) as 2 rank processes on the one B200: each partition kernel stores
+    ~3 GB straight into the other process's receive buffer through the IPC mapping; the
+    concatenated D slices and rank 0's bars equal the single-GPU device path bit for bit."""
+    import paper_2203_02527_b200 as pkg
+    X = pkg.config_cloud("C4")
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_worker, args=(r, 2, port, X, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    res = sorted([q.get(timeout=600) for _ in range(2)], key=lambda t: t[0])
+    for p in procs:
+        p.join(timeout=120)
+        assert p.exitcode == 0
+    bc = pkg.h0_barcode(X)
+    D = np.concatenate([r[2] for r in res])
+    assert np.array_equal(D.view(np.uint64), bc.scale.view(np.uint64))
+    assert np.array_equal(res[0][3], bc.death_grade)
+    assert np.array_equal(res[0][4].view(np.uint64), bc.death_length.view(np.uint64))
+    assert res[0][5] == bc.essential_count
