@@ -329,7 +329,7 @@ Status Context::reserve_points(uint64_t n, uint64_t d) {
     if (status_words * 8 > status_cap_) status_zeroed_ = false;
     G(status_, status_cap_, status_words * 8);
     G(comp_, comp_cap_, std::max<uint64_t>(4, n * 4));
-    G(best_, best_cap_, std::max<uint64_t>(16, 2 * n * 4 + n * 2 + 16));
+    G(best_, best_cap_, std::max<uint64_t>(16, 2 * n * 4 + n * 2 + 48));
     G(surv_, surv_cap_, std::max<uint64_t>(4, n * 4));
     G(surv_sorted_, surv_sorted_cap_, std::max<uint64_t>(4, n * 4));
     G(lows_, lows_cap_, std::max<uint64_t>(4, n * 4));

@@ -29,6 +29,7 @@
 
 #include <algorithm>
 #include <cstdint>
+#include <cstdlib>
 
 #include "common.cuh"
 #include "kernels.h"
@@ -146,6 +147,69 @@ __global__ void __launch_bounds__(kThreads)
     }
 }
 
+// Same filter with the u16 label copy staged in shared memory (≤ 128 KB for N ≤ 65536): the
+// 16 label gathers per thread are shared-memory reads instead of L1/L2 round trips.  One
+// 1024-thread CTA per SM.
+constexpr int kFThreads = 1024;
+__global__ void __launch_bounds__(kFThreads)
+    k4_filter_range_s(const uint32_t* __restrict__ uv, uint64_t begin, uint64_t end,
+                      const uint16_t* __restrict__ comp16, uint32_t n, uint32_t* __restrict__ out,
+                      uint64_t cap, uint32_t* counters) {
+    extern __shared__ __align__(16) uint16_t s_comp[];
+    {
+        const uint32_t n8 = (n + 7) / 8;  // 16-byte pieces (the label copy is padded)
+        const uint4* src = reinterpret_cast<const uint4*>(comp16);
+        uint4* dst = reinterpret_cast<uint4*>(s_comp);
+        for (uint32_t i = threadIdx.x; i < n8; i += kFThreads) dst[i] = __ldg(src + i);
+    }
+    __syncthreads();
+    const uint32_t lane = threadIdx.x & 31;
+    const uint64_t a0 = begin & ~7ull;
+    const uint64_t groups = (end - a0 + 7) / 8;
+    const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+    for (uint64_t g0 = (uint64_t)blockIdx.x * blockDim.x; g0 < groups; g0 += stride) {
+        const uint64_t g = g0 + threadIdx.x;
+        uint32_t e[8];
+        uint32_t keep = 0;
+        if (g < groups) {
+            const uint64_t first = a0 + 8 * g;
+            if (first + 8 <= end) {
+                const uint4* p = reinterpret_cast<const uint4*>(uv + first);
+                const uint4 x = __ldg(p), y = __ldg(p + 1);
+                e[0] = x.x; e[1] = x.y; e[2] = x.z; e[3] = x.w;
+                e[4] = y.x; e[5] = y.y; e[6] = y.z; e[7] = y.w;
+            } else {
+#pragma unroll
+                for (int i = 0; i < 8; ++i) e[i] = first + i < end ? __ldg(uv + first + i) : 0u;
+            }
+#pragma unroll
+            for (int i = 0; i < 8; ++i) {
+                const uint64_t j = a0 + 8 * g + i;
+                if (j >= begin && j < end && s_comp[e[i] >> 16] != s_comp[e[i] & 0xFFFFu])
+                    keep |= 1u << i;
+            }
+        }
+        const uint32_t c = __popc(keep);
+        uint32_t inc = c;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const uint32_t y = __shfl_up_sync(0xffffffffu, inc, o);
+            if (lane >= o) inc += y;
+        }
+        const uint32_t wtot = __shfl_sync(0xffffffffu, inc, 31);
+        if (wtot == 0) continue;
+        uint32_t slot = 0;
+        if (lane == 31) slot = atomicAdd(&counters[kCntCand], wtot);
+        slot = __shfl_sync(0xffffffffu, slot, 31) + inc - c;
+        if (slot + c > cap) {
+            if (c) counters[kCntOverflow] = 1;
+            continue;
+        }
+        for (int i = 0; i < 8; ++i)
+            if (keep & (1u << i)) out[slot++] = (uint32_t)(a0 + 8 * g + i);
+    }
+}
+
 // Each live tree's minimum candidate column (its pivot candidate for this round).
 __global__ void __launch_bounds__(kThreads)
     k4_min_edge(const uint32_t* __restrict__ cand, uint32_t ncand, const uint32_t* __restrict__ uv,
@@ -238,7 +302,8 @@ int run_reduction(ReduceState& st, cudaStream_t s, int num_sms, uint32_t& epoch,
         return 0;
     }
     uint32_t* par = st.best + n;  // best buffer holds [best | par | comp16]
-    uint16_t* comp16 = reinterpret_cast<uint16_t*>(st.best + 2 * n);
+    // (16-byte aligned: the shared-memory filter stages it with 16-byte loads)
+    uint16_t* comp16 = reinterpret_cast<uint16_t*>(st.best + ((2ull * n + 3) & ~3ull));
     const unsigned gn = grid_for(n, num_sms, 4);
     cudaMemsetAsync(st.counters, 0, sizeof(uint32_t) * 8, s);
     k4_init<<<gn, kThreads, 0, s>>>(st.comp, st.best, par, n, comp16);
@@ -250,6 +315,19 @@ int run_reduction(ReduceState& st, cudaStream_t s, int num_sms, uint32_t& epoch,
         cudaStreamSynchronize(s);
     };
 
+    // labels in shared memory for the window filter (PH0B_SMEM_FILTER=0: through L1)
+    static const bool smem_env = [] {
+        const char* e = getenv("PH0B_SMEM_FILTER");
+        return !(e && e[0] == '0');
+    }();
+    const size_t fsmem = ((size_t)n * 2 + 15) & ~(size_t)15;
+    bool smem_filter = smem_env && fsmem <= 200 * 1024;
+    if (smem_filter && cudaFuncSetAttribute(k4_filter_range_s,
+                                            cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                            (int)fsmem) != cudaSuccess) {
+        cudaGetLastError();
+        smem_filter = false;
+    }
     uint64_t pos = 0;
     uint64_t window = std::min<uint64_t>(st.k, std::max<uint64_t>(8ull * n, 1u << 16));
     uint32_t survivors = 0;
@@ -258,8 +336,15 @@ int run_reduction(ReduceState& st, cudaStream_t s, int num_sms, uint32_t& epoch,
         // (i) clearing filter over the window
         cudaMemsetAsync(st.counters + kCntCand, 0, sizeof(uint32_t), s);
         cudaMemsetAsync(st.counters + kCntOverflow, 0, sizeof(uint32_t), s);
-        k4_filter_range<<<grid_for((end - pos + 7) / 8, num_sms), kThreads, 0, s>>>(
-            st.uv, pos, end, comp16, st.cand[0], st.cap, st.counters);
+        if (smem_filter) {
+            uint64_t blocks = ((end - pos + 7) / 8 + kFThreads - 1) / kFThreads;
+            if (blocks > (uint64_t)num_sms) blocks = num_sms;
+            k4_filter_range_s<<<(unsigned)(blocks ? blocks : 1), kFThreads, fsmem, s>>>(
+                st.uv, pos, end, comp16, n, st.cand[0], st.cap, st.counters);
+        } else {
+            k4_filter_range<<<grid_for((end - pos + 7) / 8, num_sms), kThreads, 0, s>>>(
+                st.uv, pos, end, comp16, st.cand[0], st.cap, st.counters);
+        }
         S.launches += 1;
         pull();
         if (h[kCntOverflow]) {  // too many live columns in this window: shrink and retry
