@@ -133,6 +133,21 @@ def test_random_sizes_sweep():
                             ref["scale"])
 
 
+@pytest.mark.parametrize("d", [5, 6, 7, 12, 17, 24, 31, 32, 33, 40, 64])
+def test_dimension_paths(d):
+    """Every distance-kernel path: d in {1,2,3,4,8,16} specialised (other tests), other d <= 32
+    through the runtime-d TMA kernel, d > 32 through the global-memory kernel — same fold
+    order, bit-exact D and bars."""
+    rng = np.random.default_rng(100 + d)
+    n = 300 + 7 * d
+    X = np.concatenate([rng.normal(0, 1, size=(n // 2, d)),
+                        rng.normal(4, 0.5, size=(n - n // 2, d))])
+    bc = pkg.h0_barcode(X)
+    ref = ob.oracle_filtration_and_bars(X)
+    assert_same_barcode(bc, ref["death_grade"], ref["death_length"], ref["essential"],
+                        ref["scale"])
+
+
 def test_quantized_ties_medium():
     """Coordinates on a coarse grid (many equal lengths), N=3000: ties across sort tiles."""
     rng = np.random.default_rng(5)
