@@ -70,16 +70,17 @@ def test_virtual_ranks_match_oracle(parts, cloud, exchange, monkeypatch):
     assert r0.essential_count == ref["essential"]
 
 
-@pytest.mark.parametrize("exchange", ["peer", "collective"])
-def test_virtual_ranks_c4_scale(exchange, monkeypatch):
-    """C4 (N=32768, d=3, 5.4e8 edges) as 2 virtual ranks: the multi-rank path at scale (each
-    rank ~2.7e8 edges, full 5-pass sorts, peer-memory scatter of ~4 GB) equals the single-GPU
-    device path: ordered bars bit for bit, D slices concatenated = D."""
+@pytest.mark.parametrize("exchange,parts", [("peer", 2), ("collective", 2), ("peer", 8)])
+def test_virtual_ranks_c4_scale(exchange, parts, monkeypatch):
+    """C4 (N=32768, d=3, 5.4e8 edges) as 2 or 8 virtual ranks: the multi-rank path at scale
+    (full 5-pass sorts per rank, peer-memory scatter of GBs, 8-way splitters as on one 8-GPU
+    box) equals the single-GPU device path: ordered bars bit for bit, D slices concatenated =
+    D."""
     import torch
     monkeypatch.setenv("PH0B_EXCHANGE", exchange)
     X = pkg.config_cloud("C4")
     n, d = X.shape
-    out = run_virtual(X, 2)
+    out = run_virtual(X, parts)
     D = np.concatenate([o[1] for o in out])
     ctx = pkg.Context(0)
     xt = torch.from_numpy(np.asfortranarray(X).ravel(order="F").copy()).cuda()
