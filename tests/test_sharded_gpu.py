@@ -96,3 +96,24 @@ def test_virtual_ranks_c4_scale(exchange, parts, monkeypatch):
     assert np.array_equal(r0.death_length.view(np.uint64), bc.death_length.view(np.uint64))
     assert r0.essential_count == bc.essential_count
     ctx.close()
+
+
+def test_virtual_ranks_c5_8way(monkeypatch):
+    """The target configuration's multi-GPU decomposition — C5 (N=65536, d=8, 2.1e9 edges)
+    split over 8 ranks exactly as on one 8-GPU box (row shards, 8-way splitters, peer-memory
+    scatter, per-rank sort/unique/reduction, final reduction) — run as 8 virtual ranks on the
+    one B200: D slices concatenated and rank 0's bars equal the single-GPU path bit for bit."""
+    monkeypatch.setenv("PH0B_EXCHANGE", "peer")
+    X = pkg.config_cloud("C5")
+    out = run_virtual(X, 8)
+    D = np.concatenate([o[1] for o in out])
+    offs = [o[0].scale_offset for o in out]
+    assert offs == list(np.cumsum([0] + [len(o[1]) for o in out])[:-1])
+    del out[1:]
+    bc = pkg.h0_barcode(X)
+    assert len(D) == len(bc.scale)
+    assert np.array_equal(D.view(np.uint64), bc.scale.view(np.uint64))
+    r0 = out[0][0]
+    assert np.array_equal(r0.death_grade, bc.death_grade)
+    assert np.array_equal(r0.death_length.view(np.uint64), bc.death_length.view(np.uint64))
+    assert r0.essential_count == bc.essential_count
