@@ -273,7 +273,7 @@ __device__ __forceinline__ void mbar_wait_parity(uint64_t* bar, uint32_t parity)
 // (measured ablation: PH0B_LOOKBACK=restart); default: the early probe's aggregate is
 // consumed and the look-back continues at tile - 2 in windows of kLookbackWin.
 constexpr int kLookbackWin = 4;
-template <bool kVals, bool kCountNext, bool kRestart>
+template <bool kVals, bool kCountNext, bool kRestart, bool kTop = false>
 __global__ void __launch_bounds__(kThreads, 2)
     k2_onesweep_p(const uint64_t* __restrict__ keys_in, uint64_t* __restrict__ keys_out,
                   const uint32_t* __restrict__ vals_in, uint32_t* __restrict__ vals_out,
@@ -329,6 +329,11 @@ __global__ void __launch_bounds__(kThreads, 2)
 #pragma unroll
         for (int w = 0; w < kWarps; ++w) s_whist[w][tid] = 0;
         __syncthreads();
+        // kTop: the look-back's probe of tile - 1 goes out here, before this tile is even
+        // ranked: its latency hides behind the rank, scan and scatter phases (C5: 14.51 ->
+        // 13.83 ms per pass vs issuing it after this tile's aggregate is published)
+        uint64_t probe_top = 0;
+        if (kTop && tile > 0) probe_top = ld_relaxed_u64(status + (uint64_t)(tile - 1) * kBins + t);
         mbar_wait_parity(&s_bar, parity);
         parity ^= 1u;
 
@@ -364,7 +369,8 @@ __global__ void __launch_bounds__(kThreads, 2)
         // early probe of tile - 1 (its latency hides behind the scan and the scatter; an
         // aggregate read now is still valid after the scatter)
         const uint64_t probe =
-            tile > 0 ? ld_relaxed_u64(status + (uint64_t)(tile - 1) * kBins + t) : 0ull;
+            kTop ? probe_top
+                 : (tile > 0 ? ld_relaxed_u64(status + (uint64_t)(tile - 1) * kBins + t) : 0ull);
         const uint32_t tstart = block_exclusive_scan(cnt, s_scan, nullptr);
         s_tile_start[t] = tstart;
         __syncthreads();
@@ -506,7 +512,12 @@ bool lookback_restart() {
 template <bool kVals, bool kCountNext>
 void launch_pass_p(const SortArgs& a, int cur, uint32_t p, const SortPlan& plan, uint32_t rot,
                    uint32_t* next_hist, cudaStream_t s, int num_sms) {
+    static const bool top = [] {  // PH0B_TOP_PROBE=0: probe after the publish (ablation)
+        const char* e = getenv("PH0B_TOP_PROBE");
+        return !(e && e[0] == '0');
+    }();
     auto kern = lookback_restart() ? k2_onesweep_p<kVals, kCountNext, true>
+                : top              ? k2_onesweep_p<kVals, kCountNext, false, true>
                                    : k2_onesweep_p<kVals, kCountNext, false>;
     const size_t smem = (size_t)kPTile * 8 * 2 + (size_t)kPTile * 4 * 2;
     static int grid_per_sm = 0;
