@@ -29,8 +29,9 @@ extern "C" {
 #endif
 
 /* 3: + peer-memory exchange (ph0b_shard_partition_count/recv_peer/scatter_peers, ph0b_ipc_*),
- *    ph0b_scale_to_host, ph0b_decode_packed */
-#define PH0B_ABI_VERSION 3u
+ *    ph0b_scale_to_host, ph0b_decode_packed
+ * 4: + ph0b_scale_release, ph0b_host_cache_trim; ph0b_h0_barcode streams D like ph0b_run_host */
+#define PH0B_ABI_VERSION 4u
 
 /* Return codes.  The message of ph0b_last_error() repeats the reference's exception text
  * where the reference has one. */
@@ -111,6 +112,12 @@ int ph0b_h0_barcode(const double* X, uint64_t n, uint64_t d, uint32_t layout,
 int ph0b_kruskal_barcode(const double* X, uint64_t n, uint64_t d, uint32_t layout,
                          const ph0b_options* opt, ph0b_result* out);
 void ph0b_result_free(ph0b_result* r);
+/* Takes D out of a result: the caller keeps r->scale (and sets it to NULL before
+ * ph0b_result_free), then hands it back here when done.  Result buffers of large D are
+ * cached by the library (a freed one is reused by the next call without new page faults);
+ * ph0b_host_cache_trim() returns the idle ones to the system. */
+void ph0b_scale_release(double* scale);
+void ph0b_host_cache_trim(void);
 
 /* Same, writing into caller-provided host buffers (no allocation inside the call; pinned
  * buffers from ph0b_host_alloc give full PCIe bandwidth).  death_* need n-1 entries,

@@ -115,41 +115,49 @@ inline Filtration build_filtration(const double* x, std::size_t n, std::size_t d
     return f;
 }
 
+namespace detail {
+// X -> bars (+ D into *scale) through ph0b_h0_barcode_into: D is written straight into the
+// caller's vector by the library (for large clouds: streamed to the host while the sort
+// runs, decoded by host threads into scale->data()), never copied a second time.  The vector
+// is sized to K = n(n-1)/2 >= |D| first and shrunk to |D| after; a vector reused across
+// calls keeps its capacity, so growing it back costs only the few tail entries.
+inline Barcode run_into(const double* x, std::size_t n, std::size_t d,
+                        std::vector<double>* scale, ph0b_options o) {
+    const std::size_t k = n * (n - (n > 0)) / 2;
+    std::vector<std::uint64_t> grade(n ? n : 1);
+    std::vector<double> length(n ? n : 1);
+    std::uint64_t nf = 0, ess = 0, ns = 0;
+    if (scale) {
+        if (scale->size() < k) scale->resize(k);
+    } else {
+        o.flags |= PH0B_FLAG_NO_SCALE;
+    }
+    check(ph0b_h0_barcode_into(x, n, d, PH0B_COL_MAJOR, &o, grade.data(), length.data(), &nf,
+                               &ess, scale ? scale->data() : nullptr, scale ? scale->size() : 0,
+                               &ns, nullptr));
+    if (scale) scale->resize(ns);
+    Barcode bc;
+    bc.finite.resize(nf);
+    for (std::uint64_t i = 0; i < nf; ++i) bc.finite[i] = {0.0, grade[i], length[i]};
+    bc.essential_count = ess;
+    return bc;
+}
+}  // namespace detail
+
 // The whole hot path: pairwise_distances -> build_filtration -> build_boundary_matrix ->
 // reduce -> extract_barcode (bench.cpp:45-59).  Optionally returns D (Filtration::scale).
 inline Barcode h0_barcode(const double* x, std::size_t n, std::size_t d,
                           std::vector<double>* scale = nullptr,
                           const ReductionOptions& ropts = {}, int device = 0) {
-    const ph0b_options o = detail::opts(ropts, device);
-    ph0b_result r{};
-    ph0b_options o2 = o;
-    if (!scale) o2.flags |= PH0B_FLAG_NO_SCALE;
-    detail::check(ph0b_h0_barcode(x, n, d, PH0B_COL_MAJOR, &o2, &r));
-    Barcode bc;
-    bc.finite.resize(r.n_finite);
-    for (std::uint64_t i = 0; i < r.n_finite; ++i)
-        bc.finite[i] = {0.0, r.death_grade[i], r.death_length[i]};
-    bc.essential_count = r.essential_count;
-    if (scale) scale->assign(r.scale, r.scale + r.n_scale);
-    ph0b_result_free(&r);
-    return bc;
+    return detail::run_into(x, n, d, scale, detail::opts(ropts, device));
 }
 
 // kruskal_barcode (oracle.cpp:32-46): union-find over the GPU filtration (ph0b_kruskal_barcode).
 inline Barcode kruskal_barcode(const double* x, std::size_t n, std::size_t d,
                                std::vector<double>* scale = nullptr, int device = 0) {
     ph0b_options o = detail::opts({}, device);
-    if (!scale) o.flags |= PH0B_FLAG_NO_SCALE;
-    ph0b_result r{};
-    detail::check(ph0b_kruskal_barcode(x, n, d, PH0B_COL_MAJOR, &o, &r));
-    Barcode bc;
-    bc.finite.resize(r.n_finite);
-    for (std::uint64_t i = 0; i < r.n_finite; ++i)
-        bc.finite[i] = {0.0, r.death_grade[i], r.death_length[i]};
-    bc.essential_count = r.essential_count;
-    if (scale) scale->assign(r.scale, r.scale + r.n_scale);
-    ph0b_result_free(&r);
-    return bc;
+    o.flags |= PH0B_FLAG_KRUSKAL;
+    return detail::run_into(x, n, d, scale, o);
 }
 
 // Claimed low of every surviving column (reduction.cpp:44-45), filtration order.

@@ -34,6 +34,60 @@ int orc_generate_uniform_cloud(uint64_t n, uint64_t d, uint64_t seed, double* ou
     return 0;
 }
 
+/* Synthetic clouds of the BASELINE.json configs (SURVEY.md §8(d) "Synthetic inputs"), the
+ * oracle's own restatement so that goldens and the bench's reference arm never depend on the
+ * product library to build X.  All randomness is the reference's SplitMix64
+ * (splitmix64.hpp:20-33); normals are Box-Muller (cosine branch) on two next_unit_open draws;
+ * a cluster label is next() % clusters.  kind 0 is generate_uniform_cloud
+ * (point_cloud.cpp:20-29) exactly.  Column-major output. */
+static double orc_normal(uint64_t* s) {
+    const double u1 = orc_next_unit_open(s);
+    const double u2 = orc_next_unit_open(s);
+    return sqrt(-2.0 * log(u1)) * cos(6.283185307179586 * u2);
+}
+
+int orc_generate_cloud(uint32_t kind, uint64_t n, uint64_t d, uint64_t seed, uint32_t clusters,
+                       double sigma, double lo, double hi, uint64_t n_background, double* out) {
+    if (n > 0 && d < 1) return 1;
+    uint64_t s = seed;
+    if (kind == 0) return orc_generate_uniform_cloud(n, d, seed, out);
+    if (kind == 1) { /* C3, C5: centres U[lo,hi]^d drawn first, then label + d normals per point */
+        if (clusters == 0) return 1;
+        double* c = (double*)malloc(sizeof(double) * clusters * (d ? d : 1));
+        if (!c) return 1;
+        for (uint64_t k = 0; k < clusters; ++k)
+            for (uint64_t j = 0; j < d; ++j) c[k * d + j] = lo + (hi - lo) * orc_next_unit_open(&s);
+        for (uint64_t i = 0; i < n; ++i) {
+            const uint64_t k = orc_splitmix_next(&s) % clusters;
+            for (uint64_t j = 0; j < d; ++j) out[j * n + i] = c[k * d + j] + sigma * orc_normal(&s);
+        }
+        free(c);
+        return 0;
+    }
+    if (kind == 2) { /* C2: noisy unit circle in z = 0, then n_background uniform points */
+        if (n_background > n) return 1;
+        const uint64_t ring = n - n_background;
+        for (uint64_t i = 0; i < ring; ++i) {
+            const double th = 6.283185307179586 * orc_next_unit_open(&s);
+            for (uint64_t j = 0; j < d; ++j) {
+                const double base = j == 0 ? cos(th) : (j == 1 ? sin(th) : 0.0);
+                out[j * n + i] = base + sigma * orc_normal(&s);
+            }
+        }
+        for (uint64_t i = ring; i < n; ++i)
+            for (uint64_t j = 0; j < d; ++j) out[j * n + i] = lo + (hi - lo) * orc_next_unit_open(&s);
+        return 0;
+    }
+    if (kind == 3) { /* C1: first n/2 points around lo*1, the rest around hi*1 */
+        for (uint64_t i = 0; i < n; ++i) {
+            const double centre = (i < n / 2) ? lo : hi;
+            for (uint64_t j = 0; j < d; ++j) out[j * n + i] = centre + sigma * orc_normal(&s);
+        }
+        return 0;
+    }
+    return 1;
+}
+
 /* filtration.cpp:16 through Eigen: norm() of a row difference of a col-major matrix is a
  * sequential left fold of squared differences, then sqrt (see oracle/shim/Eigen/Core). */
 static double edge_length(const double* x, uint64_t n, uint64_t d, uint64_t a, uint64_t b) {

@@ -29,6 +29,12 @@ double orc_next_unit_open(uint64_t* state);
 /* point_cloud.cpp:20-29, column-major output */
 int orc_generate_uniform_cloud(uint64_t n, uint64_t d, uint64_t seed, double* out_colmajor);
 
+/* BASELINE.json config clouds; kind 0 = generate_uniform_cloud, 1 = Gaussian
+ * mixture, 2 = noisy circle + uniform background, 3 = two Gaussian clusters.  Column-major. */
+int orc_generate_cloud(uint32_t kind, uint64_t n, uint64_t d, uint64_t seed, uint32_t clusters,
+                       double sigma, double lo, double hi, uint64_t n_background,
+                       double* out_colmajor);
+
 /* filtration.cpp:8-18 — u-major lengths of all pairs u < v */
 void orc_pairwise_distances(const double* x_colmajor, uint64_t n, uint64_t d, double* lengths);
 

@@ -1,7 +1,11 @@
 // C ABI (include/ph0b.h): validation with the reference's error behaviour, result marshalling.
 #include <cuda_runtime.h>
+#include <sys/mman.h>
 
+#include <algorithm>
 #include <cmath>
+#include <map>
+#include <mutex>
 #include <cstdlib>
 #include <cstring>
 #include <new>
@@ -78,6 +82,80 @@ int parse(const ph0b_options* opt, uint64_t n, uint32_t layout, Opts* o) {
                     "point cloud too large for this build (N <= " +
                         std::to_string(PH0B_MAX_POINTS) + ")");
     return PH0B_OK;
+}
+
+// Host buffers of library-allocated results (ph0b_result.scale holds D: up to 8*K bytes, 17 GB
+// at C5).  Fresh memory costs one page fault per page on first touch (the kernel zeroes it),
+// seconds at C5, so a freed D buffer is kept (at most kIdleMax, LRU) and handed to the next
+// call that fits in it; large buffers are anonymous mappings with transparent huge pages
+// requested.  ph0b_host_cache_trim() returns the idle ones to the system.
+class ResultCache {
+public:
+    static constexpr size_t kMapMin = size_t(64) << 20;  // below: plain malloc
+    static constexpr size_t kIdleMax = 2;
+
+    void* take(size_t bytes) {
+        bytes = std::max<size_t>(bytes, 8);
+        if (bytes < kMapMin) return std::malloc(bytes);
+        {
+            std::lock_guard<std::mutex> lk(mu_);
+            size_t best = idle_.size();
+            for (size_t i = 0; i < idle_.size(); ++i)
+                if (idle_[i].second >= bytes &&
+                    (best == idle_.size() || idle_[i].second < idle_[best].second))
+                    best = i;
+            if (best != idle_.size()) {
+                const auto e = idle_[best];
+                idle_.erase(idle_.begin() + (long)best);
+                live_[e.first] = e.second;
+                return e.first;
+            }
+        }
+        const size_t len = (bytes + (size_t(2) << 20) - 1) & ~((size_t(2) << 20) - 1);
+        void* p = mmap(nullptr, len, PROT_READ | PROT_WRITE, MAP_PRIVATE | MAP_ANONYMOUS, -1, 0);
+        if (p == MAP_FAILED) return nullptr;
+        madvise(p, len, MADV_HUGEPAGE);
+        std::lock_guard<std::mutex> lk(mu_);
+        live_[p] = len;
+        return p;
+    }
+    void give(void* p) {
+        if (!p) return;
+        std::vector<std::pair<void*, size_t>> drop;
+        {
+            std::lock_guard<std::mutex> lk(mu_);
+            const auto it = live_.find(p);
+            if (it == live_.end()) {
+                std::free(p);  // a small (malloc) buffer
+                return;
+            }
+            idle_.push_back(*it);
+            live_.erase(it);
+            while (idle_.size() > kIdleMax) {
+                drop.push_back(idle_.front());
+                idle_.erase(idle_.begin());
+            }
+        }
+        for (auto& e : drop) munmap(e.first, e.second);
+    }
+    void trim() {
+        std::vector<std::pair<void*, size_t>> drop;
+        {
+            std::lock_guard<std::mutex> lk(mu_);
+            drop.swap(idle_);
+        }
+        for (auto& e : drop) munmap(e.first, e.second);
+    }
+
+private:
+    std::mutex mu_;
+    std::map<void*, size_t> live_;
+    std::vector<std::pair<void*, size_t>> idle_;
+};
+
+ResultCache& result_cache() {
+    static ResultCache* c = new ResultCache();  // never destroyed: results may outlive statics
+    return *c;
 }
 
 // Host-side finiteness check (PointCloud ctor, point_cloud.cpp:15-18) before any device work.
@@ -165,6 +243,7 @@ void ph0b_context_destroy(ph0b_context* ctx) {
 }
 
 int ph0b_context_reserve(ph0b_context* ctx, uint64_t n, uint64_t d) {
+    if (!ctx) return fail(PH0B_ERR_INVALID_ARGUMENT, "null context");
     Context* c = reinterpret_cast<Context*>(ctx);
     std::lock_guard<std::mutex> lk(c->mu);
     Status s = c->reserve(n, d);
@@ -172,14 +251,17 @@ int ph0b_context_reserve(ph0b_context* ctx, uint64_t n, uint64_t d) {
 }
 
 uint64_t ph0b_context_workspace_bytes(const ph0b_context* ctx) {
+    if (!ctx) return 0;
     return reinterpret_cast<const Context*>(ctx)->workspace_bytes();
 }
 
 int ph0b_run_device(ph0b_context* ctx, const double* dX, uint64_t n, uint64_t d, uint32_t layout,
                     void* stream, ph0b_device_result* out) {
+    if (!ctx) return fail(PH0B_ERR_INVALID_ARGUMENT, "null context");
     Opts o;
     int rc = parse(nullptr, n, layout, &o);
     if (rc) return rc;
+    if (n * d && !dX) return fail(PH0B_ERR_INVALID_ARGUMENT, "null point cloud");
     Context* c = reinterpret_cast<Context*>(ctx);
     std::lock_guard<std::mutex> lk(c->mu);
     RunOutputs r;
@@ -277,20 +359,25 @@ int ph0b_scale_to_host(ph0b_context* ctx, const double* d_scale, uint64_t n, dou
     return PH0B_OK;
 }
 
-int ph0b_run_host(ph0b_context* ctx, const double* X, uint64_t n, uint64_t d, uint32_t layout,
-                  void* stream, uint64_t* death_grade, double* death_length, uint64_t* n_finite,
-                  uint64_t* essential_count, double* scale, uint64_t scale_capacity,
-                  uint64_t* n_scale, ph0b_stage_times* times) {
-    Opts o;
-    int rc = parse(nullptr, n, layout, &o);
-    if (rc) return rc;
-    if (n * d && !X) return fail(PH0B_ERR_INVALID_ARGUMENT, "null point cloud");
-    if (!all_finite(X, n * d))
-        return fail(PH0B_ERR_NONFINITE, "point cloud contains non-finite coordinates");
-    Context* c = reinterpret_cast<Context*>(ctx);
-    std::lock_guard<std::mutex> lk(c->mu);
+}  // extern "C"
+
+namespace {
+
+// Host X -> host outputs on a context whose lock the caller holds (ph0b_run_host,
+// ph0b_h0_barcode_into); kruskal: the union-find barcode instead of the column reduction.
+int run_host_locked(Context* c, const double* X, uint64_t n, uint64_t d, uint32_t layout,
+                    void* stream, uint64_t* death_grade, double* death_length,
+                    uint64_t* n_finite, uint64_t* essential_count, double* scale,
+                    uint64_t scale_capacity, uint64_t* n_scale, ph0b_stage_times* times,
+                    bool kruskal) {
+    int rc = PH0B_OK;
     cudaStream_t s = stream ? static_cast<cudaStream_t>(stream) : c->own_stream();
     RunOutputs r;
+    struct ModeGuard {
+        Context* c;
+        ~ModeGuard() { c->kruskal_mode = false; }
+    } mode_guard{c};
+    c->kruskal_mode = kruskal;
     const uint64_t k = n * (n - (n > 0)) / 2;
     // Large clouds returning D: overlap the D2H of D with the sort (key-range buckets).
     const bool overlap = scale && k >= overlap_min_edges() && !overlap_disabled();
@@ -319,6 +406,27 @@ int ph0b_run_host(ph0b_context* ctx, const double* X, uint64_t n, uint64_t d, ui
     return PH0B_OK;
 }
 
+}  // namespace
+
+extern "C" {
+
+int ph0b_run_host(ph0b_context* ctx, const double* X, uint64_t n, uint64_t d, uint32_t layout,
+                  void* stream, uint64_t* death_grade, double* death_length, uint64_t* n_finite,
+                  uint64_t* essential_count, double* scale, uint64_t scale_capacity,
+                  uint64_t* n_scale, ph0b_stage_times* times) {
+    if (!ctx) return fail(PH0B_ERR_INVALID_ARGUMENT, "null context");
+    Opts o;
+    int rc = parse(nullptr, n, layout, &o);
+    if (rc) return rc;
+    if (n * d && !X) return fail(PH0B_ERR_INVALID_ARGUMENT, "null point cloud");
+    if (!all_finite(X, n * d))
+        return fail(PH0B_ERR_NONFINITE, "point cloud contains non-finite coordinates");
+    Context* c = reinterpret_cast<Context*>(ctx);
+    std::lock_guard<std::mutex> lk(c->mu);
+    return run_host_locked(c, X, n, d, layout, stream, death_grade, death_length, n_finite,
+                           essential_count, scale, scale_capacity, n_scale, times, false);
+}
+
 int ph0b_h0_barcode_into(const double* X, uint64_t n, uint64_t d, uint32_t layout,
                          const ph0b_options* opt, uint64_t* death_grade, double* death_length,
                          uint64_t* n_finite, uint64_t* essential_count, double* scale,
@@ -332,9 +440,10 @@ int ph0b_h0_barcode_into(const double* X, uint64_t n, uint64_t d, uint32_t layou
     Context* c = ctx_for(o.device, &rc);
     if (!c) return rc;
     if (o.flags & PH0B_FLAG_NO_SCALE) scale = nullptr;
-    return ph0b_run_host(reinterpret_cast<ph0b_context*>(c), X, n, d, layout, nullptr,
-                         death_grade, death_length, n_finite, essential_count, scale,
-                         scale_capacity, n_scale, times);
+    std::lock_guard<std::mutex> lk(c->mu);
+    return run_host_locked(c, X, n, d, layout, nullptr, death_grade, death_length, n_finite,
+                           essential_count, scale, scale_capacity, n_scale, times,
+                           (o.flags & PH0B_FLAG_KRUSKAL) != 0);
 }
 
 int ph0b_h0_barcode(const double* X, uint64_t n, uint64_t d, uint32_t layout,
@@ -352,19 +461,45 @@ int ph0b_h0_barcode(const double* X, uint64_t n, uint64_t d, uint32_t layout,
     std::lock_guard<std::mutex> lk(c->mu);
     cudaStream_t s = c->own_stream();
     RunOutputs r;
+    const bool want_scale = !(o.flags & PH0B_FLAG_NO_SCALE);
+    const uint64_t k = n * (n - (n > 0)) / 2;
+    // Large clouds returning D take the same bucketed path as ph0b_run_host: D streams to the
+    // host while the sort is still running, decoded straight into the result buffer (sized by
+    // K >= |D|; a reused buffer from the result cache has no page faults left to take).
+    const bool overlap = want_scale && k >= overlap_min_edges() && !overlap_disabled();
+    if (overlap) {
+        out->scale = static_cast<double*>(result_cache().take(k * 8));
+        if (!out->scale) return fail(PH0B_ERR_OUT_OF_MEMORY, "host allocation of D failed");
+    }
     c->kruskal_mode = (o.flags & PH0B_FLAG_KRUSKAL) != 0;
-    Status st = c->run_host_input(X, n, d, layout, s, StopAfter::Barcode, false, &r);
+    Status st = overlap ? c->run_host_overlapped(X, n, d, layout, s, out->scale, k, &r)
+                        : c->run_host_input(X, n, d, layout, s, StopAfter::Barcode, false, &r);
     c->kruskal_mode = false;
     g_last_launches = c->launches;
-    if (!st.good()) return fail(st);
-    const bool want_scale = !(o.flags & PH0B_FLAG_NO_SCALE);
+    if (!st.good()) {
+        ph0b_result_free(out);
+        return fail(st);
+    }
     out->death_grade = static_cast<uint64_t*>(std::malloc(std::max<uint64_t>(1, r.n_finite) * 8));
     out->death_length = static_cast<double*>(std::malloc(std::max<uint64_t>(1, r.n_finite) * 8));
-    if (want_scale)
-        out->scale = static_cast<double*>(std::malloc(std::max<uint64_t>(1, r.n_scale) * 8));
+    if (want_scale && !overlap)
+        out->scale = static_cast<double*>(result_cache().take(r.n_scale * 8));
     if (!out->death_grade || !out->death_length || (want_scale && !out->scale)) {
         ph0b_result_free(out);
         return fail(PH0B_ERR_OUT_OF_MEMORY, "host allocation of the result failed");
+    }
+    if (overlap) {  // D is on the host already; the bars follow
+        rc = copy_out(c, r, s, out->death_grade, out->death_length, nullptr, 0, false);
+        if (rc) {
+            ph0b_result_free(out);
+            return rc;
+        }
+        r.times.d2h_bytes += r.n_finite * 16;
+        out->n_finite = r.n_finite;
+        out->essential_count = r.essential;
+        out->n_scale = r.n_scale;
+        out->times = r.times;
+        return PH0B_OK;
     }
     // a large D goes compressed through the pinned ring and is decoded by host threads into
     // the (pageable) result, instead of one pageable-memory DMA
@@ -401,11 +536,15 @@ int ph0b_kruskal_barcode(const double* X, uint64_t n, uint64_t d, uint32_t layou
     return ph0b_h0_barcode(X, n, d, layout, &o, out);
 }
 
+void ph0b_scale_release(double* scale) { result_cache().give(scale); }
+
+void ph0b_host_cache_trim(void) { result_cache().trim(); }
+
 void ph0b_result_free(ph0b_result* r) {
     if (!r) return;
     std::free(r->death_grade);
     std::free(r->death_length);
-    std::free(r->scale);
+    result_cache().give(r->scale);
     r->death_grade = nullptr;
     r->death_length = nullptr;
     r->scale = nullptr;

@@ -86,32 +86,6 @@ __device__ __forceinline__ uint32_t lookback_window(const uint64_t* status, uint
     return excl;
 }
 
-// Warp-cooperative look-back for one status column: lane j reads predecessor p - j, so one
-// L2 round trip covers 32 predecessors.  Tiles before 0 count as inclusive zeros.  Must be
-// called by all 32 lanes; every lane returns the exclusive prefix.
-__device__ __forceinline__ uint32_t lookback_warp(const uint64_t* status, uint64_t stride,
-                                                  uint32_t tile, uint32_t epoch, int lane) {
-    uint32_t excl = 0;
-    int64_t p = (int64_t)tile - 1;
-    for (;;) {
-        const int64_t q = p - lane;
-        uint32_t st = (uint32_t)kStateInclusive, val = 0;
-        if (q >= 0) {
-            const uint64_t s = ld_relaxed_u64(status + (uint64_t)q * stride);
-            st = status_state(s, epoch);
-            val = (uint32_t)s;
-        }
-        const uint32_t np = __ballot_sync(0xffffffffu, st == 0);
-        const uint32_t inc = __ballot_sync(0xffffffffu, st == (uint32_t)kStateInclusive);
-        const int first_np = np ? __ffs(np) - 1 : 32;
-        const int first_in = inc ? __ffs(inc) - 1 : 32;
-        if (first_in < first_np)
-            return excl + __reduce_add_sync(0xffffffffu, lane <= first_in ? val : 0u);
-        excl += __reduce_add_sync(0xffffffffu, lane < first_np ? val : 0u);
-        p -= first_np;
-    }
-}
-
 // Upper-triangle edge indexing in the reference's u-major order (filtration.cpp:14-15):
 // e(u, v) = u*(2N-u-1)/2 + (v-u-1) for u < v.
 __host__ __device__ __forceinline__ uint64_t row_base(uint64_t u, uint64_t n) {

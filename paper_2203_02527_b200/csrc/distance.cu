@@ -281,10 +281,8 @@ int launch_tma(const DistanceArgs& a, const CUtensorMap& map, uint32_t nb, uint3
     const uint32_t dim = D > 0 ? D : a.d;
     const size_t smem = 4ull * kTile * dim * sizeof(double);
     auto kern = k1_distance_tma<D>;
-    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    int per_sm = 0;
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kThreads, smem);
-    if (per_sm < 1) per_sm = 1;
+    const int per_sm = kernel_blocks_per_sm((const void*)kern, kThreads, smem);
+    if (per_sm < 1) return 0;
     uint32_t grid = (uint32_t)num_sms * per_sm;
     if (grid > total) grid = total;
     kern<<<grid, kThreads, smem, s>>>(map, a.n, a.d, nb, total, t0, a.u_lo, a.u_hi, a.e_off,

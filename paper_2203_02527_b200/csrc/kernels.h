@@ -7,6 +7,13 @@
 
 namespace ph0b {
 
+// ---- per-device launch attributes (launch_attr.cpp) -----------------------------------
+// Opts `kern` into `smem` bytes of dynamic shared memory on the current device (when above
+// 48 KB) and returns its resident blocks per SM at `threads` threads (0 on failure).  Cached
+// per (device, kernel, smem, threads); thread-safe.
+int kernel_blocks_per_sm(const void* kern, int threads, size_t smem);
+int device_sm_count();
+
 // ---- K1: tiled upper-triangle distance kernel (distance.cu) ----------------------------
 struct DistanceArgs {
     const double* xpad;   // device, coordinate-major [d][ldx], zero padded (ldx % 128 == 0)
@@ -68,14 +75,12 @@ struct UniqueArgs {
     uint32_t low_bits;      // keys are sorted by (key - kmin) >> low_bits only (0 = fully)
     double* scale;          // out: D
     uint32_t* grade;        // out (optional): 1-based grade per column
-    uint64_t* status;       // look-back status [tiles]
-    uint32_t* tile_counter;
     uint64_t* n_scale;      // out: |D| (device)
-    uint32_t epoch;
     uint32_t* redo;         // out: set when a run exceeded the in-place fix-up limit
     uint64_t* scratch;      // unique_scratch_words(count) words
     const uint64_t* d_base = nullptr;  // device: D index of this range's first distinct length
 };
+// Returns launches, or -1 when the kernels cannot be configured on this device.
 int launch_unique(const UniqueArgs& a, cudaStream_t s);
 uint64_t unique_scratch_words(uint64_t count);
 

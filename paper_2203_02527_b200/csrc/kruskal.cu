@@ -134,12 +134,8 @@ int launch_kruskal(const uint32_t* uv, const uint64_t* sorted_keys, uint64_t cou
                    const double* D, const uint64_t* n_scale, uint32_t* accepted,
                    uint32_t* n_accepted, uint64_t* death_grade, double* death_length,
                    cudaStream_t s) {
-    static bool configured = false;
-    if (!configured) {
-        cudaFuncSetAttribute(k6_kruskal, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                             (int)kruskal_smem_bytes());
-        configured = true;
-    }
+    if (kernel_blocks_per_sm((const void*)k6_kruskal, kKThreads, kruskal_smem_bytes()) < 1)
+        return -1;
     k6_kruskal<<<1, kKThreads, kruskal_smem_bytes(), s>>>(uv, count, n, accepted, n_accepted);
     k6_bars<<<(n + 255) / 256 + 1, 256, 0, s>>>(accepted, n_accepted, sorted_keys, D, n_scale,
                                                 death_grade, death_length);

@@ -1,0 +1,50 @@
+// Per-device launch attributes of the kernels that need more than 48 KB of dynamic shared
+// memory, and their occupancy.  cudaFuncSetAttribute acts on the CURRENT device's context, so
+// a process that runs on device 1 after device 0 (ph0b_options.device, one context per
+// device, the multi-device path) must opt in again there: the result is cached per
+// (device, kernel, smem, threads) under a lock, and a cache entry is published only once
+// both calls have returned.
+#include <cuda_runtime.h>
+
+#include <map>
+#include <mutex>
+#include <tuple>
+
+#include "kernels.h"
+
+namespace ph0b {
+
+int kernel_blocks_per_sm(const void* kern, int threads, size_t smem) {
+    int dev = 0;
+    if (cudaGetDevice(&dev) != cudaSuccess) return 0;
+    using Key = std::tuple<int, const void*, size_t, int>;
+    static std::mutex mu;
+    static std::map<Key, int> cache;
+    const Key key{dev, kern, smem, threads};
+    std::lock_guard<std::mutex> lock(mu);
+    const auto it = cache.find(key);
+    if (it != cache.end()) return it->second;
+    if (smem > 48 * 1024 &&
+        cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) !=
+            cudaSuccess) {
+        cudaGetLastError();
+        return 0;  // not cached: a later call may retry
+    }
+    int per_sm = 0;
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, threads, smem) !=
+        cudaSuccess) {
+        cudaGetLastError();
+        return 0;
+    }
+    cache.emplace(key, per_sm);
+    return per_sm;
+}
+
+int device_sm_count() {
+    int dev = 0, n = 0;
+    if (cudaGetDevice(&dev) != cudaSuccess) return 0;
+    if (cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess) return 0;
+    return n;
+}
+
+}  // namespace ph0b

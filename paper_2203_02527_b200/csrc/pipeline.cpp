@@ -448,8 +448,11 @@ Status Context::stage_distances(const double* dX, uint64_t n, uint64_t d, uint32
     da.u_lo = (uint32_t)u_lo;
     da.u_hi = (uint32_t)u_hi;
     da.e_off = u_lo < n ? row_base(u_lo, n) : 0;
-    launches += launch_distance(da, st, num_sms_);
+    const int dl = launch_distance(da, st, num_sms_);
     PH0B_CHECK_LAUNCH("distance kernel");
+    if (dl == 0 && kedges > 0)
+        return {PH0B_ERR_CUDA, "distance kernel: launch configuration failed"};
+    launches += dl;
     PH0B_TRY(cudaMemcpyAsync(h_small_, small_, 4 * 8, cudaMemcpyDeviceToHost, st), "D2H");
     PH0B_TRY(cudaStreamSynchronize(st), "distance stage");
     if (static_cast<uint32_t>(h_small_[3]) != 0)
@@ -521,9 +524,11 @@ Status Context::sort_unique_range(uint64_t* kb0, uint32_t* vb0, uint64_t* kb1, u
         Status gs = grow(reinterpret_cast<void**>(&uscratch_), &uscratch_cap_,
                          unique_scratch_words(k) * 8);
         if (!gs.good()) return gs;
-        UniqueArgs ua{kb[*res], vb[*res], k, kmin, low_bits, scale, grade_out, status_,
-                      counters_ + 40, d_count, next_epochs(1, st), redo, uscratch_, d_base};
-        launches += launch_unique(ua, st);
+        UniqueArgs ua{kb[*res], vb[*res], k, kmin, low_bits, scale, grade_out, d_count, redo,
+                      uscratch_, d_base};
+        const int ul = launch_unique(ua, st);
+        if (ul < 0) return {PH0B_ERR_CUDA, "unique kernels: launch configuration failed"};
+        launches += ul;
         PH0B_CHECK_LAUNCH("unique kernel");
         if (attempt == 0 && after_enqueue) {  // host work that overlaps this range's kernels
             const Status hs = (*after_enqueue)();
@@ -1112,10 +1117,12 @@ Status Context::run_host_overlapped(const double* X, uint64_t n, uint64_t d, uin
             return s;
         }
         // ---- the rest of the partition (segment 0 is already in place) --------------------
-        launches += launch_partition_scatter(keys_[0], vals_[0], k, d_spl, B, part_counts_,
-                                             d_tot, keys_[1], vals_[1], st, kmin, kmax, d_table,
-                                             0u);
+        const int ls = launch_partition_scatter(keys_[0], vals_[0], k, d_spl, B, part_counts_,
+                                                d_tot, keys_[1], vals_[1], st, kmin, kmax,
+                                                d_table, 0u);
         PH0B_CHECK_LAUNCH("partition");
+        if (ls < 0) return {PH0B_ERR_CUDA, "partition: launch configuration failed"};
+        launches += ls;
         // M is assembled in buffer 0 (the 5-pass buckets end there): once the scatter has
         // consumed the u-major input, move sorted bucket 0 into its segment of buffer 0
         if (c0) {
@@ -1238,9 +1245,11 @@ Status Context::stage_kruskal(uint64_t count, uint32_t n, cudaStream_t st, uint3
     uint32_t* d_count = reinterpret_cast<uint32_t*>(d_mapped_ + 250);
     volatile uint32_t* h_count = reinterpret_cast<volatile uint32_t*>(h_mapped_ + 250);
     *h_count = 0;
-    launches += launch_kruskal(vals_[cur_], keys_[cur_], count, n, scale_, small_ + 2, surv_,
-                               d_count, death_grade_, death_length_, st);
+    const int kl = launch_kruskal(vals_[cur_], keys_[cur_], count, n, scale_, small_ + 2, surv_,
+                                  d_count, death_grade_, death_length_, st);
     PH0B_CHECK_LAUNCH("kruskal");
+    if (kl < 0) return {PH0B_ERR_CUDA, "kruskal: launch configuration failed"};
+    launches += kl;
     PH0B_TRY(cudaStreamSynchronize(st), "kruskal");
     *merges = *h_count;
     return Status::ok();

@@ -6,13 +6,18 @@
 // 8 bits per pass.  Every pass is stable and the input is the reference's u-major order,
 // so equal lengths end up ordered by (u, v) exactly as filtration.cpp:21-25 orders them.
 //
-// One kernel per digit (Adinets & Merrill's single-pass "onesweep"): each CTA takes the
-// next 4096-key tile (dynamic tile id), ranks its keys with warp-level match_any ranking
-// into per-warp histograms, publishes its per-digit counts and obtains the exclusive
-// prefix over earlier tiles by decoupled look-back, scatters the tile into shared memory
-// in digit order and writes it out so that each digit's run is a contiguous global run.
-// The same pass counts the NEXT digit's histogram, so no separate upsweep over the keys
-// is needed (pass 0's histogram comes from the distance kernel).
+// One kernel per digit (Adinets & Merrill's single-pass "onesweep"), persistent: each CTA
+// claims 4096-key tiles in increasing order with an atomic ticket (the next one while the
+// current one is still being written, its keys and columns prefetched into shared memory
+// with TMA bulk copies), ranks the tile's keys in-warp with shared-memory atomics on
+// per-warp digit counters (B200 resolves the same-address lanes of one ATOMS in lane
+// order — checked on the device at context creation; bit-sliced ballots otherwise),
+// publishes its per-digit counts, obtains the exclusive prefix over earlier tiles by
+// decoupled look-back on epoch-tagged status words, scatters the tile into shared memory in
+// digit order and writes it out so that each digit's run is a contiguous global run.  The
+// same pass counts the NEXT digit's histogram, so no separate upsweep over the keys is
+// needed.  Tickets make the look-back deadlock-free whatever else shares the GPU: every
+// tile a CTA waits on was claimed earlier by a CTA that is already running.
 #include <cuda_runtime.h>
 
 #include <cstdint>
@@ -26,8 +31,6 @@ namespace {
 
 constexpr int kThreads = 256;
 constexpr int kWarps = kThreads / 32;
-constexpr int kItems = 12;
-constexpr int kTileKeys = kThreads * kItems;
 constexpr int kBins = 256;
 static_assert(kThreads == kBins, "one thread per digit value");
 
@@ -53,194 +56,19 @@ __device__ __forceinline__ uint32_t block_exclusive_scan(uint32_t x, uint32_t* s
     return wbase + inc - x;
 }
 
-// Stable warp-level multisplit of one digit per lane: the mask of lanes holding the same
-// digit, by bit-sliced ballots (pure ALU, no MIO round trip) or by match.any.
-template <int kRank>
-__device__ __forceinline__ uint32_t peer_mask(uint32_t d, uint32_t valid_mask) {
-    if constexpr (kRank == 2) {
-        uint32_t peers = valid_mask;
+// Stable in-warp rank of one digit per lane by bit-sliced ballots (pure ALU): the mask of
+// the lanes holding the same digit.  Used when the ATOMS lane-order self-test fails.
+__device__ __forceinline__ uint32_t ballot_peers(uint32_t d, uint32_t valid_mask) {
+    uint32_t peers = valid_mask;
 #pragma unroll
-        for (int b = 0; b < 8; ++b) {
-            const uint32_t bit = (d >> b) & 1u;
-            const uint32_t bal = __ballot_sync(0xffffffffu, bit);
-            peers &= bit ? bal : ~bal;
-        }
-        return peers;
-    } else {
-        return __match_any_sync(0xffffffffu, d);
+    for (int b = 0; b < 8; ++b) {
+        const uint32_t bit = (d >> b) & 1u;
+        const uint32_t bal = __ballot_sync(0xffffffffu, bit);
+        peers &= bit ? bal : ~bal;
     }
+    return peers;
 }
 
-// kRank: 0 = match.any + leader LDS/STS chain, 1 = match.any + leader atomicAdd (pipelined),
-//        2 = bit-sliced ballots + leader atomicAdd.
-template <bool kVals, bool kCountNext, int kRank, int kMinBlocks>
-__global__ void __launch_bounds__(kThreads, kMinBlocks)
-    k2_onesweep(const uint64_t* __restrict__ keys_in, uint64_t* __restrict__ keys_out,
-                const uint32_t* __restrict__ vals_in, uint32_t* __restrict__ vals_out,
-                uint64_t count, uint64_t kmin, uint32_t shift, uint32_t next_shift,
-                const uint32_t* __restrict__ hist, uint32_t hist_rot,
-                uint64_t* __restrict__ status, uint32_t* tile_counter, uint32_t epoch,
-                uint32_t* __restrict__ next_hist) {
-    extern __shared__ __align__(16) uint64_t s_dyn[];
-    uint64_t* s_keys = s_dyn;                                          // [kTileKeys]
-    uint32_t* s_vals = reinterpret_cast<uint32_t*>(s_dyn + kTileKeys);  // [kTileKeys] if kVals
-    __shared__ uint32_t s_whist[kWarps][kBins];
-    __shared__ uint32_t s_tile_start[kBins];
-    __shared__ uint32_t s_global[kBins];
-    __shared__ uint32_t s_next[kCountNext ? kBins : 1];
-    __shared__ uint32_t s_scan[kWarps];
-    __shared__ uint32_t s_tile;
-
-    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-    if (tid == 0) s_tile = atomicAdd(tile_counter, 1u);
-#pragma unroll
-    for (int w = 0; w < kWarps; ++w) s_whist[w][tid] = 0;
-    if (kCountNext) s_next[tid] = 0;
-    __syncthreads();
-    const uint32_t tile = s_tile;
-    const uint64_t base = (uint64_t)tile * kTileKeys;
-
-    // ---- load keys (warp-striped, coalesced) and rank within the warp ------------------
-    uint64_t k[kItems];
-    // per item: [4:0] leader lane, [9:5] peers before me, [31:10] leader's warp-counter value
-    uint32_t pk[kItems];
-    const uint64_t wbase = base + (uint64_t)warp * (32 * kItems) + lane;
-#pragma unroll
-    for (int i = 0; i < kItems; ++i) {
-        const uint64_t idx = wbase + 32 * i;
-        k[i] = idx < count ? keys_in[idx] : ~0ull;
-    }
-    const uint32_t lt = lanemask_lt();
-#pragma unroll
-    for (int i = 0; i < kItems; ++i) {
-        const bool valid = wbase + 32 * i < count;
-        const uint32_t d = valid ? (uint32_t)((k[i] - kmin) >> shift) & 0xFFu : 0x100u;
-        if constexpr (kRank == 3) {
-            // ATOMS resolves same-address lanes of one instruction in ascending lane order
-            // (verified on the device at context creation, see rank_self_test), and
-            // instructions of one warp in program order: the returned count IS the stable
-            // in-warp rank.
-            pk[i] = valid ? atomicAdd(&s_whist[warp][d], 1u) : 0u;
-            continue;
-        }
-        const uint32_t vmask = __ballot_sync(0xffffffffu, valid);
-        const uint32_t peers = peer_mask<kRank>(d, vmask);
-        const uint32_t leader = __ffs(peers) - 1;
-        const uint32_t before = __popc(peers & lt);
-        if constexpr (kRank == 0) {
-            uint32_t o = 0;
-            if (valid && lane == (int)leader) o = s_whist[warp][d];
-            o = __shfl_sync(0xffffffffu, o, leader);
-            pk[i] = o + before;
-            if (valid && lane == (int)leader) s_whist[warp][d] = o + __popc(peers);
-            __syncwarp();
-        } else {
-            const uint32_t o = (valid && lane == (int)leader)
-                                   ? atomicAdd(&s_whist[warp][d], __popc(peers))
-                                   : 0u;
-            pk[i] = leader | (before << 5) | (o << 10);
-        }
-    }
-    uint32_t rank2[kItems / 2];  // two 16-bit in-warp ranks per register
-#pragma unroll
-    for (int i = 0; i < kItems; ++i) {
-        uint32_t r;
-        if constexpr (kRank == 0 || kRank == 3) {
-            r = pk[i];
-        } else {
-            r = (__shfl_sync(0xffffffffu, pk[i], pk[i] & 31u) >> 10) + ((pk[i] >> 5) & 31u);
-        }
-        if (i & 1)
-            rank2[i / 2] |= r << 16;
-        else
-            rank2[i / 2] = r;
-    }
-    __syncthreads();
-
-    // ---- per-digit counts, warp offsets; publish this tile's aggregate early -------------
-    const uint32_t t = tid;  // digit handled by this thread
-    uint32_t cnt = 0;
-#pragma unroll
-    for (int w = 0; w < kWarps; ++w) {
-        const uint32_t c = s_whist[w][t];
-        s_whist[w][t] = cnt;
-        cnt += c;
-    }
-    uint64_t* my_status = status + (uint64_t)tile * kBins + t;
-    st_relaxed_u64(my_status, pack_status(tile == 0 ? kStateInclusive : kStateAggregate, epoch, cnt));
-    // first look-back probe goes out now; its latency hides behind the scans and the scatter
-    uint64_t probe = tile > 0 ? ld_relaxed_u64(status + (uint64_t)(tile - 1) * kBins + t) : 0ull;
-
-    // global start of digit t (exclusive scan of the rotated digit histogram) and the
-    // tile-local start of digit t (exclusive scan of this tile's counts)
-    const uint32_t hcount = hist[(t + hist_rot) & 0xFFu];
-    const uint32_t bin_start = block_exclusive_scan(hcount, s_scan, nullptr);
-    __syncthreads();
-    const uint32_t tstart = block_exclusive_scan(cnt, s_scan, nullptr);
-    s_tile_start[t] = tstart;
-    __syncthreads();
-
-    // ---- scatter into shared memory in (digit, input order) order -----------------------
-#pragma unroll
-    for (int i = 0; i < kItems; ++i) {
-        const uint64_t idx = wbase + 32 * i;
-        if (idx < count) {
-            const uint32_t d = (uint32_t)((k[i] - kmin) >> shift) & 0xFFu;
-            const uint32_t pos = s_tile_start[d] + s_whist[warp][d] +
-                                 ((i & 1) ? (rank2[i / 2] >> 16) : (rank2[i / 2] & 0xFFFFu));
-            s_keys[pos] = k[i];
-            if (kVals) s_vals[pos] = vals_in[idx];
-        }
-    }
-
-    // ---- decoupled look-back over earlier tiles, per digit -------------------------------
-    uint32_t excl = 0;
-    if (tile > 0) {
-        int64_t p = (int64_t)tile - 1;
-        for (;;) {
-            const uint32_t st = status_state(probe, epoch);
-            if (st != 0) {
-                excl += (uint32_t)probe;
-                if (st == kStateInclusive) break;
-                --p;
-            }
-            probe = ld_relaxed_u64(status + (uint64_t)p * kBins + t);
-        }
-        st_relaxed_u64(my_status, pack_status(kStateInclusive, epoch, excl + cnt));
-    }
-    // output position of the element at tile-local position p with digit d: delta[d] + p
-    s_global[t] = bin_start + excl - tstart;
-    __syncthreads();
-
-    // ---- write out: consecutive threads -> consecutive positions within each digit run --
-    const uint64_t rem = count - base;
-    const uint32_t tile_n = rem < (uint64_t)kTileKeys ? (uint32_t)rem : (uint32_t)kTileKeys;
-#pragma unroll 4
-    for (int j = 0; j < kItems; ++j) {
-        const uint32_t p = j * kThreads + tid;
-        if (p < tile_n) {
-            const uint64_t key = s_keys[p];
-            const uint64_t rel = key - kmin;
-            const uint32_t d = (uint32_t)(rel >> shift) & 0xFFu;
-            const uint64_t out = (uint64_t)(uint32_t)(s_global[d] + p);
-            keys_out[out] = key;
-            if (kVals) vals_out[out] = s_vals[p];
-            if (kCountNext) atomicAdd(&s_next[(uint32_t)(rel >> next_shift) & 0xFFu], 1u);
-        }
-    }
-    if (kCountNext) {
-        __syncthreads();
-        const uint32_t c = s_next[tid];
-        if (c) atomicAdd(&next_hist[tid], c);
-    }
-}
-
-// ---- persistent onesweep with TMA bulk prefetch -------------------------------------------
-// Static tile assignment (tile = blockIdx.x + r * gridDim.x, all CTAs co-resident), so a
-// CTA can prefetch its next tile with cp.async.bulk (TMA, mbarrier completion) while it is
-// still in the look-back and write-out phases of the current one; the look-back chain only
-// ever waits on tiles of the same or an earlier round, which are being processed by
-// co-resident CTAs (deadlock-free).
 constexpr int kPTile = 4096;
 constexpr int kPItems = kPTile / kThreads;  // 16
 
@@ -269,44 +97,36 @@ __device__ __forceinline__ void mbar_wait_parity(uint64_t* bar, uint32_t parity)
         : "memory");
 }
 
-// kRestart: if the early probe of tile - 1 is not inclusive, the look-back restarts at tile - 1
-// (measured ablation: PH0B_LOOKBACK=restart); default: the early probe's aggregate is
-// consumed and the look-back continues at tile - 2 in windows of kLookbackWin.
+// Look-back after the early probe of tile - 1: its aggregate is kept and the walk continues
+// at tile - 2 in windows of 4 predecessors per round trip (C5: 14.85 -> 14.26 ms per pass vs
+// restarting at tile - 1 in windows of 8; windows of 3 / 6 measured slower).
 constexpr int kLookbackWin = 4;
-template <bool kVals, bool kCountNext, bool kRestart, bool kTop = false>
+
+template <bool kVals, bool kCountNext, bool kBallot>
 __global__ void __launch_bounds__(kThreads, 2)
     k2_onesweep_p(const uint64_t* __restrict__ keys_in, uint64_t* __restrict__ keys_out,
                   const uint32_t* __restrict__ vals_in, uint32_t* __restrict__ vals_out,
                   uint64_t count, uint64_t kmin, uint32_t shift, uint32_t next_shift,
                   const uint32_t* __restrict__ hist, uint32_t hist_rot,
                   uint64_t* __restrict__ status, uint32_t epoch,
-                  uint32_t* __restrict__ next_hist, uint32_t num_tiles) {
+                  uint32_t* __restrict__ next_hist, uint32_t num_tiles,
+                  uint32_t* __restrict__ ticket) {
     extern __shared__ __align__(128) uint64_t p_dyn[];
     uint64_t* st_k = p_dyn;                                                    // stage keys
     uint32_t* st_v = reinterpret_cast<uint32_t*>(p_dyn + kPTile);              // stage vals
     uint64_t* so_k = p_dyn + kPTile + kPTile / 2;                              // sorted keys
     uint32_t* so_v = reinterpret_cast<uint32_t*>(so_k + kPTile);               // sorted vals
+    // per-warp digit counters; after the scan: tile-local start of (warp, digit)
     __shared__ uint32_t s_whist[kWarps][kBins];
-    __shared__ uint32_t s_tile_start[kBins];
     __shared__ uint32_t s_global[kBins];
     __shared__ uint32_t s_bin_start[kBins];
     __shared__ uint32_t s_next[kCountNext ? kBins : 1];
     __shared__ uint32_t s_scan[kWarps];
+    __shared__ uint32_t s_tile[2];
     __shared__ __align__(8) uint64_t s_bar;
 
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const uint32_t t = tid;  // digit handled by this thread in the per-digit phases
-    if (tid == 0) {
-        asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_addr(&s_bar)));
-        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-    }
-    if (kCountNext) s_next[tid] = 0;
-    {
-        const uint32_t hcount = hist[(t + hist_rot) & 0xFFu];
-        s_bin_start[t] = block_exclusive_scan(hcount, s_scan, nullptr);
-    }
-    __syncthreads();
-
     auto issue = [&](uint32_t tl) {
         const uint64_t b0 = (uint64_t)tl * kPTile;
         const uint64_t n = count - b0 < (uint64_t)kPTile ? count - b0 : (uint64_t)kPTile;
@@ -317,23 +137,35 @@ __global__ void __launch_bounds__(kThreads, 2)
         bulk_g2s(st_k, keys_in + b0, bk, &s_bar);
         if (kVals) bulk_g2s(st_v, vals_in + b0, bv, &s_bar);
     };
-    uint32_t tile = blockIdx.x;
-    if (tid == 0 && tile < num_tiles) issue(tile);
+    if (tid == 0) {
+        asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_addr(&s_bar)));
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+        const uint32_t first = atomicAdd(ticket, 1u);
+        s_tile[0] = first;
+        if (first < num_tiles) issue(first);
+    }
+    if (kCountNext) s_next[tid] = 0;
+    {
+        const uint32_t hcount = hist[(t + hist_rot) & 0xFFu];
+        s_bin_start[t] = block_exclusive_scan(hcount, s_scan, nullptr);
+    }
+    __syncthreads();
+    uint32_t tile = s_tile[0];
     uint32_t parity = 0;
     const uint32_t lt = lanemask_lt();
 
-    for (; tile < num_tiles; tile += gridDim.x) {
+    while (tile < num_tiles) {
         const uint64_t base = (uint64_t)tile * kPTile;
         const uint64_t rem = count - base;
         const uint32_t tile_n = rem < (uint64_t)kPTile ? (uint32_t)rem : (uint32_t)kPTile;
 #pragma unroll
         for (int w = 0; w < kWarps; ++w) s_whist[w][tid] = 0;
         __syncthreads();
-        // kTop: the look-back's probe of tile - 1 goes out here, before this tile is even
-        // ranked: its latency hides behind the rank, scan and scatter phases (C5: 14.51 ->
-        // 13.83 ms per pass vs issuing it after this tile's aggregate is published)
-        uint64_t probe_top = 0;
-        if (kTop && tile > 0) probe_top = ld_relaxed_u64(status + (uint64_t)(tile - 1) * kBins + t);
+        // the look-back's probe of tile - 1 goes out before this tile is even ranked: its
+        // latency hides behind the rank, scan and scatter phases (C5: 14.51 -> 13.83 ms per
+        // pass vs issuing it after this tile's aggregate is published)
+        const uint64_t probe =
+            tile > 0 ? ld_relaxed_u64(status + (uint64_t)(tile - 1) * kBins + t) : 0ull;
         mbar_wait_parity(&s_bar, parity);
         parity ^= 1u;
 
@@ -347,32 +179,42 @@ __global__ void __launch_bounds__(kThreads, 2)
             const bool valid = pos < tile_n;
             k[i] = valid ? st_k[pos] : ~0ull;
             const uint32_t d = valid ? (uint32_t)((k[i] - kmin) >> shift) & 0xFFu : 0x100u;
-            const uint32_t r = valid ? atomicAdd(&s_whist[warp][d], 1u) : 0u;
+            uint32_t r;
+            if constexpr (kBallot) {
+                const uint32_t peers = ballot_peers(d, __ballot_sync(0xffffffffu, valid));
+                const uint32_t leader = __ffs(peers) - 1;
+                const uint32_t o = (valid && lane == (int)leader)
+                                       ? atomicAdd(&s_whist[warp][d], __popc(peers))
+                                       : 0u;
+                r = __shfl_sync(0xffffffffu, o, leader & 31u) + __popc(peers & lt);
+            } else {
+                // ATOMS resolves same-address lanes of one instruction in ascending lane
+                // order, and instructions of one warp in program order: the returned count
+                // IS the stable in-warp rank
+                r = valid ? atomicAdd(&s_whist[warp][d], 1u) : 0u;
+            }
             if (i & 1)
                 rank2[i / 2] |= r << 16;
             else
                 rank2[i / 2] = r;
         }
-        (void)lt;
         __syncthreads();
 
+        // ---- per-digit counts; publish this tile's aggregate; tile-local starts ----------
+        uint32_t wpre[kWarps];
         uint32_t cnt = 0;
 #pragma unroll
         for (int w = 0; w < kWarps; ++w) {
-            const uint32_t c = s_whist[w][t];
-            s_whist[w][t] = cnt;
-            cnt += c;
+            wpre[w] = cnt;
+            cnt += s_whist[w][t];
         }
         uint64_t* my_status = status + (uint64_t)tile * kBins + t;
         st_relaxed_u64(my_status,
                        pack_status(tile == 0 ? kStateInclusive : kStateAggregate, epoch, cnt));
-        // early probe of tile - 1 (its latency hides behind the scan and the scatter; an
-        // aggregate read now is still valid after the scatter)
-        const uint64_t probe =
-            kTop ? probe_top
-                 : (tile > 0 ? ld_relaxed_u64(status + (uint64_t)(tile - 1) * kBins + t) : 0ull);
         const uint32_t tstart = block_exclusive_scan(cnt, s_scan, nullptr);
-        s_tile_start[t] = tstart;
+        // one lookup per key in the scatter: tile start of the digit + the warp's offset in it
+#pragma unroll
+        for (int w = 0; w < kWarps; ++w) s_whist[w][t] = tstart + wpre[w];
         __syncthreads();
 
         // ---- scatter the staged tile into the sorted buffer (shared -> shared) ----------
@@ -381,15 +223,18 @@ __global__ void __launch_bounds__(kThreads, 2)
             const uint32_t pos = wofs + 32 * i;
             if (pos < tile_n) {
                 const uint32_t d = (uint32_t)((k[i] - kmin) >> shift) & 0xFFu;
-                const uint32_t dst = s_tile_start[d] + s_whist[warp][d] +
+                const uint32_t dst = s_whist[warp][d] +
                                      ((i & 1) ? (rank2[i / 2] >> 16) : (rank2[i / 2] & 0xFFFFu));
                 so_k[dst] = k[i];
                 if (kVals) so_v[dst] = st_v[pos];
             }
         }
-        __syncthreads();  // the stage buffer is free: prefetch the next tile now
-        const uint32_t next = tile + gridDim.x;
-        if (tid == 0 && next < num_tiles) issue(next);
+        __syncthreads();  // the stage buffer is free: claim and prefetch the next tile now
+        if (tid == 0) {
+            const uint32_t nx = atomicAdd(ticket, 1u);
+            s_tile[1] = nx;
+            if (nx < num_tiles) issue(nx);
+        }
 
         // ---- decoupled look-back, per digit ----------------------------------------------
         uint32_t excl = 0;
@@ -397,12 +242,9 @@ __global__ void __launch_bounds__(kThreads, 2)
             const uint32_t st0 = status_state(probe, epoch);
             if (st0 == kStateInclusive) {
                 excl = (uint32_t)probe;  // the early probe already has it
-            } else if (kRestart || st0 == 0) {
-                excl = lookback_window<kRestart ? 8 : kLookbackWin>(status + t, kBins, tile, epoch);
+            } else if (st0 == 0) {
+                excl = lookback_window<kLookbackWin>(status + t, kBins, tile, epoch);
             } else {
-                // tile - 1 had published its aggregate: keep it and continue at tile - 2
-                // (older tiles are the ones likely inclusive by now); C5: 14.85 -> 14.26
-                // ms per pass vs restarting at tile - 1 with windows of 8
                 excl = (uint32_t)probe +
                        lookback_window<kLookbackWin>(status + t, kBins, tile - 1, epoch);
             }
@@ -410,6 +252,7 @@ __global__ void __launch_bounds__(kThreads, 2)
         }
         s_global[t] = s_bin_start[t] + excl - tstart;
         __syncthreads();
+        const uint32_t next_tile = s_tile[1];
 
         // ---- write out: consecutive threads -> consecutive positions of each digit run ---
 #pragma unroll 4
@@ -425,6 +268,7 @@ __global__ void __launch_bounds__(kThreads, 2)
                 if (kCountNext) atomicAdd(&s_next[(uint32_t)(rel >> next_shift) & 0xFFu], 1u);
             }
         }
+        tile = next_tile;
     }
     if (kCountNext) {
         __syncthreads();
@@ -474,92 +318,41 @@ __global__ void __launch_bounds__(kBins)
     if (c) atomicAdd(&hist[threadIdx.x], c);
 }
 
-template <bool kVals, bool kCountNext, int kRank, int kMinBlocks>
-void launch_pass_r(const SortArgs& a, int cur, uint32_t p, const SortPlan& plan, uint32_t rot,
-                   uint32_t* next_hist, uint64_t tiles, cudaStream_t s) {
-    auto kern = k2_onesweep<kVals, kCountNext, kRank, kMinBlocks>;
-    const size_t smem = kTileKeys * (sizeof(uint64_t) + (kVals ? sizeof(uint32_t) : 0));
-    static bool configured = false;
-    if (!configured) {
-        cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-        configured = true;
-    }
-    const uint32_t next_shift = kCountNext ? plan.shift[p + 1] : 0u;
-    kern<<<(unsigned)tiles, kThreads, smem, s>>>(
-        a.keys[cur], a.keys[cur ^ 1], kVals ? a.vals[cur] : nullptr,
-        kVals ? a.vals[cur ^ 1] : nullptr, a.count, a.kmin, plan.shift[p], next_shift,
-        a.hist + kBins * p, rot, a.status, a.tile_counter + p, a.epoch_base + p, next_hist);
-}
-
-int g_rank_variant = -1;  // set by sort_self_test(); env PH0B_RANK overrides
+int g_rank_variant = -1;  // 3 = ATOMS ranking, 2 = ballots; set by sort_self_test()
 
 int rank_variant() {
     if (g_rank_variant < 0) {
-        const char* e = getenv("PH0B_RANK");
+        const char* e = getenv("PH0B_RANK");  // test hook: force the ballot ranking
         g_rank_variant = e ? atoi(e) : 2;
     }
     return g_rank_variant;
 }
 
-bool lookback_restart() {
-    static const bool v = [] {
-        const char* e = getenv("PH0B_LOOKBACK");
-        return e && e[0] == 'r';  // "restart": the pre-continuation look-back (ablation)
-    }();
-    return v;
-}
-
-template <bool kVals, bool kCountNext>
-void launch_pass_p(const SortArgs& a, int cur, uint32_t p, const SortPlan& plan, uint32_t rot,
-                   uint32_t* next_hist, cudaStream_t s, int num_sms) {
-    static const bool top = [] {  // PH0B_TOP_PROBE=0: probe after the publish (ablation)
-        const char* e = getenv("PH0B_TOP_PROBE");
-        return !(e && e[0] == '0');
-    }();
-    auto kern = lookback_restart() ? k2_onesweep_p<kVals, kCountNext, true>
-                : top              ? k2_onesweep_p<kVals, kCountNext, false, true>
-                                   : k2_onesweep_p<kVals, kCountNext, false>;
+template <bool kVals, bool kCountNext, bool kBallot>
+int launch_pass_t(const SortArgs& a, int cur, uint32_t p, const SortPlan& plan, uint32_t rot,
+                  uint32_t* next_hist, cudaStream_t s, int num_sms) {
+    auto kern = k2_onesweep_p<kVals, kCountNext, kBallot>;
     const size_t smem = (size_t)kPTile * 8 * 2 + (size_t)kPTile * 4 * 2;
-    static int grid_per_sm = 0;
-    if (!grid_per_sm) {
-        cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&grid_per_sm, kern, kThreads, smem);
-        if (grid_per_sm < 1) grid_per_sm = 1;
-    }
+    const int per_sm = kernel_blocks_per_sm((const void*)kern, kThreads, smem);
+    if (per_sm < 1) return -1;
     const uint64_t tiles = (a.count + kPTile - 1) / kPTile;
-    uint64_t grid = (uint64_t)num_sms * grid_per_sm;
+    uint64_t grid = (uint64_t)num_sms * per_sm;
     if (grid > tiles) grid = tiles;
     const uint32_t next_shift = kCountNext ? plan.shift[p + 1] : 0u;
     kern<<<(unsigned)grid, kThreads, smem, s>>>(
         a.keys[cur], a.keys[cur ^ 1], kVals ? a.vals[cur] : nullptr,
         kVals ? a.vals[cur ^ 1] : nullptr, a.count, a.kmin, plan.shift[p], next_shift,
-        a.hist + kBins * p, rot, a.status, a.epoch_base + p, next_hist, (uint32_t)tiles);
-}
-
-bool use_persistent() {
-    static const bool v = [] {
-        const char* e = getenv("PH0B_SORT_KERNEL");
-        return !(e && e[0] == 'o');  // 'o' = original dynamic-tile onesweep
-    }();
-    return v;
+        a.hist + kBins * p, rot, a.status, a.epoch_base + p, next_hist, (uint32_t)tiles,
+        a.tile_counter + p);
+    return 1;
 }
 
 template <bool kVals, bool kCountNext>
-void launch_pass(const SortArgs& a, int cur, uint32_t p, const SortPlan& plan, uint32_t rot,
-                 uint32_t* next_hist, uint64_t tiles, cudaStream_t s) {
-    static const int minb = [] {
-        const char* e = getenv("PH0B_MINB");
-        return e ? atoi(e) : 4;
-    }();
-    const int rv = rank_variant();
-    if (rv == 3) {
-        if (minb == 3)
-            launch_pass_r<kVals, kCountNext, 3, 3>(a, cur, p, plan, rot, next_hist, tiles, s);
-        else
-            launch_pass_r<kVals, kCountNext, 3, 4>(a, cur, p, plan, rot, next_hist, tiles, s);
-    } else {
-        launch_pass_r<kVals, kCountNext, 2, 4>(a, cur, p, plan, rot, next_hist, tiles, s);
-    }
+int launch_pass(const SortArgs& a, int cur, uint32_t p, const SortPlan& plan, uint32_t rot,
+                uint32_t* next_hist, cudaStream_t s, int num_sms) {
+    return rank_variant() == 3
+               ? launch_pass_t<kVals, kCountNext, false>(a, cur, p, plan, rot, next_hist, s, num_sms)
+               : launch_pass_t<kVals, kCountNext, true>(a, cur, p, plan, rot, next_hist, s, num_sms);
 }
 
 // Self-test of the ordering property rank variant 3 relies on.  Returns true when every
@@ -602,7 +395,7 @@ bool sort_self_test(cudaStream_t s) {
     return h == 0;
 }
 
-uint64_t sort_tiles(uint64_t count) { return (count + kTileKeys - 1) / kTileKeys; }
+uint64_t sort_tiles(uint64_t count) { return (count + kPTile - 1) / kPTile; }
 
 int launch_digit_histogram(const uint64_t* keys, uint64_t count, uint64_t kmin, uint32_t shift,
                            uint32_t* hist, cudaStream_t s, int num_sms) {
@@ -622,9 +415,8 @@ int launch_digit_histogram(const uint64_t* keys, uint64_t count, uint64_t kmin, 
 int launch_sort_passes(const SortArgs& a, const SortPlan& plan, cudaStream_t s, int num_sms,
                        int* launches) {
     int cur = 0;
-    const uint64_t tiles = sort_tiles(a.count);
     if (a.count == 0 || plan.passes == 0) return 0;
-    cudaMemsetAsync(a.tile_counter, 0, sizeof(uint32_t) * 8, s);
+    cudaMemsetAsync(a.tile_counter, 0, sizeof(uint32_t) * 8, s);  // tile tickets per pass
     // hist rows 1..passes-1 are produced by the passes themselves
     if (plan.passes > 1)
         cudaMemsetAsync(a.hist + kBins, 0, sizeof(uint32_t) * kBins * (plan.passes - 1), s);
@@ -632,29 +424,14 @@ int launch_sort_passes(const SortArgs& a, const SortPlan& plan, cudaStream_t s, 
         const bool last = p + 1 == plan.passes;
         uint32_t* next_hist = last ? nullptr : a.hist + kBins * (p + 1);
         const uint32_t rot = (p == 0) ? a.hist0_rot : 0u;
-        if (use_persistent() && rank_variant() == 3) {
-            if (a.vals[0]) {
-                if (last)
-                    launch_pass_p<true, false>(a, cur, p, plan, rot, next_hist, s, num_sms);
-                else
-                    launch_pass_p<true, true>(a, cur, p, plan, rot, next_hist, s, num_sms);
-            } else {
-                if (last)
-                    launch_pass_p<false, false>(a, cur, p, plan, rot, next_hist, s, num_sms);
-                else
-                    launch_pass_p<false, true>(a, cur, p, plan, rot, next_hist, s, num_sms);
-            }
-        } else if (a.vals[0]) {
-            if (last)
-                launch_pass<true, false>(a, cur, p, plan, rot, next_hist, tiles, s);
-            else
-                launch_pass<true, true>(a, cur, p, plan, rot, next_hist, tiles, s);
-        } else {
-            if (last)
-                launch_pass<false, false>(a, cur, p, plan, rot, next_hist, tiles, s);
-            else
-                launch_pass<false, true>(a, cur, p, plan, rot, next_hist, tiles, s);
-        }
+        int r;
+        if (a.vals[0])
+            r = last ? launch_pass<true, false>(a, cur, p, plan, rot, next_hist, s, num_sms)
+                     : launch_pass<true, true>(a, cur, p, plan, rot, next_hist, s, num_sms);
+        else
+            r = last ? launch_pass<false, false>(a, cur, p, plan, rot, next_hist, s, num_sms)
+                     : launch_pass<false, true>(a, cur, p, plan, rot, next_hist, s, num_sms);
+        if (r < 0) return -1;
         if (launches) ++*launches;
         cur ^= 1;
     }

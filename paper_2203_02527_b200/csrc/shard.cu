@@ -460,11 +460,7 @@ int launch_partition_scatter(const uint64_t* keys, const uint32_t* vals, uint64_
     const uint32_t bits = span ? 64u - (uint32_t)__builtin_clzll(span) : 0u;
     const CellMap cm{kmin, bits > (uint32_t)kCellBits ? bits - kCellBits : 0u};
     constexpr size_t kScSmem = (size_t)kTile * (8 + 4 + 1);
-    static bool configured = false;
-    if (!configured) {
-        cudaFuncSetAttribute(k7_scatter, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kScSmem);
-        configured = true;
-    }
+    if (kernel_blocks_per_sm((const void*)k7_scatter, kThreads, kScSmem) < 1) return -1;
     k7_scatter<<<(unsigned)tiles, kThreads, kScSmem, s>>>(keys, vals, count, d_splitters, parts,
                                                           d_counts_scratch, d_totals + parts,
                                                           keys_out, vals_out, d_table, cm,
@@ -487,9 +483,10 @@ int launch_partition(const uint64_t* keys, const uint32_t* vals, uint64_t count,
                                          d_totals, d_bminmax, keys_out, vals_out, s, align, kmin,
                                          kmax, h_splitters, d_table);
     if (l < 0) return l;
-    return l + launch_partition_scatter(keys, vals, count, d_splitters, parts, d_counts_scratch,
+    const int sc = launch_partition_scatter(keys, vals, count, d_splitters, parts, d_counts_scratch,
                                         d_totals, keys_out, vals_out, s, kmin, kmax, d_table,
                                         ~0u, nullptr, nullptr);
+    return sc < 0 ? sc : l + sc;
 }
 
 int launch_sample(const uint64_t* keys, uint64_t count, uint64_t s, uint64_t* out, cudaStream_t st) {

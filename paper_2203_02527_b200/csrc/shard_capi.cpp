@@ -150,6 +150,7 @@ extern "C" {
 int ph0b_shard_distances(ph0b_context* ctx, const double* dX, uint64_t n, uint64_t d,
                          uint32_t layout, uint64_t u_lo, uint64_t u_hi, void* stream,
                          uint64_t* count, uint64_t* kmin, uint64_t* kmax) {
+    if (!ctx) return ph0b::capi_fail(PH0B_ERR_INVALID_ARGUMENT, "null context");
     Context* c = reinterpret_cast<Context*>(ctx);
     std::lock_guard<std::mutex> lk(c->mu);
     if (n > PH0B_MAX_POINTS) return ph0b::capi_fail(PH0B_ERR_TOO_LARGE, "point cloud too large");
@@ -174,6 +175,7 @@ int ph0b_shard_distances(ph0b_context* ctx, const double* dX, uint64_t n, uint64
 }
 
 int ph0b_shard_sample(ph0b_context* ctx, uint64_t s, uint64_t* out_host) {
+    if (!ctx) return ph0b::capi_fail(PH0B_ERR_INVALID_ARGUMENT, "null context");
     Context* c = reinterpret_cast<Context*>(ctx);
     std::lock_guard<std::mutex> lk(c->mu);
     ShardScratch& sc = scratch(c);
@@ -192,6 +194,7 @@ int ph0b_shard_sample(ph0b_context* ctx, uint64_t s, uint64_t* out_host) {
 int ph0b_shard_partition(ph0b_context* ctx, const uint64_t* splitters, uint32_t parts,
                          void* stream, uint64_t** d_keys_send, uint32_t** d_vals_send,
                          uint64_t* counts, uint64_t* part_min, uint64_t* part_max) {
+    if (!ctx) return ph0b::capi_fail(PH0B_ERR_INVALID_ARGUMENT, "null context");
     Context* c = reinterpret_cast<Context*>(ctx);
     std::lock_guard<std::mutex> lk(c->mu);
     if (parts < 1 || parts > 256)
@@ -204,6 +207,7 @@ int ph0b_shard_partition(ph0b_context* ctx, const uint64_t* splitters, uint32_t 
                                          sc.d_counts, sc.d_totals, sc.d_bminmax, c->keys(1),
                                          c->vals(1), st, 1, sc.local_kmin, sc.local_kmax,
                                          splitters, sc.d_table);
+    if (c->launches < 0) return ph0b::capi_fail(PH0B_ERR_CUDA, "shard partition: launch failed");
     ph0b::capi_set_launches(c->launches);
     if ((rc = read_partition(sc, parts, st, counts, part_min, part_max))) return rc;
     if (d_keys_send) *d_keys_send = c->keys(1);
@@ -214,6 +218,7 @@ int ph0b_shard_partition(ph0b_context* ctx, const uint64_t* splitters, uint32_t 
 int ph0b_shard_partition_count(ph0b_context* ctx, const uint64_t* splitters, uint32_t parts,
                                void* stream, uint64_t* counts, uint64_t* part_min,
                                uint64_t* part_max) {
+    if (!ctx) return ph0b::capi_fail(PH0B_ERR_INVALID_ARGUMENT, "null context");
     Context* c = reinterpret_cast<Context*>(ctx);
     std::lock_guard<std::mutex> lk(c->mu);
     if (parts < 1 || parts > 256)
@@ -232,6 +237,7 @@ int ph0b_shard_partition_count(ph0b_context* ctx, const uint64_t* splitters, uin
 
 int ph0b_shard_recv_peer(ph0b_context* ctx, uint64_t count, uint64_t** d_keys,
                          uint32_t** d_vals) {
+    if (!ctx) return ph0b::capi_fail(PH0B_ERR_INVALID_ARGUMENT, "null context");
     Context* c = reinterpret_cast<Context*>(ctx);
     std::lock_guard<std::mutex> lk(c->mu);
     Status s = c->reserve_recv(count, 1);  // buffer 0 still holds the local edges
@@ -247,6 +253,7 @@ int ph0b_shard_recv_peer(ph0b_context* ctx, uint64_t count, uint64_t** d_keys,
 int ph0b_shard_scatter_peers(ph0b_context* ctx, uint32_t parts, const uint64_t* dst_keys,
                              const uint64_t* dst_vals, const uint64_t* dst_offsets,
                              void* stream) {
+    if (!ctx) return ph0b::capi_fail(PH0B_ERR_INVALID_ARGUMENT, "null context");
     Context* c = reinterpret_cast<Context*>(ctx);
     std::lock_guard<std::mutex> lk(c->mu);
     ShardScratch& sc = scratch(c);
@@ -270,6 +277,7 @@ int ph0b_shard_scatter_peers(ph0b_context* ctx, uint32_t parts, const uint64_t* 
         c->keys(0), c->vals(0), sc.local_count, sc.d_spl, parts, sc.d_counts, sc.d_totals,
         nullptr, nullptr, st, sc.local_kmin, sc.local_kmax, sc.d_table, ~0u, sc.d_peer,
         sc.d_peer + 256);
+    if (c->launches < 0) return ph0b::capi_fail(PH0B_ERR_CUDA, "shard scatter: launch configuration failed");
     ph0b::capi_set_launches(c->launches);
     // the stores into peer memory are complete when the kernel is; the caller's barrier
     // then publishes them to the receiving ranks
@@ -307,6 +315,7 @@ int ph0b_ipc_close(void* d_ptr) {
 }
 
 int ph0b_shard_recv(ph0b_context* ctx, uint64_t count, uint64_t** d_keys, uint32_t** d_vals) {
+    if (!ctx) return ph0b::capi_fail(PH0B_ERR_INVALID_ARGUMENT, "null context");
     Context* c = reinterpret_cast<Context*>(ctx);
     std::lock_guard<std::mutex> lk(c->mu);
     Status s = c->reserve_recv(count);  // grows buffer 0 only: buffer 1 holds the send data
@@ -320,6 +329,7 @@ int ph0b_shard_recv(ph0b_context* ctx, uint64_t count, uint64_t** d_keys, uint32
 int ph0b_shard_sort_unique(ph0b_context* ctx, uint64_t count, uint64_t kmin, uint64_t kmax,
                            void* stream, uint64_t* n_distinct, const double** d_scale,
                            uint32_t* passes_out) {
+    if (!ctx) return ph0b::capi_fail(PH0B_ERR_INVALID_ARGUMENT, "null context");
     Context* c = reinterpret_cast<Context*>(ctx);
     std::lock_guard<std::mutex> lk(c->mu);
     Status s = c->reserve_edges(count);  // the send buffer is free now: grow the ping-pong
@@ -345,6 +355,7 @@ int ph0b_shard_sort_unique(ph0b_context* ctx, uint64_t count, uint64_t kmin, uin
 int ph0b_shard_reduce(ph0b_context* ctx, uint64_t n, uint64_t count, uint64_t grade_offset,
                       void* stream, uint64_t* m, const uint32_t** d_uv, const uint64_t** d_grade,
                       const double** d_length) {
+    if (!ctx) return ph0b::capi_fail(PH0B_ERR_INVALID_ARGUMENT, "null context");
     Context* c = reinterpret_cast<Context*>(ctx);
     std::lock_guard<std::mutex> lk(c->mu);
     cudaStream_t st = pick(c, stream);
@@ -371,6 +382,7 @@ int ph0b_shard_reduce(ph0b_context* ctx, uint64_t n, uint64_t count, uint64_t gr
 
 int ph0b_reduce_columns(ph0b_context* ctx, const uint32_t* d_uv, uint64_t count, uint64_t n,
                         void* stream, uint32_t* idx_host, uint64_t* n_out) {
+    if (!ctx) return ph0b::capi_fail(PH0B_ERR_INVALID_ARGUMENT, "null context");
     Context* c = reinterpret_cast<Context*>(ctx);
     std::lock_guard<std::mutex> lk(c->mu);
     Status s = c->reserve_points(n, 0);

@@ -6,15 +6,17 @@
 //   grade_i = inclusive_scan(flag)_i                     (1-based, filtration.cpp:32)
 //   D[grade_i - 1] = length_i  for flagged i             (Filtration::scale)
 //
-// Default: a chain-free split over 4096-key tiles — (1) a persistent TMA-staged count pass
-// (run fix-ups of truncated radix plans, per-tile distinct counts and owned ranges), (2) a
-// scan of the tile counts, (3) a persistent TMA-staged pass writing D and the grades.  The
-// single-pass variant with decoupled look-back is kept behind PH0B_UNIQUE=1.  Column j of M
+// A chain-free split over 4096-key tiles — (1) a persistent TMA-staged count pass (run
+// fix-ups of truncated radix plans, per-tile distinct counts and owned ranges), (2) a scan of
+// the tile counts, (3) a persistent TMA-staged pass writing D and the grades.  No tile waits
+// on another tile (a single pass with decoupled look-back measured 15.4 ms at C5 against
+// 12.1 ms for the split: its look-back serialised every tile behind one warp).  Column j of M
 // is {u_j, v_j} at grade_j: the sorted (u << 16 | v) array already holds the supports, and
 // the grades are written only when requested (parity surfaces); the barcode collect
 // recovers a survivor's grade from D by binary search instead.
 #include <cuda_runtime.h>
 
+#include <algorithm>
 #include <cstdint>
 #include <cstdlib>
 
@@ -87,10 +89,10 @@ __global__ void __launch_bounds__(1024)
 
 }  // namespace
 
-// ---- persistent single-pass unique (default) ---------------------------------------------
-// Static tile order over co-resident CTAs (deadlock-free look-back), the next tile's keys
-// (+ the kMaxRun extension) prefetched with a TMA bulk copy while this tile is fixed up,
-// counted, looked back and written.  One read of the keys, one write of D.
+// ---- persistent count / write passes ------------------------------------------------------
+// Static tile order (no tile waits on another, so residency is not required); the next
+// tile's keys (+ the kMaxRun extension) are prefetched with a TMA bulk copy while this tile
+// is fixed up and counted (pass 1) or written (pass 2).
 __device__ __forceinline__ uint32_t u_smem(const void* p) {
     return static_cast<uint32_t>(__cvta_generic_to_shared(p));
 }
@@ -101,15 +103,13 @@ constexpr int kUWarps = kUThreads / 32;
 constexpr int kUItems = kUT / kUThreads;
 constexpr int kUStage = kUT + 72;  // tile + extension (>= kExt), 16 B multiple
 
-// kMode 0: single pass (fix-ups, counts, look-back, D).  kMode 1: fix-ups + per-tile counts
-// and owned ranges only (no look-back, no D).  kMode 2: D and grades from the per-tile
-// offsets of a scan of those counts (no fix-ups, no look-back) — the chain-free split.
+// kMode 1: fix-ups + per-tile counts and owned ranges only (no D).  kMode 2: D and grades
+// from the per-tile offsets of a scan of those counts (no fix-ups).
 template <int kMode>
 __global__ void __launch_bounds__(kUThreads, 3)
     k3_unique_p(uint64_t* __restrict__ keys, uint32_t* __restrict__ vals, uint64_t count,
                 uint64_t kmin, uint32_t low_bits, double* __restrict__ scale,
-                uint32_t* __restrict__ grade, uint64_t* __restrict__ status, uint32_t epoch,
-                uint64_t* n_scale, uint32_t* redo, uint32_t num_tiles,
+                uint32_t* __restrict__ grade, uint32_t* redo, uint32_t num_tiles,
                 const uint64_t* __restrict__ d_base, uint32_t* __restrict__ tile_counts,
                 int2* __restrict__ tile_own, const uint64_t* __restrict__ tile_offsets) {
     extern __shared__ __align__(128) uint64_t up_dyn[];
@@ -117,7 +117,6 @@ __global__ void __launch_bounds__(kUThreads, 3)
     __shared__ uint32_t s_warp_tot[kUWarps];
     __shared__ int s_own[2];
     __shared__ uint32_t s_ext_tot;
-    __shared__ uint64_t s_prefix;
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     auto pre = [&](uint64_t kk) { return (kk - kmin) >> low_bits; };
     if (tid == 0) {
@@ -315,27 +314,7 @@ __global__ void __launch_bounds__(kUThreads, 3)
             }
             continue;  // (the loop-top barrier orders the buffer reuse)
         }
-        const uint32_t tile_tot = main_tot + (low_bits && kMode == 0 ? s_ext_tot : 0u);
-        if (kMode == 2) {
-            if (tid == 0) s_prefix = base0 + tile_offsets[tile];
-        } else if (warp == 0) {  // warp-wide look-back: 32 predecessors per round trip
-            uint64_t* my = status + tile;
-            uint32_t excl = 0;
-            if (tile == 0) {
-                if (lane == 0) st_relaxed_u64(my, pack_status(kStateInclusive, epoch, tile_tot));
-            } else {
-                if (lane == 0) st_relaxed_u64(my, pack_status(kStateAggregate, epoch, tile_tot));
-                excl = lookback_warp(status, 1, tile, epoch, lane);
-                if (lane == 0)
-                    st_relaxed_u64(my, pack_status(kStateInclusive, epoch, excl + tile_tot));
-            }
-            if (lane == 0) {
-                s_prefix = base0 + excl;
-                if (tile == num_tiles - 1) *n_scale = base0 + (uint64_t)excl + tile_tot;
-            }
-        }
-        __syncthreads();
-        const uint64_t base = s_prefix;
+        const uint64_t base = base0 + tile_offsets[tile];
         uint64_t run = base + warp_base;
         const uint32_t lt = lanemask_lt();
 #pragma unroll
@@ -370,10 +349,6 @@ int launch_unique(const UniqueArgs& a, cudaStream_t s) {
         cudaMemsetAsync(a.n_scale, 0, sizeof(uint64_t), s);
         return 0;
     }
-    static const int mode_env = [] {  // PH0B_UNIQUE: 1 single pass, 2 split (default)
-        const char* e = getenv("PH0B_UNIQUE");
-        return e ? atoi(e) : 2;
-    }();
     const uint64_t tiles = (a.count + kUT - 1) / kUT;
     static_assert(kUT == kTileKeys, "scratch sizing uses the same tiling");
     // scratch: counts (u32) | own (int2) | offsets (u64), unique_scratch_words(count) words
@@ -381,32 +356,19 @@ int launch_unique(const UniqueArgs& a, cudaStream_t s) {
     int2* own = reinterpret_cast<int2*>(a.scratch + (tiles + 1) / 2 + 1);
     uint64_t* offsets = a.scratch + (tiles + 1) / 2 + 1 + tiles + 1;
     const size_t smem = (size_t)2 * kUStage * 8;
-    static int per_sm = 0;
-    static int num_sms = 0;
-    if (!per_sm) {
-        for (auto kern : {k3_unique_p<0>, k3_unique_p<1>, k3_unique_p<2>})
-            cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k3_unique_p<0>, kUThreads, smem);
-        if (per_sm < 1) per_sm = 1;
-        int dev = 0;
-        cudaGetDevice(&dev);
-        cudaDeviceGetAttribute(&num_sms, cudaDevAttrMultiProcessorCount, dev);
-    }
-    uint64_t grid = (uint64_t)num_sms * per_sm;
-    if (grid > tiles) grid = tiles;
-    if (mode_env == 1) {
-        k3_unique_p<0><<<(unsigned)grid, kUThreads, smem, s>>>(
-            a.keys, a.vals, a.count, a.kmin, a.low_bits, a.scale, a.grade, a.status, a.epoch,
-            a.n_scale, a.redo, (uint32_t)tiles, a.d_base, nullptr, nullptr, nullptr);
-        return 1;
-    }
-    k3_unique_p<1><<<(unsigned)grid, kUThreads, smem, s>>>(
-        a.keys, a.vals, a.count, a.kmin, a.low_bits, a.scale, a.grade, a.status, a.epoch,
-        a.n_scale, a.redo, (uint32_t)tiles, a.d_base, counts, own, nullptr);
+    const int per_sm1 = kernel_blocks_per_sm((const void*)k3_unique_p<1>, kUThreads, smem);
+    const int per_sm2 = kernel_blocks_per_sm((const void*)k3_unique_p<2>, kUThreads, smem);
+    if (per_sm1 < 1 || per_sm2 < 1) return -1;
+    const uint64_t sms = (uint64_t)device_sm_count();
+    const uint64_t g1 = std::min<uint64_t>(sms * per_sm1, tiles);
+    const uint64_t g2 = std::min<uint64_t>(sms * per_sm2, tiles);
+    k3_unique_p<1><<<(unsigned)g1, kUThreads, smem, s>>>(
+        a.keys, a.vals, a.count, a.kmin, a.low_bits, a.scale, a.grade, a.redo, (uint32_t)tiles,
+        a.d_base, counts, own, nullptr);
     k3_scan<<<1, 1024, 0, s>>>(counts, (uint32_t)tiles, offsets, a.n_scale, a.d_base);
-    k3_unique_p<2><<<(unsigned)grid, kUThreads, smem, s>>>(
-        a.keys, a.vals, a.count, a.kmin, a.low_bits, a.scale, a.grade, a.status, a.epoch,
-        a.n_scale, a.redo, (uint32_t)tiles, a.d_base, counts, own, offsets);
+    k3_unique_p<2><<<(unsigned)g2, kUThreads, smem, s>>>(
+        a.keys, a.vals, a.count, a.kmin, a.low_bits, a.scale, a.grade, a.redo, (uint32_t)tiles,
+        a.d_base, counts, own, offsets);
     return 3;
 }
 

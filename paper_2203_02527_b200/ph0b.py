@@ -40,6 +40,7 @@ EXPORTED_SYMBOLS = [
     "ph0b_decode_deltas", "ph0b_decode_packed", "ph0b_scale_to_host",
     "ph0b_shard_partition_count", "ph0b_shard_recv_peer",
     "ph0b_shard_scatter_peers", "ph0b_ipc_get_handle", "ph0b_ipc_open_handle", "ph0b_ipc_close",
+    "ph0b_scale_release", "ph0b_host_cache_trim",
 ]
 
 
@@ -96,6 +97,8 @@ def lib() -> C.CDLL:
     sig = {
         "ph0b_h0_barcode": (C.c_int, [vp, u64, u64, u32, C.POINTER(Options), C.POINTER(Result)]),
         "ph0b_result_free": (None, [C.POINTER(Result)]),
+        "ph0b_scale_release": (None, [vp]),
+        "ph0b_host_cache_trim": (None, []),
         "ph0b_kruskal_barcode": (C.c_int, [vp, u64, u64, u32, C.POINTER(Options),
                                            C.POINTER(Result)]),
         "ph0b_generate_uniform_cloud_device": (C.c_int, [vp, u64, u64, u64, vp, vp]),
@@ -170,24 +173,20 @@ class Barcode:
         return [(0.0, int(g), float(x)) for g, x in zip(self.death_grade, self.death_length)]
 
 
-_libc = None
-
-
 def _take_scale(res) -> np.ndarray:
-    """D of a ph0b_result as a numpy array that takes over the library's malloc'd buffer
-    (freed with the array) instead of copying it; res.scale is cleared so ph0b_result_free
-    leaves it alone."""
-    global _libc
+    """D of a ph0b_result as a numpy array that takes over the library's buffer (handed back
+    with ph0b_scale_release when the array dies) instead of copying it; res.scale is cleared
+    so ph0b_result_free leaves it alone."""
     if not res.n_scale:
         return np.zeros(0)
-    if _libc is None:
-        _libc = C.CDLL(None)
-        _libc.free.argtypes = [C.c_void_p]
+    L = lib()
     ptr = C.cast(res.scale, C.c_void_p).value
-    arr = np.ctypeslib.as_array(res.scale, (res.n_scale,))
-    weakref.finalize(arr, _libc.free, ptr)
+    # the finalizer hangs on the ctypes buffer every numpy view of D refers to (numpy collapses
+    # view bases to it), so D is released only when no array uses it any more
+    buf = (C.c_double * res.n_scale).from_address(ptr)
+    weakref.finalize(buf, L.ph0b_scale_release, C.c_void_p(ptr))
     res.scale = None
-    return arr
+    return np.frombuffer(buf, dtype=np.float64, count=res.n_scale)
 
 
 def h0_barcode(X, *, device: int = 0, return_scale: bool = True, workers: int = 1,

@@ -48,6 +48,9 @@ def orc() -> C.CDLL:
         L.orc_reduce_barcode.restype = C.c_int64
         L.orc_reduce_barcode.argtypes = [u64, u64, vp, vp, vp, vp, u64, vp, vp, vp,
                                          C.POINTER(u64), C.POINTER(u64)]
+        L.orc_generate_cloud.restype = C.c_int
+        L.orc_generate_cloud.argtypes = [u32, u64, u64, u64, u32, C.c_double, C.c_double,
+                                         C.c_double, u64, vp]
         L.orc_kruskal_barcode.restype = C.c_int64
         L.orc_kruskal_barcode.argtypes = [u64, u64, vp, vp, vp, vp, vp, vp, C.POINTER(u64)]
         _orc = L
@@ -89,6 +92,33 @@ def uniform_cloud(n: int, d: int, seed: int) -> np.ndarray:
     buf = np.empty(max(n * d, 1))
     assert orc().orc_generate_uniform_cloud(n, d, seed, _p(buf)) == 0
     return buf[: n * d].reshape(d, n).T
+
+
+# BASELINE.json configs, restated on the oracle side so fixtures and the
+# bench's reference arm build X without the product library.
+CONFIGS = {
+    "C1": dict(kind=3, n=500, d=2, seed=1, sigma=0.05, lo=0.3, hi=0.7),
+    "C2": dict(kind=2, n=2000, d=3, seed=2, sigma=0.05, lo=-1.5, hi=1.5, n_background=400),
+    "C3": dict(kind=1, n=8192, d=16, seed=3, clusters=10, sigma=0.5, lo=-5.0, hi=5.0),
+    "C4": dict(kind=0, n=32768, d=3, seed=4),
+    "C5": dict(kind=1, n=65536, d=8, seed=5, clusters=32, sigma=0.3, lo=-5.0, hi=5.0),
+}
+
+
+def generate_cloud(kind: int, n: int, d: int, seed: int, clusters: int = 0, sigma: float = 0.0,
+                   lo: float = 0.0, hi: float = 1.0, n_background: int = 0) -> np.ndarray:
+    buf = np.empty(max(n * d, 1))
+    rc = orc().orc_generate_cloud(kind, n, d, seed, clusters, sigma, lo, hi, n_background,
+                                  _p(buf))
+    assert rc == 0, rc
+    return buf[: n * d].reshape(d, n).T
+
+
+def config_cloud(name: str, n: int | None = None) -> np.ndarray:
+    cfg = dict(CONFIGS[name])
+    if n is not None:
+        cfg["n"] = n
+    return generate_cloud(**cfg)
 
 
 def pairwise(X) -> np.ndarray:

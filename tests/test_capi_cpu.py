@@ -28,7 +28,7 @@ def test_header_symbols_exported():
 
 
 def test_abi_version():
-    assert pkg.lib().ph0b_abi_version() == 3
+    assert pkg.lib().ph0b_abi_version() == 4
 
 
 def test_nonfinite_rejected_with_reference_message():  # point_cloud.cpp:15-18

@@ -2,8 +2,8 @@
 the union-find restatement of the reference oracle (oracle.cpp:32-46) over the GPU
 filtration must give the reference's bars bit for bit (acceptance.cpp:79-90: oracle
 equivalence), and agree with the column-reduction path on every config where the CPU
-cannot follow (C4 here, C5 with PH0B_FULL)."""
-import os
+cannot follow (C4 here; C4 and C5 against the reference itself in
+test_gpu_reference_large.py)."""
 
 import numpy as np
 import pytest
@@ -69,11 +69,4 @@ def test_kruskal_degenerate():
 def test_kruskal_c4_equals_reduction():
     """C4 at full size (5.4e8 edges): two different algorithms on the same filtration."""
     X = pkg.config_cloud("C4")
-    same(pkg.kruskal_barcode(X, return_scale=False), pkg.h0_barcode(X, return_scale=False))
-
-
-@pytest.mark.slow
-@pytest.mark.skipif(not os.environ.get("PH0B_FULL"), reason="set PH0B_FULL=1 for C5 full size")
-def test_kruskal_c5_equals_reduction():
-    X = pkg.config_cloud("C5")
     same(pkg.kruskal_barcode(X, return_scale=False), pkg.h0_barcode(X, return_scale=False))
