@@ -30,7 +30,8 @@ extern "C" {
 
 /* 3: + peer-memory exchange (ph0b_shard_partition_count/recv_peer/scatter_peers, ph0b_ipc_*),
  *    ph0b_scale_to_host, ph0b_decode_packed
- * 4: + ph0b_scale_release, ph0b_host_cache_trim; ph0b_h0_barcode streams D like ph0b_run_host */
+ * 4: + ph0b_scale_release, ph0b_host_cache_trim, ph0b_reduced_supports; ph0b_h0_barcode
+ *    streams D like ph0b_run_host */
 #define PH0B_ABI_VERSION 4u
 
 /* Return codes.  The message of ph0b_last_error() repeats the reference's exception text
@@ -144,6 +145,16 @@ int ph0b_build_filtration(const double* X, uint64_t n, uint64_t d, uint32_t layo
  * entries).  Stronger-than-barcode parity surface. */
 int ph0b_claimed_lows(const double* X, uint64_t n, uint64_t d, uint32_t layout,
                       const ph0b_options* opt, uint32_t* lows, uint64_t* n_lows);
+
+/* The whole reduced matrix of reduce() (reduction.cpp:33-49): every column of M ends empty
+ * (a cycle) or as a 2-element support {rows_lo[i], rows_hi[i]} (rows_lo < rows_hi =
+ * its claimed low, reduction.cpp:44-45).  Lists the n_columns = n-1 surviving columns in
+ * filtration order: columns[i] is the column index j (0-based position in the filtration);
+ * all other columns are empty.  The reference compares whole reduced matrices across its
+ * options (acceptance.cpp:106-133); so can a caller, against this. Arrays need n-1 entries. */
+int ph0b_reduced_supports(const double* X, uint64_t n, uint64_t d, uint32_t layout,
+                          const ph0b_options* opt, uint64_t* columns, uint32_t* rows_lo,
+                          uint32_t* rows_hi, uint64_t* n_columns);
 
 /* ---- device-resident path (benchmarks, multi-GPU orchestration) ----------------------- */
 typedef struct ph0b_context ph0b_context;

@@ -215,6 +215,103 @@ int64_t orc_reduce_barcode(uint64_t n, uint64_t k, const uint32_t* u, const uint
     return nf;
 }
 
+int64_t orc_reduce_sparse(uint64_t n, uint64_t k, const uint32_t* u, const uint32_t* v,
+                          const uint64_t* grade, const double* scale, uint64_t n_scale,
+                          uint64_t* death_grade, double* death_length, uint64_t* columns,
+                          uint32_t* rows_lo, uint32_t* rows_hi, uint64_t* essential,
+                          uint64_t* additions, int stop_at_spanning) {
+    /* reduction.cpp:33-49 over every column, with each support held as its (at most two)
+     * rows instead of a bit vector: boundary_matrix.cpp:22-24 starts every column at {u, v}
+     * and the symmetric difference of two 2-element supports that share their low is again
+     * at most 2 elements, so this is the same arithmetic at O(1) per addition. */
+    uint64_t* claimed = (uint64_t*)malloc(sizeof(uint64_t) * (n ? n : 1));
+    uint32_t* lo = (uint32_t*)malloc(sizeof(uint32_t) * (k ? k : 1));
+    uint32_t* hi = (uint32_t*)malloc(sizeof(uint32_t) * (k ? k : 1));
+    uint8_t* cnt = (uint8_t*)malloc(k ? k : 1);
+    if (!claimed || !lo || !hi || !cnt) {
+        free(claimed);
+        free(lo);
+        free(hi);
+        free(cnt);
+        return -1;
+    }
+    const uint64_t none = ~0ULL;
+    for (uint64_t r = 0; r < n; ++r) claimed[r] = none; /* reduction.cpp:21-22 */
+    uint64_t adds = 0;
+    int64_t nf = 0;
+    for (uint64_t j = 0; j < k; ++j) {
+        uint32_t a = u[j] < v[j] ? u[j] : v[j], c = u[j] < v[j] ? v[j] : u[j];
+        uint8_t m = u[j] == v[j] ? 0 : 2; /* {u, u} would be empty (never: u < v) */
+        while (m) {
+            const uint32_t low = m == 2 ? c : a; /* top() */
+            const uint64_t kk = claimed[low];
+            if (kk == none) {
+                claimed[low] = j; /* reduction.cpp:44-45 */
+                break;
+            }
+            /* add_column: {a, c} ^ {lo_k, hi_k} with hi_k == low */
+            uint32_t x[4];
+            int nx = 0;
+            const uint32_t mine[2] = {a, c}, theirs[2] = {lo[kk], hi[kk]};
+            for (int i = 2 - m; i < 2; ++i) x[nx++] = mine[i];
+            for (int i = 2 - cnt[kk]; i < 2; ++i) x[nx++] = theirs[i];
+            uint32_t y[4];
+            int ny = 0;
+            for (int i = 0; i < nx; ++i) {
+                int dup = 0;
+                for (int q = 0; q < nx; ++q)
+                    if (q != i && x[q] == x[i]) dup = 1;
+                if (!dup) y[ny++] = x[i];
+            }
+            if (ny > 2) { /* cannot happen: supports stay 2-sparse */
+                free(claimed);
+                free(lo);
+                free(hi);
+                free(cnt);
+                return -3;
+            }
+            m = (uint8_t)ny;
+            if (ny == 2) {
+                a = y[0] < y[1] ? y[0] : y[1];
+                c = y[0] < y[1] ? y[1] : y[0];
+            } else if (ny == 1) {
+                a = y[0];
+                c = y[0];
+            }
+            ++adds;
+        }
+        cnt[j] = m;
+        lo[j] = m == 2 ? a : (m == 1 ? a : 0);
+        hi[j] = m ? c : 0;
+        if (m) { /* extract_barcode, reduction.cpp:140-150 */
+            if (grade[j] < 1 || grade[j] > n_scale) {
+                free(claimed);
+                free(lo);
+                free(hi);
+                free(cnt);
+                return -2;
+            }
+            if (death_grade) death_grade[nf] = grade[j];
+            if (death_length) death_length[nf] = scale[grade[j] - 1];
+            if (columns) columns[nf] = j;
+            if (rows_lo) rows_lo[nf] = lo[j];
+            if (rows_hi) rows_hi[nf] = hi[j];
+            ++nf;
+            /* stop_at_spanning: after n-1 survivors every later column is a cycle (it ends
+             * empty and claims nothing), so the outputs are complete; only the addition
+             * count then covers the columns processed so far */
+            if (stop_at_spanning && (uint64_t)nf + 1 == n) break;
+        }
+    }
+    *essential = n - (uint64_t)nf;
+    if (additions) *additions = adds;
+    free(claimed);
+    free(lo);
+    free(hi);
+    free(cnt);
+    return nf;
+}
+
 static uint32_t uf_find(uint32_t* parent, uint32_t x) { /* oracle.cpp:13-19, path halving */
     while (parent[x] != x) {
         parent[x] = parent[parent[x]];

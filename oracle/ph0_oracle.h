@@ -52,6 +52,18 @@ int64_t orc_reduce_barcode(uint64_t n, uint64_t k, const uint32_t* u, const uint
                            uint64_t* death_grade, double* death_length, uint32_t* claimed_low,
                            uint64_t* essential, uint64_t* additions);
 
+/* The same reduction (reduction.cpp:33-49 + extract_barcode) with every column held as its
+ * at most two rows (supports stay 2-sparse, boundary_matrix.cpp:22-24): memory 9 B per
+ * column, so it runs at sizes the bit-vector form cannot.  Per surviving column, in
+ * filtration order: its index, its reduced support {rows_lo < rows_hi = claimed low}.  Any
+ * output pointer may be NULL.  stop_at_spanning: stop after n-1 survivors (all later
+ * columns are cycles; additions then cover the processed columns only).  Returns the number of finite bars or < 0 on error. */
+int64_t orc_reduce_sparse(uint64_t n, uint64_t k, const uint32_t* u, const uint32_t* v,
+                          const uint64_t* grade, const double* scale, uint64_t n_scale,
+                          uint64_t* death_grade, double* death_length, uint64_t* columns,
+                          uint32_t* rows_lo, uint32_t* rows_hi, uint64_t* essential,
+                          uint64_t* additions, int stop_at_spanning);
+
 /* oracle.cpp:8-46 — Kruskal with union by rank + path halving. Returns number of bars. */
 int64_t orc_kruskal_barcode(uint64_t n, uint64_t k, const uint32_t* u, const uint32_t* v,
                             const uint64_t* grade, const double* length, uint64_t* death_grade,

@@ -154,6 +154,50 @@ int ref_h0_barcode(const double* x, std::uint64_t n, std::uint64_t d, int mode, 
     }
 }
 
+// The whole reduced matrix (reduction.cpp:33-49) under ReductionOptions{pivoting, workers}:
+// reduce() for workers == 1 (reduction.cpp:129-131), reduce_parallel() otherwise
+// (reduction.cpp:133-138) — the matrices acceptance.cpp:106-133 compares.  For every
+// nonzero column j in order: cols[m] = j and its two rows lo[m] < hi[m] (any other support
+// size is reported as an error: the reference's columns stay 2-sparse).  stats[3] =
+// ReductionStats{additions, row_ops, probe_ops} (reduction.hpp:21-27).
+int ref_reduced_matrix(const double* x, std::uint64_t n, std::uint64_t d, int pivoting,
+                       unsigned workers, std::uint64_t* cols, std::uint32_t* lo,
+                       std::uint32_t* hi, std::uint64_t* m, std::uint64_t* stats) {
+    try {
+        const ph0::Filtration f = ph0::build_filtration(ph0::pairwise_distances(make_cloud(x, n, d)));
+        ph0::BoundaryMatrix mat = ph0::build_boundary_matrix(f, n);
+        const ph0::ReductionOptions opts{pivoting != 0, workers};
+        const ph0::ReductionStats st =
+            workers > 1 ? ph0::reduce_parallel(mat, opts) : ph0::reduce(mat, opts);
+        std::uint64_t k = 0;
+        for (std::size_t j = 0; j < mat.columns.size(); ++j) {
+            const ph0::BitVector& sup = mat.columns[j].support;
+            if (!sup.any()) continue;
+            if (sup.count() != 2) {
+                g_err = "reduced column with support size " + std::to_string(sup.count());
+                return 1;
+            }
+            const std::uint32_t t = sup.top();
+            std::uint32_t b = 0;
+            while (!sup.test(b)) ++b;
+            cols[k] = j;
+            lo[k] = b;
+            hi[k] = t;
+            ++k;
+        }
+        *m = k;
+        if (stats) {
+            stats[0] = st.additions;
+            stats[1] = st.row_ops;
+            stats[2] = st.probe_ops;
+        }
+        return 0;
+    } catch (const std::exception& e) {
+        g_err = e.what();
+        return 1;
+    }
+}
+
 // Text front-end of the reference CLI (ph0_cli.cpp:58-80, :199-205) without CLI11: the text a
 // `compute`/`oracle` (mode 0/1) run prints for a point file's contents, or "error: <what>\n"
 // (ph0_cli.cpp:278-281) with return 1; `generate` as write_points(generate_uniform_cloud).

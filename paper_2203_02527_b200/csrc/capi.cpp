@@ -606,8 +606,15 @@ int ph0b_build_filtration(const double* X, uint64_t n, uint64_t d, uint32_t layo
     return PH0B_OK;
 }
 
-int ph0b_claimed_lows(const double* X, uint64_t n, uint64_t d, uint32_t layout,
-                      const ph0b_options* opt, uint32_t* lows, uint64_t* n_lows) {
+}  // extern "C"
+
+namespace {
+
+// The pipeline, then the survivors' reduced supports (claimed lows, and the other row when
+// xs != nullptr) in filtration order; cols (optional) receives each survivor's column index.
+int supports_impl(const double* X, uint64_t n, uint64_t d, uint32_t layout,
+                  const ph0b_options* opt, uint64_t* cols, uint32_t* xs, uint32_t* lows,
+                  uint64_t* m_out) {
     Opts o;
     int rc = parse(opt, n, layout, &o);
     if (rc) return rc;
@@ -621,14 +628,37 @@ int ph0b_claimed_lows(const double* X, uint64_t n, uint64_t d, uint32_t layout,
     RunOutputs r;
     Status st = c->run_host_input(X, n, d, layout, s, StopAfter::Barcode, false, &r);
     if (!st.good()) return fail(st);
-    if (n_lows) *n_lows = r.n_finite;
+    if (m_out) *m_out = r.n_finite;
     if (r.n_finite == 0) return PH0B_OK;
-    st = c->claimed_lows(r, (uint32_t)n, c->lows_buffer(), s);
+    st = c->reduced_supports(r, (uint32_t)n, xs != nullptr, s);
     g_last_launches = c->launches;
     if (!st.good()) return fail(st);
-    if (cudaMemcpy(lows, c->lows_buffer(), r.n_finite * 4, cudaMemcpyDeviceToHost) != cudaSuccess)
-        return fail(PH0B_ERR_CUDA, "D2H lows");
+    const uint64_t m = r.n_finite;
+    std::vector<uint32_t> surv(cols ? m : 0);
+    if ((lows && cudaMemcpy(lows, c->lows_buffer(), m * 4, cudaMemcpyDeviceToHost)) ||
+        (xs && cudaMemcpy(xs, c->lows_buffer() + n, m * 4, cudaMemcpyDeviceToHost)) ||
+        (cols && cudaMemcpy(surv.data(), r.d_surv_sorted, m * 4, cudaMemcpyDeviceToHost)))
+        return fail(PH0B_ERR_CUDA, "D2H reduced supports");
+    for (uint64_t i = 0; cols && i < m; ++i) cols[i] = surv[i];
     return PH0B_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+int ph0b_claimed_lows(const double* X, uint64_t n, uint64_t d, uint32_t layout,
+                      const ph0b_options* opt, uint32_t* lows, uint64_t* n_lows) {
+    if (n >= 2 && !lows) return fail(PH0B_ERR_INVALID_ARGUMENT, "null output");
+    return supports_impl(X, n, d, layout, opt, nullptr, nullptr, lows, n_lows);
+}
+
+int ph0b_reduced_supports(const double* X, uint64_t n, uint64_t d, uint32_t layout,
+                          const ph0b_options* opt, uint64_t* columns, uint32_t* rows_lo,
+                          uint32_t* rows_hi, uint64_t* n_columns) {
+    if (n >= 2 && (!columns || !rows_lo || !rows_hi))
+        return fail(PH0B_ERR_INVALID_ARGUMENT, "null output");
+    return supports_impl(X, n, d, layout, opt, columns, rows_lo, rows_hi, n_columns);
 }
 
 }  // extern "C"

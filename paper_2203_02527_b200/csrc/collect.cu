@@ -49,29 +49,46 @@ __global__ void k5_map(const uint64_t* __restrict__ cols_sorted, uint32_t m,
     }
 }
 
-// Claimed low of each surviving column, in filtration order (reduction.cpp:44-45): the larger
-// of the two pivot-tree roots (= minimum vertex of each tree) it joins.  One thread walks the
-// N-1 survivors with a union-find whose root is always the tree minimum; parity surface only.
-__global__ void k5_claimed_lows(const uint32_t* __restrict__ surv_sorted, uint32_t m,
-                                const uint32_t* __restrict__ uv, uint32_t n, uint32_t* lows) {
-    extern __shared__ uint16_t parent[];
+// Reduced support {x, low} (x < low) of each surviving column, in filtration order — the
+// column the reference's reduce() leaves in M (reduction.cpp:33-49) — and its claimed low
+// (reduction.cpp:44-45).  Supports stay 2-sparse (boundary_matrix.cpp:22-24): reducing {a, c}
+// (a < c) against the earlier column that claimed row c, whose support is {parent(c), c},
+// gives {a, parent(c)}; the walk ends when the larger row is unclaimed, and that column then
+// claims it.  Only surviving columns claim rows, so replaying the walk over the N-1 survivors
+// in filtration order reproduces the reference's pivot table and reduced columns exactly
+// (the cycle columns end empty).  One thread, parent table in shared memory: a parity
+// surface, not on the hot path.
+__global__ void k5_reduced_supports(const uint32_t* __restrict__ surv_sorted, uint32_t m,
+                                    const uint32_t* __restrict__ uv, uint32_t n,
+                                    uint32_t* __restrict__ xs, uint32_t* __restrict__ lows,
+                                    uint32_t* __restrict__ err) {
+    extern __shared__ uint16_t parent[];  // parent[r] == r: row r is unclaimed
     for (uint32_t v = threadIdx.x; v < n; v += blockDim.x) parent[v] = (uint16_t)v;
     __syncthreads();
     if (threadIdx.x != 0) return;
-    auto find = [&](uint32_t x) {
-        while (parent[x] != x) {
-            parent[x] = parent[parent[x]];
-            x = parent[x];
-        }
-        return x;
-    };
+    uint32_t bad = 0;
     for (uint32_t i = 0; i < m; ++i) {
         const uint32_t e = uv[surv_sorted[i]];
-        const uint32_t ru = find(e >> 16), rv = find(e & 0xFFFFu);
-        const uint32_t hi = ru > rv ? ru : rv, lo = ru > rv ? rv : ru;
-        lows[i] = hi;
-        parent[hi] = (uint16_t)lo;
+        uint32_t a = e >> 16, c = e & 0xFFFFu;
+        if (a > c) {
+            const uint32_t t = a;
+            a = c;
+            c = t;
+        }
+        while (parent[c] != c) {  // row c claimed by an earlier column {parent(c), c}
+            const uint32_t p = parent[c];
+            if (p == a) {  // the column would empty: not a survivor (cannot happen)
+                bad = 1;
+                break;
+            }
+            c = p > a ? p : a;
+            a = p > a ? a : p;
+        }
+        parent[c] = (uint16_t)a;
+        lows[i] = c;
+        if (xs) xs[i] = a;
     }
+    if (err) *err = bad;
 }
 
 }  // namespace
@@ -101,12 +118,13 @@ int launch_widen(const uint32_t* in, uint32_t m, uint64_t* out, cudaStream_t s) 
     return 1;
 }
 
-int launch_claimed_lows(const uint32_t* surv_sorted, uint32_t m, const uint32_t* uv, uint32_t n,
-                        uint32_t* lows, cudaStream_t s) {
+int launch_reduced_supports(const uint32_t* surv_sorted, uint32_t m, const uint32_t* uv,
+                            uint32_t n, uint32_t* xs, uint32_t* lows, uint32_t* err,
+                            cudaStream_t s) {
     if (m == 0) return 0;
     const size_t smem = sizeof(uint16_t) * ((n + 1) & ~1u);
-    cudaFuncSetAttribute(k5_claimed_lows, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    k5_claimed_lows<<<1, 1024, smem, s>>>(surv_sorted, m, uv, n, lows);
+    if (kernel_blocks_per_sm((const void*)k5_reduced_supports, 1024, smem) < 1) return -1;
+    k5_reduced_supports<<<1, 1024, smem, s>>>(surv_sorted, m, uv, n, xs, lows, err);
     return 1;
 }
 

@@ -8,9 +8,9 @@
 namespace ph0b {
 
 // ---- per-device launch attributes (launch_attr.cpp) -----------------------------------
-// Opts `kern` into `smem` bytes of dynamic shared memory on the current device (when above
-// 48 KB) and returns its resident blocks per SM at `threads` threads (0 on failure).  Cached
-// per (device, kernel, smem, threads); thread-safe.
+// Opts `kern` into `smem` bytes of dynamic shared memory on the current device and returns
+// its resident blocks per SM at `threads` threads (0 on failure).  Cached per (device,
+// kernel, smem, threads); thread-safe.
 int kernel_blocks_per_sm(const void* kern, int threads, size_t smem);
 int device_sm_count();
 
@@ -148,9 +148,12 @@ int launch_collect_map(const uint64_t* cols_sorted, uint32_t m, const uint64_t* 
 int launch_widen(const uint32_t* in, uint32_t m, uint64_t* out, cudaStream_t s);
 int launch_narrow(const uint64_t* in, uint32_t m, uint32_t* out, cudaStream_t s);
 
-// Claimed lows (reduction.cpp:44-45) of survivors in filtration order: single-CTA union-find.
-int launch_claimed_lows(const uint32_t* surv_sorted, uint32_t m, const uint32_t* uv, uint32_t n,
-                        uint32_t* lows, cudaStream_t s);
+// Reduced supports {xs[i], lows[i]} of the survivors in filtration order (reduction.cpp:33-49)
+// and their claimed lows (reduction.cpp:44-45), replaying the reference's column additions
+// over the survivors; xs may be null; *err = 1 if a survivor emptied (internal error).
+int launch_reduced_supports(const uint32_t* surv_sorted, uint32_t m, const uint32_t* uv,
+                            uint32_t n, uint32_t* xs, uint32_t* lows, uint32_t* err,
+                            cudaStream_t s);
 
 // ---- multi-GPU splitter partition (shard.cu) ---------------------------------------------
 int launch_partition(const uint64_t* keys, const uint32_t* vals, uint64_t count,

@@ -1,5 +1,5 @@
-// Per-device launch attributes of the kernels that need more than 48 KB of dynamic shared
-// memory, and their occupancy.  cudaFuncSetAttribute acts on the CURRENT device's context, so
+// Per-device launch attributes of the kernels with dynamic shared memory (the opt-in above
+// 48 KB), and their occupancy.  cudaFuncSetAttribute acts on the CURRENT device's context, so
 // a process that runs on device 1 after device 0 (ph0b_options.device, one context per
 // device, the multi-device path) must opt in again there: the result is cached per
 // (device, kernel, smem, threads) under a lock, and a cache entry is published only once
@@ -24,7 +24,8 @@ int kernel_blocks_per_sm(const void* kern, int threads, size_t smem) {
     std::lock_guard<std::mutex> lock(mu);
     const auto it = cache.find(key);
     if (it != cache.end()) return it->second;
-    if (smem > 48 * 1024 &&
+    // (the opt-in also covers dynamic + static shared memory crossing 48 KB together)
+    if (smem > 0 &&
         cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) !=
             cudaSuccess) {
         cudaGetLastError();

@@ -332,7 +332,7 @@ Status Context::reserve_points(uint64_t n, uint64_t d) {
     G(best_, best_cap_, std::max<uint64_t>(16, 2 * n * 4 + n * 2 + 48));
     G(surv_, surv_cap_, std::max<uint64_t>(4, n * 4));
     G(surv_sorted_, surv_sorted_cap_, std::max<uint64_t>(4, n * 4));
-    G(lows_, lows_cap_, std::max<uint64_t>(4, n * 4));
+    G(lows_, lows_cap_, std::max<uint64_t>(8, n * 8));  // lows | xs
     G(death_grade_, death_grade_cap_, std::max<uint64_t>(8, n * 8));
     G(death_length_, death_length_cap_, std::max<uint64_t>(8, n * 8));
 #undef G
@@ -1255,13 +1255,19 @@ Status Context::stage_kruskal(uint64_t count, uint32_t n, cudaStream_t st, uint3
     return Status::ok();
 }
 
-Status Context::claimed_lows(const RunOutputs& r, uint32_t n, uint32_t* d_lows,
-                             cudaStream_t stream) {
+Status Context::reduced_supports(const RunOutputs& r, uint32_t n, bool want_x,
+                                 cudaStream_t stream) {
     cudaStream_t st = stream ? stream : stream_;
-    launches += launch_claimed_lows(r.d_surv_sorted, (uint32_t)r.n_finite, r.d_uv_sorted, n,
-                                    d_lows, st);
-    PH0B_CHECK_LAUNCH("claimed lows");
-    PH0B_TRY(cudaStreamSynchronize(st), "claimed lows");
+    uint32_t* d_err = reinterpret_cast<uint32_t*>(d_mapped_ + 251);
+    volatile uint32_t* h_err = reinterpret_cast<volatile uint32_t*>(h_mapped_ + 251);
+    *h_err = 0;
+    const int l = launch_reduced_supports(r.d_surv_sorted, (uint32_t)r.n_finite, r.d_uv_sorted,
+                                          n, want_x ? lows_ + n : nullptr, lows_, d_err, st);
+    PH0B_CHECK_LAUNCH("reduced supports");
+    if (l < 0) return {PH0B_ERR_CUDA, "reduced supports: launch configuration failed"};
+    launches += l;
+    PH0B_TRY(cudaStreamSynchronize(st), "reduced supports");
+    if (*h_err) return {PH0B_ERR_CUDA, "internal error: a surviving column reduced to zero"};
     return Status::ok();
 }
 

@@ -56,7 +56,9 @@ public:
     // Host cloud -> device staging buffer, then run().
     Status run_host_input(const double* X, uint64_t n, uint64_t d, uint32_t layout,
                           cudaStream_t stream, StopAfter stop, bool want_grade, RunOutputs* out);
-    Status claimed_lows(const RunOutputs& r, uint32_t n, uint32_t* d_lows, cudaStream_t stream);
+    // Reduced supports {xs, lows} of the survivors (filtration order) into lows_buffer():
+    // lows at [0, n), xs at [n, 2n) when want_x.
+    Status reduced_supports(const RunOutputs& r, uint32_t n, bool want_x, cudaStream_t stream);
 
     // ---- pipeline stages (single-GPU run() composes them; sharded runs call them) ------
     Status stage_distances(const double* dX, uint64_t n, uint64_t d, uint32_t layout,

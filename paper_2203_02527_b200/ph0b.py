@@ -40,7 +40,7 @@ EXPORTED_SYMBOLS = [
     "ph0b_decode_deltas", "ph0b_decode_packed", "ph0b_scale_to_host",
     "ph0b_shard_partition_count", "ph0b_shard_recv_peer",
     "ph0b_shard_scatter_peers", "ph0b_ipc_get_handle", "ph0b_ipc_open_handle", "ph0b_ipc_close",
-    "ph0b_scale_release", "ph0b_host_cache_trim",
+    "ph0b_scale_release", "ph0b_host_cache_trim", "ph0b_reduced_supports",
 ]
 
 
@@ -109,6 +109,8 @@ def lib() -> C.CDLL:
         "ph0b_build_filtration": (C.c_int, [vp, u64, u64, u32, C.POINTER(Options), vp, vp, vp,
                                             vp, u64p]),
         "ph0b_claimed_lows": (C.c_int, [vp, u64, u64, u32, C.POINTER(Options), vp, u64p]),
+        "ph0b_reduced_supports": (C.c_int, [vp, u64, u64, u32, C.POINTER(Options), vp, vp, vp,
+                                            u64p]),
         "ph0b_context_create": (C.c_int, [C.c_int, C.POINTER(vp)]),
         "ph0b_context_destroy": (None, [vp]),
         "ph0b_context_reserve": (C.c_int, [vp, u64, u64]),
@@ -259,6 +261,22 @@ def claimed_lows(X, *, device: int = 0) -> np.ndarray:
     _check(lib().ph0b_claimed_lows(_ptr(Xf), n, d, COL_MAJOR, C.byref(_opts(device)), _ptr(out),
                                    C.byref(m)))
     return out[: m.value].copy()
+
+
+def reduced_supports(X, *, device: int = 0, workers: int = 1, pivoting: bool = True):
+    """The reduced matrix of reduce() (reduction.cpp:33-49) as (columns, rows_lo, rows_hi):
+    surviving column j = columns[i] ends as {rows_lo[i], rows_hi[i]} (rows_hi = its claimed
+    low), every other column ends empty."""
+    Xf, n, d = _as_cloud(X)
+    cols = np.empty(max(n, 1), np.uint64)
+    lo = np.empty(max(n, 1), np.uint32)
+    hi = np.empty(max(n, 1), np.uint32)
+    m = C.c_uint64(0)
+    _check(lib().ph0b_reduced_supports(_ptr(Xf), n, d, COL_MAJOR,
+                                       C.byref(_opts(device, 0, workers, pivoting)), _ptr(cols),
+                                       _ptr(lo), _ptr(hi), C.byref(m)))
+    k = m.value
+    return cols[:k].copy(), lo[:k].copy(), hi[:k].copy()
 
 
 def last_launch_count() -> int:

@@ -32,6 +32,12 @@ def main():
         u, v, g, sc = pkg.build_filtration(X)
         assert np.array_equal(u, ref["u"]) and np.array_equal(v, ref["v"])
         assert np.array_equal(g, ref["grade"])
+    # tie order across many sort tiles decides the surviving columns and their supports
+    g = np.array([[x, y] for x in range(64) for y in range(64)], np.float64)
+    ref = ob.reduce_sparse(ob.filtration(g), stop_at_spanning=True)
+    cols, lo, hi = pkg.reduced_supports(g)
+    assert np.array_equal(cols, ref["columns"]) and np.array_equal(lo, ref["rows_lo"])
+    assert np.array_equal(hi, ref["rows_hi"])
     print("OK")
 
 

@@ -51,6 +51,9 @@ def orc() -> C.CDLL:
         L.orc_generate_cloud.restype = C.c_int
         L.orc_generate_cloud.argtypes = [u32, u64, u64, u64, u32, C.c_double, C.c_double,
                                          C.c_double, u64, vp]
+        L.orc_reduce_sparse.restype = C.c_int64
+        L.orc_reduce_sparse.argtypes = [u64, u64, vp, vp, vp, vp, u64, vp, vp, vp, vp, vp,
+                                        C.POINTER(u64), C.POINTER(u64), C.c_int]
         L.orc_kruskal_barcode.restype = C.c_int64
         L.orc_kruskal_barcode.argtypes = [u64, u64, vp, vp, vp, vp, vp, vp, C.POINTER(u64)]
         _orc = L
@@ -72,6 +75,8 @@ def ref() -> C.CDLL:
         L.ref_build_filtration.argtypes = [vp, u64, u64, vp, vp, vp, vp, C.POINTER(u64)]
         L.ref_h0_barcode.argtypes = [vp, u64, u64, C.c_int, C.c_uint, vp, vp, C.POINTER(u64),
                                      C.POINTER(u64), vp, C.POINTER(u64), vp, vp]
+        L.ref_reduced_matrix.argtypes = [vp, u64, u64, C.c_int, C.c_uint, vp, vp, vp,
+                                         C.POINTER(u64), vp]
         _ref = L
     return _ref
 
@@ -157,6 +162,26 @@ def reduce_bars(f: dict):
                 essential=ess.value, additions=adds.value)
 
 
+def reduce_sparse(f: dict, stop_at_spanning: bool = False):
+    """The literal column reduction with 2-sparse supports: bars, the survivors' column
+    indices and reduced supports {rows_lo, rows_hi}, and the addition count (of the columns
+    processed: all of them unless stop_at_spanning)."""
+    n, k = f["n"], f["k"]
+    dg = np.empty(max(n, 1), np.uint64)
+    dl = np.empty(max(n, 1))
+    cols = np.empty(max(n, 1), np.uint64)
+    lo = np.empty(max(n, 1), np.uint32)
+    hi = np.empty(max(n, 1), np.uint32)
+    ess, adds = u64(0), u64(0)
+    m = orc().orc_reduce_sparse(n, k, _p(f["u"]), _p(f["v"]), _p(f["grade"]), _p(f["scale"]),
+                                len(f["scale"]), _p(dg), _p(dl), _p(cols), _p(lo), _p(hi),
+                                C.byref(ess), C.byref(adds), int(stop_at_spanning))
+    assert m >= 0, m
+    return dict(death_grade=dg[:m].copy(), death_length=dl[:m].copy(), columns=cols[:m].copy(),
+                rows_lo=lo[:m].copy(), rows_hi=hi[:m].copy(), essential=ess.value,
+                additions=adds.value)
+
+
 def kruskal_bars(f: dict):
     n, k = f["n"], f["k"]
     dg = np.empty(max(n, 1), np.uint64)
@@ -197,6 +222,23 @@ def ref_h0(X, mode: int = 0, workers: int = 1, want_scale: bool = True, want_low
     if want_lows:
         out["claimed_low"] = lows[: nf.value].copy()
     return out
+
+
+def ref_reduced_matrix(X, pivoting: bool = True, workers: int = 1):
+    """The reference's whole reduced matrix: (columns, rows_lo, rows_hi) of the nonzero
+    columns, plus ReductionStats (additions, row_ops, probe_ops)."""
+    Xf, n, d = colmajor(X)
+    cols = np.empty(max(n, 1), np.uint64)
+    lo = np.empty(max(n, 1), np.uint32)
+    hi = np.empty(max(n, 1), np.uint32)
+    m = u64(0)
+    st = np.zeros(3, np.uint64)
+    rc = ref().ref_reduced_matrix(_p(Xf), n, d, int(pivoting), workers, _p(cols), _p(lo),
+                                  _p(hi), C.byref(m), _p(st))
+    if rc != 0:
+        raise ValueError(ref().ref_last_error().decode())
+    k = m.value
+    return cols[:k].copy(), lo[:k].copy(), hi[:k].copy(), st
 
 
 def ref_filtration(X):
