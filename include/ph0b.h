@@ -30,8 +30,9 @@ extern "C" {
 
 /* 3: + peer-memory exchange (ph0b_shard_partition_count/recv_peer/scatter_peers, ph0b_ipc_*),
  *    ph0b_scale_to_host, ph0b_decode_packed
- * 4: + ph0b_scale_release, ph0b_host_cache_trim, ph0b_reduced_supports; ph0b_h0_barcode
- *    streams D like ph0b_run_host */
+ * 4: + ph0b_options.n_gpus/devices (in-process multi-GPU), ph0b_scale_release,
+ *    ph0b_host_cache_trim, ph0b_reduced_supports; ph0b_h0_barcode streams D like
+ *    ph0b_run_host */
 #define PH0B_ABI_VERSION 4u
 
 /* Return codes.  The message of ph0b_last_error() repeats the reference's exception text
@@ -70,6 +71,16 @@ typedef struct ph0b_options {
      * reference's message "worker count must be at least 1" (reduction.cpp:134). */
     uint32_t pivoting;
     uint32_t workers;
+    /* ABI 4 — multi-GPU; struct_size of an ABI-3 caller (20 bytes) still
+     * works and means one GPU.  n_gpus > 1: ph0b_h0_barcode / ph0b_h0_barcode_into split the
+     * cloud over that many GPUs of this node in this process — row blocks for the distances,
+     * a splitter partition whose kernel stores every part straight into its destination
+     * GPU's receive buffer (NVLink P2P), local sort/unique (D sharded), the column reduction
+     * continuing the forest from key range to key range, D slices to the host in parallel.
+     * Same results bit for bit.  PH0B_FLAG_KRUSKAL runs on one GPU. */
+    uint32_t n_gpus;          /* 0 or 1: one GPU (`device`) */
+    const int32_t* devices;   /* n_gpus ordinals, or NULL for device, device+1, ...; an
+                                 ordinal may repeat (ranks sharing a GPU: tests) */
 } ph0b_options;
 
 /* Per-stage device milliseconds of the last run (CUDA events on the pipeline stream). */

@@ -59,19 +59,29 @@ struct Opts {
     int device = 0;
     uint32_t flags = 0;
     uint32_t workers = 1;
+    std::vector<int> devices;  // > 1 entries: the multi-GPU path (multi.cpp)
 };
+
+// ph0b_options before ABI 4 ended at `workers`
+constexpr uint32_t kOptionsV3Size = 5 * sizeof(uint32_t);
 
 // Validation mirrors the reference's throws: filtration.cpp:10-11 (N > 2^32-1),
 // reduction.cpp:134 (workers < 1); PH0B_MAX_POINTS is this build's packing limit.
 int parse(const ph0b_options* opt, uint64_t n, uint32_t layout, Opts* o) {
     if (opt && opt->struct_size != 0) {
-        if (opt->struct_size < sizeof(ph0b_options))
+        if (opt->struct_size < kOptionsV3Size)
             return fail(PH0B_ERR_INVALID_ARGUMENT, "ph0b_options.struct_size too small");
         o->device = opt->device;
         o->flags = opt->flags;
         o->workers = opt->workers;
         if (opt->workers < 1)
             return fail(PH0B_ERR_INVALID_ARGUMENT, "worker count must be at least 1");
+        if (opt->struct_size >= sizeof(ph0b_options) && opt->n_gpus > 1) {
+            if (opt->n_gpus > 64)
+                return fail(PH0B_ERR_INVALID_ARGUMENT, "n_gpus must be at most 64");
+            for (uint32_t i = 0; i < opt->n_gpus; ++i)
+                o->devices.push_back(opt->devices ? opt->devices[i] : opt->device + (int)i);
+        }
     }
     if (layout != PH0B_COL_MAJOR && layout != PH0B_ROW_MAJOR)
         return fail(PH0B_ERR_INVALID_ARGUMENT, "layout must be PH0B_COL_MAJOR or PH0B_ROW_MAJOR");
@@ -158,6 +168,13 @@ ResultCache& result_cache() {
     return *c;
 }
 
+// The multi-GPU path: several devices requested, a cloud big enough to split (the per-rank
+// stages cost fixed latency), and not the union-find variant (single GPU by definition).
+bool use_multi(const Opts& o, uint64_t n) {
+    return o.devices.size() > 1 && !(o.flags & PH0B_FLAG_KRUSKAL) &&
+           n * (n - (n > 0)) / 2 >= (uint64_t)o.devices.size() * 4096;
+}
+
 // Host-side finiteness check (PointCloud ctor, point_cloud.cpp:15-18) before any device work.
 bool all_finite(const double* x, uint64_t count) {
     for (uint64_t i = 0; i < count; ++i)
@@ -200,6 +217,10 @@ int copy_out(Context* c, const RunOutputs& r, cudaStream_t s, uint64_t* death_gr
 }  // namespace
 
 namespace ph0b {
+int run_multi_gpu(const std::vector<int>& devices, const double* X, uint64_t n, uint64_t d,
+                  uint32_t layout, uint64_t* death_grade, double* death_length,
+                  uint64_t* n_finite, uint64_t* essential, double* scale,
+                  uint64_t scale_capacity, uint64_t* n_scale, ph0b_stage_times* times);
 int capi_fail(const Status& s) { return fail(s); }
 int capi_fail(int code, const std::string& msg) { return fail(code, msg); }
 void capi_set_launches(uint64_t n) { g_last_launches = n; }
@@ -437,9 +458,13 @@ int ph0b_h0_barcode_into(const double* X, uint64_t n, uint64_t d, uint32_t layou
     if (n * d && !X) return fail(PH0B_ERR_INVALID_ARGUMENT, "null point cloud");
     if (!all_finite(X, n * d))
         return fail(PH0B_ERR_NONFINITE, "point cloud contains non-finite coordinates");
+    if (o.flags & PH0B_FLAG_NO_SCALE) scale = nullptr;
+    if (use_multi(o, n))
+        return ph0b::run_multi_gpu(o.devices, X, n, d, layout, death_grade, death_length,
+                                   n_finite, essential_count, scale, scale_capacity, n_scale,
+                                   times);
     Context* c = ctx_for(o.device, &rc);
     if (!c) return rc;
-    if (o.flags & PH0B_FLAG_NO_SCALE) scale = nullptr;
     std::lock_guard<std::mutex> lk(c->mu);
     return run_host_locked(c, X, n, d, layout, nullptr, death_grade, death_length, n_finite,
                            essential_count, scale, scale_capacity, n_scale, times,
@@ -456,13 +481,32 @@ int ph0b_h0_barcode(const double* X, uint64_t n, uint64_t d, uint32_t layout,
     if (n * d && !X) return fail(PH0B_ERR_INVALID_ARGUMENT, "null point cloud");
     if (!all_finite(X, n * d))
         return fail(PH0B_ERR_NONFINITE, "point cloud contains non-finite coordinates");
+    const bool want_scale = !(o.flags & PH0B_FLAG_NO_SCALE);
+    const uint64_t k = n * (n - (n > 0)) / 2;
+    if (use_multi(o, n)) {
+        out->death_grade = static_cast<uint64_t*>(std::malloc(std::max<uint64_t>(1, n) * 8));
+        out->death_length = static_cast<double*>(std::malloc(std::max<uint64_t>(1, n) * 8));
+        if (want_scale) out->scale = static_cast<double*>(result_cache().take(k * 8));
+        if (!out->death_grade || !out->death_length || (want_scale && !out->scale)) {
+            ph0b_result_free(out);
+            return fail(PH0B_ERR_OUT_OF_MEMORY, "host allocation of the result failed");
+        }
+        rc = ph0b::run_multi_gpu(o.devices, X, n, d, layout, out->death_grade,
+                                 out->death_length, &out->n_finite, &out->essential_count,
+                                 out->scale, want_scale ? k : 0, &out->n_scale, &out->times);
+        if (rc) {
+            const std::string msg = g_last_error;
+            ph0b_result_free(out);
+            std::memset(out, 0, sizeof(*out));
+            return fail(rc, msg);
+        }
+        return PH0B_OK;
+    }
     Context* c = ctx_for(o.device, &rc);
     if (!c) return rc;
     std::lock_guard<std::mutex> lk(c->mu);
     cudaStream_t s = c->own_stream();
     RunOutputs r;
-    const bool want_scale = !(o.flags & PH0B_FLAG_NO_SCALE);
-    const uint64_t k = n * (n - (n > 0)) / 2;
     // Large clouds returning D take the same bucketed path as ph0b_run_host: D streams to the
     // host while the sort is still running, decoded straight into the result buffer (sized by
     // K >= |D|; a reused buffer from the result cache has no page faults left to take).

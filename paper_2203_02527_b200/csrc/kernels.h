@@ -109,9 +109,13 @@ struct ReduceStats {
     uint32_t survivors = 0;
     int launches = 0;
 };
-// Runs the full reduction; leaves survivor column ids (unordered) in st.surv.
+// Runs the full reduction; leaves survivor column ids (unordered) in st.surv and the final
+// tree labels in st.comp.  init_comp (device, optional): labels left by the reduction of the
+// preceding part of the filtration (a continued forest); target: stop after this many
+// survivors (0: n - 1).
 int run_reduction(ReduceState& st, cudaStream_t s, int num_sms, uint32_t& epoch,
-                  ReduceStats* stats);
+                  ReduceStats* stats, const uint32_t* init_comp = nullptr,
+                  uint32_t target = 0);
 
 // ---- K9: compressed D for the host path (d2h_codec.cu) ----------------------------------
 // Packed stream of the slice [lohi[0], lohi[1]) of d (device words; n_upper >= its length):

@@ -562,7 +562,7 @@ Status Context::stage_sort_unique(uint64_t k, uint64_t kmin, uint64_t kmax, bool
 }
 
 Status Context::stage_reduce(const uint32_t* uv, uint64_t count, uint32_t n, cudaStream_t st,
-                             ReduceStats* rst) {
+                             ReduceStats* rst, const uint32_t* init_comp, uint32_t target) {
     ReduceState rs{};
     rs.n = n;
     rs.k = count;
@@ -577,7 +577,7 @@ Status Context::stage_reduce(const uint32_t* uv, uint64_t count, uint32_t n, cud
     rs.host_counters = reinterpret_cast<uint32_t*>(h_mapped_ + 128);
     rs.mapped_counters = reinterpret_cast<uint32_t*>(d_mapped_ + 128);
     uint32_t ep = 0;
-    run_reduction(rs, st, num_sms_, ep, rst);
+    run_reduction(rs, st, num_sms_, ep, rst, init_comp, target);
     launches += rst->launches;
     PH0B_CHECK_LAUNCH("reduction");
     return Status::ok();
@@ -734,8 +734,8 @@ Status Context::prepare_stream(uint64_t k, uint32_t B) {
             return e ? atoi(e) : 0;
         }();
         const unsigned hw = std::thread::hardware_concurrency();
-        pool_ = std::make_unique<DecodePool>(
-            env_threads > 0 ? (unsigned)env_threads : (hw > 2 ? hw - 1 : 1));
+        const unsigned dflt = decode_threads_ ? decode_threads_ : (hw > 2 ? hw - 1 : 1);
+        pool_ = std::make_unique<DecodePool>(env_threads > 0 ? (unsigned)env_threads : dflt);
     }
     return Status::ok();
 }

@@ -66,8 +66,12 @@ public:
                            uint64_t* kmin, uint64_t* kmax);
     Status stage_sort_unique(uint64_t count, uint64_t kmin, uint64_t kmax, bool raw_hist,
                              bool want_grade, cudaStream_t st, uint32_t* passes, int src = 0);
+    // init_comp/target: continue the forest of a preceding part of the filtration (device
+    // labels, this device) and stop after `target` survivors (see run_reduction)
     Status stage_reduce(const uint32_t* uv, uint64_t count, uint32_t n, cudaStream_t st,
-                        ReduceStats* rst);
+                        ReduceStats* rst, const uint32_t* init_comp = nullptr,
+                        uint32_t target = 0);
+    uint32_t* comp() { return comp_; }
     // Sort (kb0, vb0) of k edges (ping-pong with kb1/vb1) and write its distinct lengths to
     // scale_out (null: the free key buffer) starting at *d_base (null: 0); *d_count receives
     // base + |D|.  *res: 0/1 = buffer holding the sorted data.
@@ -110,6 +114,10 @@ public:
     uint32_t epochs(uint32_t count, cudaStream_t s) { return next_epochs(count, s); }
     uint32_t* lows_buffer() { return lows_; }
 
+    // host threads decoding this context's D stream (0: cores - 1); set before the first
+    // host-output call (several contexts of one process share the cores)
+    void set_decode_threads(unsigned t) { decode_threads_ = t; }
+
     std::mutex mu;
     int device() const { return device_; }
     cudaStream_t own_stream() const { return stream_; }
@@ -117,6 +125,7 @@ public:
 
 private:
     Status grow(void** p, uint64_t* cap_bytes, uint64_t need_bytes);
+    unsigned decode_threads_ = 0;
     uint32_t next_epochs(uint32_t count, cudaStream_t s);
 
     int device_;

@@ -46,12 +46,16 @@ constexpr int kCntSurv = 1;      // surviving columns found so far
 constexpr int kCntHooks = 2;     // hooks made by the last resolve round
 constexpr int kCntOverflow = 3;  // filter exceeded the candidate capacity
 
+// Labels start as singletons, or (continuing an earlier range of the filtration, e.g. the
+// previous rank's key range) as that range's final labels: every label is a tree root, and a
+// root's hook parent is itself.
 __global__ void k4_init(uint32_t* comp, uint32_t* best, uint32_t* par, uint32_t n,
-                        uint16_t* comp16) {
+                        uint16_t* comp16, const uint32_t* __restrict__ init) {
     for (uint32_t v = blockIdx.x * blockDim.x + threadIdx.x; v < n; v += gridDim.x * blockDim.x) {
-        comp[v] = v;
-        comp16[v] = (uint16_t)v;
-        par[v] = v;
+        const uint32_t c = init ? init[v] : v;
+        comp[v] = c;
+        comp16[v] = (uint16_t)c;
+        par[v] = c;
         best[v] = kNone;
     }
 }
@@ -292,7 +296,7 @@ inline unsigned grid_for(uint64_t work, int num_sms, int per_sm = 8) {
 }  // namespace
 
 int run_reduction(ReduceState& st, cudaStream_t s, int num_sms, uint32_t& epoch,
-                  ReduceStats* stats) {
+                  ReduceStats* stats, const uint32_t* init_comp, uint32_t target) {
     (void)epoch;
     ReduceStats local;
     ReduceStats& S = stats ? *stats : local;
@@ -306,7 +310,8 @@ int run_reduction(ReduceState& st, cudaStream_t s, int num_sms, uint32_t& epoch,
     uint16_t* comp16 = reinterpret_cast<uint16_t*>(st.best + ((2ull * n + 3) & ~3ull));
     const unsigned gn = grid_for(n, num_sms, 4);
     cudaMemsetAsync(st.counters, 0, sizeof(uint32_t) * 8, s);
-    k4_init<<<gn, kThreads, 0, s>>>(st.comp, st.best, par, n, comp16);
+    k4_init<<<gn, kThreads, 0, s>>>(st.comp, st.best, par, n, comp16, init_comp);
+    if (target == 0 || target > n - 1) target = n - 1;
     S.launches += 1;
 
     volatile uint32_t* h = st.host_counters;
@@ -331,7 +336,7 @@ int run_reduction(ReduceState& st, cudaStream_t s, int num_sms, uint32_t& epoch,
     uint64_t pos = 0;
     uint64_t window = std::min<uint64_t>(st.k, std::max<uint64_t>(8ull * n, 1u << 16));
     uint32_t survivors = 0;
-    while (survivors < n - 1 && pos < st.k) {
+    while (survivors < target && pos < st.k) {
         uint64_t end = std::min<uint64_t>(st.k, pos + window);
         // (i) clearing filter over the window
         cudaMemsetAsync(st.counters + kCntCand, 0, sizeof(uint32_t), s);

@@ -57,7 +57,8 @@ class InvalidArgument(Ph0bError, ValueError):
 
 class Options(C.Structure):
     _fields_ = [("struct_size", C.c_uint32), ("device", C.c_int32), ("flags", C.c_uint32),
-                ("pivoting", C.c_uint32), ("workers", C.c_uint32)]
+                ("pivoting", C.c_uint32), ("workers", C.c_uint32), ("n_gpus", C.c_uint32),
+                ("devices", C.POINTER(C.c_int32))]
 
 
 class StageTimes(C.Structure):
@@ -144,8 +145,15 @@ def _check(rc: int):
     raise Ph0bError(rc, msg)
 
 
-def _opts(device: int = 0, flags: int = 0, workers: int = 1, pivoting: bool = True) -> Options:
-    return Options(C.sizeof(Options), device, flags, int(pivoting), workers)
+def _opts(device: int = 0, flags: int = 0, workers: int = 1, pivoting: bool = True,
+          devices=None) -> Options:
+    o = Options(C.sizeof(Options), device, flags, int(pivoting), workers)
+    if devices is not None and len(devices) > 1:
+        arr = (C.c_int32 * len(devices))(*devices)
+        o.n_gpus = len(devices)
+        o.devices = C.cast(arr, C.POINTER(C.c_int32))
+        o._keep = arr  # the array lives as long as the options
+    return o
 
 
 def _as_cloud(X) -> tuple[np.ndarray, int, int]:
@@ -192,14 +200,15 @@ def _take_scale(res) -> np.ndarray:
 
 
 def h0_barcode(X, *, device: int = 0, return_scale: bool = True, workers: int = 1,
-               pivoting: bool = True, kruskal: bool = False) -> Barcode:
+               pivoting: bool = True, kruskal: bool = False, devices=None) -> Barcode:
     """pairwise_distances ∘ build_filtration ∘ build_boundary_matrix ∘ reduce ∘ extract_barcode
-    (kruskal=True: the union-find barcode of oracle.cpp:32-46 over the same GPU filtration)."""
+    (kruskal=True: the union-find barcode of oracle.cpp:32-46 over the same GPU filtration;
+    devices=[...]: the in-process multi-GPU path over those ordinals, repeats allowed)."""
     Xf, n, d = _as_cloud(X)
     L = lib()
     res = Result()
     flags = (0 if return_scale else FLAG_NO_SCALE) | (FLAG_KRUSKAL if kruskal else 0)
-    opt = _opts(device, flags, workers, pivoting)
+    opt = _opts(device, flags, workers, pivoting, devices)
     rc = L.ph0b_h0_barcode(_ptr(Xf), n, d, COL_MAJOR, C.byref(opt), C.byref(res))
     _check(rc)
     try:
