@@ -46,10 +46,12 @@ extern "C" {
 #define PH0B_ERR_NO_DEVICE 6        /* no sm_100 device visible */
 #define PH0B_ERR_CAPACITY 7         /* caller-provided output buffer too small */
 
-/* Vertex ids are packed 16+16 bits into one u32 per edge column (u << 16 | v); the
- * reference allows N <= 2^32-1 (filtration.cpp:10-11) but its K x N-bit matrix cannot go
- * past N ~ 10^4 in practice. */
-#define PH0B_MAX_POINTS 65536u
+/* Each edge column travels through the sort as one u32: u << 16 | v for N <= 65536, the
+ * u-major edge index above (K = N(N-1)/2 < 2^32 up to N = 92682).  The reference allows
+ * N <= 2^32-1 (filtration.cpp:10-11) but its K x N-bit matrix cannot go past N ~ 10^4 in
+ * practice; one B200 holds the whole pipeline to N = 92682 (K = 4.3e9 edges,
+ * ~110 GB of keys, columns and ping-pong buffers).  PH0B_FLAG_KRUSKAL: N <= 65536. */
+#define PH0B_MAX_POINTS 92682u
 
 /* Layout of X. */
 #define PH0B_COL_MAJOR 0u /* Eigen::MatrixXd storage (point_cloud.hpp:30): x(i,j) at j*N + i */
@@ -130,6 +132,10 @@ void ph0b_result_free(ph0b_result* r);
  * ph0b_host_cache_trim() returns the idle ones to the system. */
 void ph0b_scale_release(double* scale);
 void ph0b_host_cache_trim(void);
+/* Frees what the library keeps between calls for speed: the multi-GPU runners (their
+ * per-GPU contexts and buffers) and the idle result buffers.  The next call re-creates
+ * what it needs. */
+void ph0b_release_resources(void);
 
 /* Same, writing into caller-provided host buffers (no allocation inside the call; pinned
  * buffers from ph0b_host_alloc give full PCIe bandwidth).  death_* need n-1 entries,

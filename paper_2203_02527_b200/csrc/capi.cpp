@@ -13,6 +13,7 @@
 #include <vector>
 
 #include "../../include/ph0b.h"
+#include "colcodec.h"
 #include "host_decode.h"
 #include "pipeline.h"
 
@@ -87,6 +88,8 @@ int parse(const ph0b_options* opt, uint64_t n, uint32_t layout, Opts* o) {
         return fail(PH0B_ERR_INVALID_ARGUMENT, "layout must be PH0B_COL_MAJOR or PH0B_ROW_MAJOR");
     if (n > 0xFFFFFFFFull)
         return fail(PH0B_ERR_TOO_LARGE, "point cloud too large for 32-bit vertex indices");
+    if ((o->flags & PH0B_FLAG_KRUSKAL) && n > ph0b::kPackedMaxN)
+        return fail(PH0B_ERR_TOO_LARGE, "union-find forest is limited to 65536 points");
     if (n > PH0B_MAX_POINTS)
         return fail(PH0B_ERR_TOO_LARGE,
                     "point cloud too large for this build (N <= " +
@@ -221,6 +224,7 @@ int run_multi_gpu(const std::vector<int>& devices, const double* X, uint64_t n, 
                   uint32_t layout, uint64_t* death_grade, double* death_length,
                   uint64_t* n_finite, uint64_t* essential, double* scale,
                   uint64_t scale_capacity, uint64_t* n_scale, ph0b_stage_times* times);
+void release_multi_gpu();
 int capi_fail(const Status& s) { return fail(s); }
 int capi_fail(int code, const std::string& msg) { return fail(code, msg); }
 void capi_set_launches(uint64_t n) { g_last_launches = n; }
@@ -584,6 +588,11 @@ void ph0b_scale_release(double* scale) { result_cache().give(scale); }
 
 void ph0b_host_cache_trim(void) { result_cache().trim(); }
 
+void ph0b_release_resources(void) {
+    ph0b::release_multi_gpu();
+    result_cache().trim();
+}
+
 void ph0b_result_free(ph0b_result* r) {
     if (!r) return;
     std::free(r->death_grade);
@@ -643,8 +652,10 @@ int ph0b_build_filtration(const double* X, uint64_t n, uint64_t d, uint32_t layo
         cudaStreamSynchronize(s))
         return fail(PH0B_ERR_CUDA, "D2H filtration");
     for (uint64_t i = 0; i < r.k; ++i) {
-        if (u) u[i] = uv[i] >> 16;
-        if (v) v[i] = uv[i] & 0xFFFFu;
+        uint32_t a, b;
+        ph0b::col_rows(uv[i], n, a, b);
+        if (u) u[i] = a;
+        if (v) v[i] = b;
         if (grade) grade[i] = g[i];
     }
     return PH0B_OK;

@@ -58,25 +58,35 @@ __global__ void k5_map(const uint64_t* __restrict__ cols_sorted, uint32_t m,
 // in filtration order reproduces the reference's pivot table and reduced columns exactly
 // (the cycle columns end empty).  One thread, parent table in shared memory: a parity
 // surface, not on the hot path.
+// kWide (N > 65536): rows do not fit u16 and the table does not fit shared memory — a u32
+// parent table in global memory (gparent, n entries).
+template <bool kWide>
 __global__ void k5_reduced_supports(const uint32_t* __restrict__ surv_sorted, uint32_t m,
                                     const uint32_t* __restrict__ uv, uint32_t n,
                                     uint32_t* __restrict__ xs, uint32_t* __restrict__ lows,
-                                    uint32_t* __restrict__ err) {
-    extern __shared__ uint16_t parent[];  // parent[r] == r: row r is unclaimed
-    for (uint32_t v = threadIdx.x; v < n; v += blockDim.x) parent[v] = (uint16_t)v;
+                                    uint32_t* __restrict__ err, uint32_t* __restrict__ gparent) {
+    extern __shared__ uint16_t s_parent[];  // parent[r] == r: row r is unclaimed
+    for (uint32_t v = threadIdx.x; v < n; v += blockDim.x) {
+        if (kWide)
+            gparent[v] = v;
+        else
+            s_parent[v] = (uint16_t)v;
+    }
+    if (kWide) __threadfence_block();
     __syncthreads();
     if (threadIdx.x != 0) return;
+    auto parent = [&](uint32_t r) -> uint32_t { return kWide ? gparent[r] : s_parent[r]; };
     uint32_t bad = 0;
     for (uint32_t i = 0; i < m; ++i) {
-        const uint32_t e = uv[surv_sorted[i]];
-        uint32_t a = e >> 16, c = e & 0xFFFFu;
+        uint32_t a, c;
+        col_rows(uv[surv_sorted[i]], n, a, c);
         if (a > c) {
             const uint32_t t = a;
             a = c;
             c = t;
         }
-        while (parent[c] != c) {  // row c claimed by an earlier column {parent(c), c}
-            const uint32_t p = parent[c];
+        while (parent(c) != c) {  // row c claimed by an earlier column {parent(c), c}
+            const uint32_t p = parent(c);
             if (p == a) {  // the column would empty: not a survivor (cannot happen)
                 bad = 1;
                 break;
@@ -84,7 +94,10 @@ __global__ void k5_reduced_supports(const uint32_t* __restrict__ surv_sorted, ui
             c = p > a ? p : a;
             a = p > a ? a : p;
         }
-        parent[c] = (uint16_t)a;
+        if (kWide)
+            gparent[c] = a;
+        else
+            s_parent[c] = (uint16_t)a;
         lows[i] = c;
         if (xs) xs[i] = a;
     }
@@ -120,11 +133,17 @@ int launch_widen(const uint32_t* in, uint32_t m, uint64_t* out, cudaStream_t s) 
 
 int launch_reduced_supports(const uint32_t* surv_sorted, uint32_t m, const uint32_t* uv,
                             uint32_t n, uint32_t* xs, uint32_t* lows, uint32_t* err,
-                            cudaStream_t s) {
+                            uint32_t* scratch, cudaStream_t s) {
     if (m == 0) return 0;
+    if (col_ids(n)) {
+        k5_reduced_supports<true><<<1, 1024, 0, s>>>(surv_sorted, m, uv, n, xs, lows, err,
+                                                     scratch);
+        return 1;
+    }
     const size_t smem = sizeof(uint16_t) * ((n + 1) & ~1u);
-    if (kernel_blocks_per_sm((const void*)k5_reduced_supports, 1024, smem) < 1) return -1;
-    k5_reduced_supports<<<1, 1024, smem, s>>>(surv_sorted, m, uv, n, xs, lows, err);
+    if (kernel_blocks_per_sm((const void*)k5_reduced_supports<false>, 1024, smem) < 1) return -1;
+    k5_reduced_supports<false><<<1, 1024, smem, s>>>(surv_sorted, m, uv, n, xs, lows, err,
+                                                      nullptr);
     return 1;
 }
 

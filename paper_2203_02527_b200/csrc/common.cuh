@@ -4,6 +4,8 @@
 #include <cstdint>
 #include <cuda_runtime.h>
 
+#include "colcodec.h"
+
 namespace ph0b {
 
 constexpr int kWarp = 32;
@@ -86,10 +88,5 @@ __device__ __forceinline__ uint32_t lookback_window(const uint64_t* status, uint
     return excl;
 }
 
-// Upper-triangle edge indexing in the reference's u-major order (filtration.cpp:14-15):
-// e(u, v) = u*(2N-u-1)/2 + (v-u-1) for u < v.
-__host__ __device__ __forceinline__ uint64_t row_base(uint64_t u, uint64_t n) {
-    return u * (2 * n - u - 1) / 2;
-}
 
 }  // namespace ph0b

@@ -10,7 +10,8 @@
 //   rounded sqrt, compiled with no FMA (proj/CMakeLists.txt:8-10).  The
 //   explicit __dsub_rn/__dmul_rn/__dadd_rn/__dsqrt_rn keep nvcc from contracting to DFMA.
 // * Output is the reference's u-major edge order (filtration.cpp:14-15):
-//   key[e] = bits(length) (monotone for lengths >= +0), val[e] = u << 16 | v.  Each warp
+//   key[e] = bits(length) (monotone for lengths >= +0), val[e] = the column value of {u, v}
+//   (u << 16 | v, or the edge index above N = 65536: colcodec.h).  Each warp
 //   writes 32 consecutive edges of one row per store.  Running min/max key and the
 //   histogram of the raw low key byte feed the radix sort's first pass.
 #include <cuda.h>
@@ -106,7 +107,7 @@ __device__ __forceinline__ void tile_edges(const double* __restrict__ xu_src,
                 const uint64_t key = static_cast<uint64_t>(__double_as_longlong(len));
                 const uint64_t e = base + v;
                 keys[e] = key;
-                vals[e] = (u << 16) | v;
+                vals[e] = col_value(u, v, e + e_off, nn);
                 kmin = key < kmin ? key : kmin;
                 kmax = key > kmax ? key : kmax;
                 if (sh_hist) atomicAdd(&sh_hist[key & 0xFFu], 1u);

@@ -5,6 +5,8 @@
 #include <cuda.h>
 #include <cuda_runtime.h>
 
+#include "colcodec.h"
+
 namespace ph0b {
 
 // ---- per-device launch attributes (launch_attr.cpp) -----------------------------------
@@ -154,10 +156,11 @@ int launch_narrow(const uint64_t* in, uint32_t m, uint32_t* out, cudaStream_t s)
 
 // Reduced supports {xs[i], lows[i]} of the survivors in filtration order (reduction.cpp:33-49)
 // and their claimed lows (reduction.cpp:44-45), replaying the reference's column additions
-// over the survivors; xs may be null; *err = 1 if a survivor emptied (internal error).
+// over the survivors; xs may be null; *err = 1 if a survivor emptied (internal error);
+// scratch: n u32 of device memory (used above N = 65536).
 int launch_reduced_supports(const uint32_t* surv_sorted, uint32_t m, const uint32_t* uv,
                             uint32_t n, uint32_t* xs, uint32_t* lows, uint32_t* err,
-                            cudaStream_t s);
+                            uint32_t* scratch, cudaStream_t s);
 
 // ---- multi-GPU splitter partition (shard.cu) ---------------------------------------------
 int launch_partition(const uint64_t* keys, const uint32_t* vals, uint64_t count,
@@ -172,13 +175,15 @@ int launch_partition_count(const uint64_t* keys, uint64_t count, const uint64_t*
                            uint32_t parts, uint32_t* d_counts_scratch, uint64_t* d_totals,
                            uint64_t* d_bminmax, uint64_t* keys_out, uint32_t* vals_out,
                            cudaStream_t s, uint32_t align, uint64_t kmin, uint64_t kmax,
-                           const uint64_t* h_splitters, uint16_t* d_table);
+                           const uint64_t* h_splitters, uint16_t* d_table,
+                           uint32_t pad_val = 0);
 int launch_partition_select(const uint64_t* keys, const uint32_t* vals, uint64_t count,
                             uint32_t parts, uint32_t bucket, const uint32_t* d_counts_scratch,
                             const uint64_t* d_totals, const uint64_t* d_bminmax,
                             uint64_t* keys_out, uint32_t* vals_out, cudaStream_t s);
+// pad_val: the cycle column of this N (col_cycle, colcodec.h) in the padding slots
 int launch_partition_pad(const uint64_t* d_totals, uint32_t parts, uint32_t align,
-                         uint64_t* keys, uint32_t* vals, cudaStream_t s);
+                         uint64_t* keys, uint32_t* vals, cudaStream_t s, uint32_t pad_val = 0);
 int launch_partition_scatter(const uint64_t* keys, const uint32_t* vals, uint64_t count,
                              const uint64_t* d_splitters, uint32_t parts,
                              const uint32_t* d_counts_scratch, const uint64_t* d_totals,

@@ -324,13 +324,23 @@ public:
         return PH0B_OK;
     }
 
-    std::mutex mu;
-
 private:
     std::vector<Rank> ranks_;
 };
 
 }  // namespace
+
+std::mutex g_runners_mu;
+std::map<std::vector<int>, std::unique_ptr<MultiRunner>>& runners() {
+    static auto* r = new std::map<std::vector<int>, std::unique_ptr<MultiRunner>>();
+    return *r;
+}
+
+// Frees every cached runner (their contexts and device buffers); ph0b_release_resources.
+void release_multi_gpu() {
+    std::lock_guard<std::mutex> lk(g_runners_mu);
+    runners().clear();
+}
 
 // The multi-GPU run of ph0b_h0_barcode / ph0b_h0_barcode_into: one runner (contexts, receive
 // buffers, decode pools) per device list, reused across calls.
@@ -338,17 +348,10 @@ int run_multi_gpu(const std::vector<int>& devices, const double* X, uint64_t n, 
                   uint32_t layout, uint64_t* death_grade, double* death_length,
                   uint64_t* n_finite, uint64_t* essential, double* scale,
                   uint64_t scale_capacity, uint64_t* n_scale, ph0b_stage_times* times) {
-    static std::mutex mu;
-    static std::map<std::vector<int>, std::unique_ptr<MultiRunner>> runners;
-    MultiRunner* m = nullptr;
-    {
-        std::lock_guard<std::mutex> lk(mu);
-        auto& slot = runners[devices];
-        if (!slot) slot = std::make_unique<MultiRunner>(devices);
-        m = slot.get();
-    }
-    std::lock_guard<std::mutex> lk(m->mu);
-    return m->run(X, n, d, layout, death_grade, death_length, n_finite, essential, scale,
+    std::lock_guard<std::mutex> lk(g_runners_mu);  // one multi-GPU run at a time
+    auto& slot = runners()[devices];
+    if (!slot) slot = std::make_unique<MultiRunner>(devices);
+    return slot->run(X, n, d, layout, death_grade, death_length, n_finite, essential, scale,
                   scale_capacity, n_scale, times);
 }
 

@@ -60,8 +60,6 @@ inline uint32_t truncated_plan(uint64_t span, uint32_t max_passes, SortPlan* pla
     return low;
 }
 
-inline uint64_t row_base(uint64_t u, uint64_t n) { return u * (2 * n - u - 1) / 2; }
-
 // PH0B_TRACE=1: host-side timeline of the overlapped host path on stderr (diagnostics only).
 struct Trace {
     bool on;
@@ -964,7 +962,7 @@ Status Context::run_host_overlapped(const double* X, uint64_t n, uint64_t d, uin
     uint16_t* d_table = reinterpret_cast<uint16_t*>(part_small_ + 1280);
     const int lc = launch_partition_count(keys_[0], k, d_spl, B, part_counts_, d_tot, d_mm,
                                           keys_[1], vals_[1], st, kAlign, kmin, kmax, spl.data(),
-                                          d_table);
+                                          d_table, col_cycle(n));
     if (lc < 0) return {PH0B_ERR_INVALID_ARGUMENT, "partition: bad bucket count"};
     launches += lc;
     PH0B_CHECK_LAUNCH("partition counts");
@@ -1173,7 +1171,8 @@ Status Context::run_host_overlapped(const double* X, uint64_t n, uint64_t d, uin
     const uint64_t kpad = start;  // columns incl. the sentinel padding
     if (target < 0) target = 0;
     // padding slots of M hold the cycle column {0, 0} in whichever buffer M ended up
-    launches += launch_partition_pad(d_tot, B, kAlign, keys_[target], vals_[target], st);
+    launches += launch_partition_pad(d_tot, B, kAlign, keys_[target], vals_[target], st,
+                                     col_cycle(n));
     PH0B_TRY(cudaEventRecord(ev_[2], st), "event");
     PH0B_TRY(cudaEventRecord(ev_[3], st), "event");
     cur_ = target;
@@ -1262,7 +1261,8 @@ Status Context::reduced_supports(const RunOutputs& r, uint32_t n, bool want_x,
     volatile uint32_t* h_err = reinterpret_cast<volatile uint32_t*>(h_mapped_ + 251);
     *h_err = 0;
     const int l = launch_reduced_supports(r.d_surv_sorted, (uint32_t)r.n_finite, r.d_uv_sorted,
-                                          n, want_x ? lows_ + n : nullptr, lows_, d_err, st);
+                                          n, want_x ? lows_ + n : nullptr, lows_, d_err, comp_,
+                                          st);
     PH0B_CHECK_LAUNCH("reduced supports");
     if (l < 0) return {PH0B_ERR_CUDA, "reduced supports: launch configuration failed"};
     launches += l;

@@ -65,7 +65,7 @@ __global__ void __launch_bounds__(kThreads)
     k4_filter(const uint32_t* __restrict__ uv, uint64_t begin, uint64_t end,
               const uint32_t* __restrict__ list, uint32_t list_n,
               const uint32_t* __restrict__ comp, uint32_t* __restrict__ out, uint64_t cap,
-              uint32_t* counters) {
+              uint32_t* counters, uint32_t n) {
     const uint64_t total = list ? (uint64_t)list_n : end - begin;
     const uint32_t lane = threadIdx.x & 31;
     const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
@@ -75,8 +75,9 @@ __global__ void __launch_bounds__(kThreads)
         uint32_t j = 0;
         if (i < total) {
             j = list ? list[i] : (uint32_t)(begin + i);
-            const uint32_t e = __ldg(uv + j);
-            keep = __ldg(comp + (e >> 16)) != __ldg(comp + (e & 0xFFFFu));
+            uint32_t a, b;
+            col_rows(__ldg(uv + j), n, a, b);
+            keep = __ldg(comp + a) != __ldg(comp + b);
         }
         const uint32_t ballot = __ballot_sync(0xffffffffu, keep);
         if (ballot) {
@@ -95,10 +96,12 @@ __global__ void __launch_bounds__(kThreads)
 
 // Clearing filter over a window of the filtration with 8 columns per thread (two 16-byte
 // loads, 16 independent label gathers from a 128 KB u16 label copy that stays in L1).
+// kIds (N > 65536, edge-id columns, colcodec.h): the labels are the u32 ones.
+template <bool kIds>
 __global__ void __launch_bounds__(kThreads)
     k4_filter_range(const uint32_t* __restrict__ uv, uint64_t begin, uint64_t end,
-                    const uint16_t* __restrict__ comp16, uint32_t* __restrict__ out, uint64_t cap,
-                    uint32_t* counters) {
+                    const uint16_t* __restrict__ comp16, const uint32_t* __restrict__ comp,
+                    uint32_t n, uint32_t* __restrict__ out, uint64_t cap, uint32_t* counters) {
     const uint32_t lane = threadIdx.x & 31;
     const uint64_t a0 = begin & ~7ull;  // 8-column (32 B) aligned groups
     const uint64_t groups = (end - a0 + 7) / 8;
@@ -118,11 +121,18 @@ __global__ void __launch_bounds__(kThreads)
 #pragma unroll
                 for (int i = 0; i < 8; ++i) e[i] = first + i < end ? __ldg(uv + first + i) : 0u;
             }
-            uint16_t lu[8], lv[8];
+            uint32_t lu[8], lv[8];
 #pragma unroll
             for (int i = 0; i < 8; ++i) {
-                lu[i] = __ldg(comp16 + (e[i] >> 16));
-                lv[i] = __ldg(comp16 + (e[i] & 0xFFFFu));
+                if constexpr (kIds) {
+                    uint32_t a, b;
+                    col_rows(e[i], n, a, b);
+                    lu[i] = __ldg(comp + a);
+                    lv[i] = __ldg(comp + b);
+                } else {
+                    lu[i] = __ldg(comp16 + (e[i] >> 16));
+                    lv[i] = __ldg(comp16 + (e[i] & 0xFFFFu));
+                }
             }
 #pragma unroll
             for (int i = 0; i < 8; ++i) {
@@ -217,12 +227,13 @@ __global__ void __launch_bounds__(kFThreads)
 // Each live tree's minimum candidate column (its pivot candidate for this round).
 __global__ void __launch_bounds__(kThreads)
     k4_min_edge(const uint32_t* __restrict__ cand, uint32_t ncand, const uint32_t* __restrict__ uv,
-                const uint32_t* __restrict__ comp, uint32_t* best) {
+                const uint32_t* __restrict__ comp, uint32_t* best, uint32_t n) {
     for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < ncand;
          i += gridDim.x * blockDim.x) {
         const uint32_t j = cand[i];
-        const uint32_t e = uv[j];
-        const uint32_t cu = comp[e >> 16], cv = comp[e & 0xFFFFu];
+        uint32_t a, b;
+        col_rows(uv[j], n, a, b);
+        const uint32_t cu = comp[a], cv = comp[b];
         if (cu == cv) continue;
         if (j < ld_cg_u32(best + cu)) atomicMin(best + cu, j);
         if (j < ld_cg_u32(best + cv)) atomicMin(best + cv, j);
@@ -237,8 +248,9 @@ __global__ void k4_hook(uint32_t n, const uint32_t* __restrict__ uv,
         if (comp[x] != x) continue;  // not a tree label
         const uint32_t j = best[x];
         if (j == kNone) continue;
-        const uint32_t e = uv[j];
-        const uint32_t cu = comp[e >> 16], cv = comp[e & 0xFFFFu];
+        uint32_t a, b;
+        col_rows(uv[j], n, a, b);
+        const uint32_t cu = comp[a], cv = comp[b];
         const uint32_t other = (cu == x) ? cv : cu;
         const bool mutual = best[other] == j;
         if (mutual && x < other) continue;  // the larger label of a mutual pair hooks
@@ -326,7 +338,7 @@ int run_reduction(ReduceState& st, cudaStream_t s, int num_sms, uint32_t& epoch,
         return !(e && e[0] == '0');
     }();
     const size_t fsmem = ((size_t)n * 2 + 15) & ~(size_t)15;
-    bool smem_filter = smem_env && fsmem <= 200 * 1024;
+    bool smem_filter = smem_env && fsmem <= 200 * 1024 && !col_ids(n);
     if (smem_filter && cudaFuncSetAttribute(k4_filter_range_s,
                                             cudaFuncAttributeMaxDynamicSharedMemorySize,
                                             (int)fsmem) != cudaSuccess) {
@@ -346,9 +358,12 @@ int run_reduction(ReduceState& st, cudaStream_t s, int num_sms, uint32_t& epoch,
             if (blocks > (uint64_t)num_sms) blocks = num_sms;
             k4_filter_range_s<<<(unsigned)(blocks ? blocks : 1), kFThreads, fsmem, s>>>(
                 st.uv, pos, end, comp16, n, st.cand[0], st.cap, st.counters);
+        } else if (col_ids(n)) {
+            k4_filter_range<true><<<grid_for((end - pos + 7) / 8, num_sms), kThreads, 0, s>>>(
+                st.uv, pos, end, comp16, st.comp, n, st.cand[0], st.cap, st.counters);
         } else {
-            k4_filter_range<<<grid_for((end - pos + 7) / 8, num_sms), kThreads, 0, s>>>(
-                st.uv, pos, end, comp16, st.cand[0], st.cap, st.counters);
+            k4_filter_range<false><<<grid_for((end - pos + 7) / 8, num_sms), kThreads, 0, s>>>(
+                st.uv, pos, end, comp16, st.comp, n, st.cand[0], st.cap, st.counters);
         }
         S.launches += 1;
         pull();
@@ -364,7 +379,7 @@ int run_reduction(ReduceState& st, cudaStream_t s, int num_sms, uint32_t& epoch,
         while (ncand > 0) {
             S.iterations += 1;
             k4_min_edge<<<grid_for(ncand, num_sms), kThreads, 0, s>>>(st.cand[cur], ncand, st.uv,
-                                                                       st.comp, st.best);
+                                                                       st.comp, st.best, n);
             cudaMemsetAsync(st.counters + kCntHooks, 0, sizeof(uint32_t), s);
             k4_hook<<<gn, kThreads, 0, s>>>(n, st.uv, st.comp, st.best, par, st.surv,
                                             st.counters);
@@ -373,7 +388,7 @@ int run_reduction(ReduceState& st, cudaStream_t s, int num_sms, uint32_t& epoch,
             cudaMemsetAsync(st.counters + kCntCand, 0, sizeof(uint32_t), s);
             k4_filter<<<grid_for(ncand, num_sms), kThreads, 0, s>>>(
                 st.uv, 0, 0, st.cand[cur], ncand, st.comp, st.cand[cur ^ 1], st.cap,
-                st.counters);
+                st.counters, n);
             S.launches += 5;
             pull();
             cur ^= 1;

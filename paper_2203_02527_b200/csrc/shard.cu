@@ -185,12 +185,13 @@ __global__ void __launch_bounds__(1024)
 }
 
 // One block: padded segment starts (segments begin on `align`-element boundaries), the
-// sentinel column {0, 0} in the padding slots, and each segment's key bounds: segment b
+// sentinel column {0, 0} (pad_val, colcodec.h) in the padding slots, and each segment's key bounds: segment b
 // holds keys in [splitter[b-1], splitter[b]) within the local range [kmin, kmax].
 __global__ void k7_layout(const uint64_t* __restrict__ totals, const uint64_t* __restrict__ splitters,
                           uint32_t parts, uint32_t align, uint64_t kmin, uint64_t kmax,
                           uint64_t* __restrict__ starts, uint64_t* __restrict__ bminmax,
-                          uint64_t* __restrict__ keys_out, uint32_t* __restrict__ vals_out) {
+                          uint64_t* __restrict__ keys_out, uint32_t* __restrict__ vals_out,
+                          uint32_t pad_val) {
     __shared__ uint64_t s_start[kMaxParts + 1];
     if (threadIdx.x == 0) {
         uint64_t acc = 0;
@@ -209,7 +210,7 @@ __global__ void k7_layout(const uint64_t* __restrict__ totals, const uint64_t* _
         bminmax[parts + b] = hi;
         for (uint64_t q = s_start[b] + totals[b]; q < s_start[b + 1]; ++q) {
             keys_out[q] = 0;
-            vals_out[q] = 0;
+            vals_out[q] = pad_val;
         }
     }
 }
@@ -363,12 +364,12 @@ __global__ void __launch_bounds__(kThreads)
 // segment of (keys, vals) — a buffer other than the one k7_layout padded.
 __global__ void k7_pad_fill(const uint64_t* __restrict__ totals, const uint64_t* __restrict__ starts,
                             uint32_t parts, uint32_t align, uint64_t* __restrict__ keys,
-                            uint32_t* __restrict__ vals) {
+                            uint32_t* __restrict__ vals, uint32_t pad_val) {
     for (uint32_t b = threadIdx.x; b < parts; b += blockDim.x) {
         const uint64_t e = starts[b] + (totals[b] + align - 1) / align * align;
         for (uint64_t q = starts[b] + totals[b]; q < e; ++q) {
             keys[q] = 0;
-            vals[q] = 0;
+            vals[q] = pad_val;
         }
     }
 }
@@ -412,7 +413,7 @@ int launch_partition_count(const uint64_t* keys, uint64_t count, const uint64_t*
                            uint32_t parts, uint32_t* d_counts_scratch, uint64_t* d_totals,
                            uint64_t* d_bminmax, uint64_t* keys_out, uint32_t* vals_out,
                            cudaStream_t s, uint32_t align, uint64_t kmin, uint64_t kmax,
-                           const uint64_t* h_splitters, uint16_t* d_table) {
+                           const uint64_t* h_splitters, uint16_t* d_table, uint32_t pad_val) {
     static_assert(kThreads == kMaxParts, "one thread per bucket in k7_scatter");
     if (parts < 1 || parts > (uint32_t)kMaxParts) return -1;
     const uint64_t tiles = (count + kTile - 1) / kTile;
@@ -431,7 +432,7 @@ int launch_partition_count(const uint64_t* keys, uint64_t count, const uint64_t*
     }
     // d_totals has room for 2 * parts words: [totals | segment starts]
     k7_layout<<<1, 256, 0, s>>>(d_totals, d_splitters, parts, align, kmin, kmax,
-                                d_totals + parts, d_bminmax, keys_out, vals_out);
+                                d_totals + parts, d_bminmax, keys_out, vals_out, pad_val);
     return l;
 }
 
@@ -469,8 +470,9 @@ int launch_partition_scatter(const uint64_t* keys, const uint32_t* vals, uint64_
 }
 
 int launch_partition_pad(const uint64_t* d_totals, uint32_t parts, uint32_t align,
-                         uint64_t* keys, uint32_t* vals, cudaStream_t s) {
-    k7_pad_fill<<<1, 256, 0, s>>>(d_totals, d_totals + parts, parts, align, keys, vals);
+                         uint64_t* keys, uint32_t* vals, cudaStream_t s, uint32_t pad_val) {
+    k7_pad_fill<<<1, 256, 0, s>>>(d_totals, d_totals + parts, parts, align, keys, vals,
+                                  pad_val);
     return 1;
 }
 

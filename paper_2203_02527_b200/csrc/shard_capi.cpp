@@ -122,7 +122,6 @@ int read_partition(ShardScratch& sc, uint32_t parts, cudaStream_t st, uint64_t* 
     return PH0B_OK;
 }
 
-inline uint64_t row_base(uint64_t u, uint64_t n) { return u * (2 * n - u - 1) / 2; }
 
 }  // namespace
 
@@ -156,7 +155,7 @@ int ph0b_shard_distances(ph0b_context* ctx, const double* dX, uint64_t n, uint64
     if (n > PH0B_MAX_POINTS) return ph0b::capi_fail(PH0B_ERR_TOO_LARGE, "point cloud too large");
     if (u_hi > n) u_hi = n;
     if (u_lo > u_hi) u_lo = u_hi;
-    const uint64_t local = row_base(u_hi, n) - row_base(u_lo, n);
+    const uint64_t local = ph0b::row_base(u_hi, n) - ph0b::row_base(u_lo, n);
     Status s = c->reserve_points(n, d);
     if (s.good()) s = c->reserve_edges(local);
     if (!s.good()) return ph0b::capi_fail(s);

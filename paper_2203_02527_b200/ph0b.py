@@ -41,6 +41,7 @@ EXPORTED_SYMBOLS = [
     "ph0b_shard_partition_count", "ph0b_shard_recv_peer",
     "ph0b_shard_scatter_peers", "ph0b_ipc_get_handle", "ph0b_ipc_open_handle", "ph0b_ipc_close",
     "ph0b_scale_release", "ph0b_host_cache_trim", "ph0b_reduced_supports",
+    "ph0b_release_resources",
 ]
 
 
@@ -100,6 +101,7 @@ def lib() -> C.CDLL:
         "ph0b_result_free": (None, [C.POINTER(Result)]),
         "ph0b_scale_release": (None, [vp]),
         "ph0b_host_cache_trim": (None, []),
+        "ph0b_release_resources": (None, []),
         "ph0b_kruskal_barcode": (C.c_int, [vp, u64, u64, u32, C.POINTER(Options),
                                            C.POINTER(Result)]),
         "ph0b_generate_uniform_cloud_device": (C.c_int, [vp, u64, u64, u64, vp, vp]),

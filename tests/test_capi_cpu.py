@@ -46,7 +46,7 @@ def test_workers_zero_rejected():  # reduction.cpp:134
 
 
 def test_too_large_rejected():
-    X = np.zeros((65537, 1))
+    X = np.zeros((92683, 1))  # K >= 2^32: beyond the 32-bit edge-column codec
     with pytest.raises(pkg.Ph0bError, match="too large"):
         pkg.h0_barcode(X)
 

@@ -70,3 +70,9 @@ def test_multi_vs_reference_full_size(cfg, ranks):
     assert bc.essential_count == int(g["essential"])
     assert np.array_equal(bc.death_grade, g["death_grade"])
     assert np.array_equal(bits(bc.death_length), bits(g["death_length"]))
+
+
+@pytest.fixture(scope="module", autouse=True)
+def _release_runners():
+    yield
+    pkg.lib().ph0b_release_resources()  # the 8 virtual ranks' buffers (C5: ~50 GB)
