@@ -11,9 +11,12 @@ matrix -> column reduction -> barcode collect) over the workload's K = N(N-1)/2 
 * e2e:   the same metric through the public C ABI (ph0b_run_host) with host buffers: the
   H2D copy of X from pinned memory and the D2H copy of the bars and of D (|D| doubles)
   into pinned memory are inside the timed region.
+* e2e_dropin: the drop-in entry point ph0b_h0_barcode itself (library-allocated result).
 * --impl reference: the reference's own CPU implementation (oracle/_ref, the unmodified
   /root/reference sources built here; else the C port in oracle/) on a bounded sample
-  of the same workload, rank 0 only.
+  of the same workload, rank 0 only; X from the oracle's generator (no product code).
+* --gpus N without torchrun: the in-process multi-GPU path of the C ABI (ph0b_options.n_gpus);
+  under torchrun (one process per GPU): the sharded pipeline of sharded.py.
 Prints ONE JSON line on rank 0.
 """
 from __future__ import annotations
@@ -350,6 +353,80 @@ def run_sharded(args, cfg_name):
     dist.destroy_process_group()
 
 
+def run_inproc_multi(args, cfg_name):
+    """--gpus N without torchrun: the in-process multi-GPU path behind the C ABI
+    (ph0b_options.n_gpus, csrc/multi.cpp) — one process, one host thread and context per GPU,
+    the partition kernel storing every part into its destination GPU's receive buffer.
+    value: X from the host, bars back, D left on the GPUs (PH0B_FLAG_NO_SCALE); e2e: the
+    same call with D streamed into a host buffer.  Host wall clock of the blocking call.
+    --virtual: all ranks on GPU 0 (a correctness/overhead run on a one-GPU box, not a
+    scaling number)."""
+    import ctypes as C
+
+    import numpy as np
+    import torch
+
+    import paper_2203_02527_b200 as pkg
+
+    P = args.gpus
+    have = torch.cuda.device_count()
+    if have < P and not args.virtual:
+        raise SystemExit(f"--gpus {P} needs {P} visible GPUs (found {have}); --virtual runs "
+                         f"the ranks on GPU 0")
+    devices = [0] * P if args.virtual else list(range(P))
+    X = pkg.config_cloud(cfg_name)
+    n, d = X.shape
+    k = n * (n - 1) // 2
+    L = pkg.lib()
+    Xc = np.asfortranarray(X)
+    dg = pkg.PinnedArray(n, np.uint64)
+    dl = pkg.PinnedArray(n, np.float64)
+    sc = pkg.PinnedArray(k, np.float64)
+    nf, ess, ns = C.c_uint64(), C.c_uint64(), C.c_uint64()
+    t = pkg.ph0b.StageTimes()
+
+    def call(with_scale):
+        opt = pkg.ph0b._opts(0, 0 if with_scale else pkg.ph0b.FLAG_NO_SCALE, 1, True, devices)
+        rc = L.ph0b_h0_barcode_into(C.c_void_p(Xc.ctypes.data), n, d, pkg.ph0b.COL_MAJOR,
+                                    C.byref(opt), C.c_void_p(dg.array.ctypes.data),
+                                    C.c_void_p(dl.array.ctypes.data), C.byref(nf), C.byref(ess),
+                                    C.c_void_p(sc.array.ctypes.data) if with_scale else None,
+                                    k if with_scale else 0, C.byref(ns), C.byref(t))
+        if rc:
+            raise RuntimeError(L.ph0b_last_error().decode())
+
+    def timed(with_scale, steps):
+        for _ in range(args.warmup):
+            call(with_scale)
+        t0 = time.perf_counter()
+        for _ in range(steps):
+            call(with_scale)
+        return (time.perf_counter() - t0) * 1e3 / steps
+
+    with ClockSampler(0) as clk:
+        ms = timed(False, args.steps)
+    e2e_steps = args.e2e_steps or max(1, min(args.steps, 5))
+    e2e_ms = timed(True, e2e_steps)
+    line = {
+        "metric": METRIC, "value": k / (ms / 1e3), "unit": UNIT, "n_gpus": P,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True,
+        "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": {"workload": f"{cfg_name}: {WORKLOADS[cfg_name]}", "n": n, "d": d, "edges": k,
+                   "parallelism": f"in-process x{P} ({'virtual ranks on GPU 0' if args.virtual else 'GPUs ' + str(devices)})",
+                   "api": "ph0b_h0_barcode_into with ph0b_options.n_gpus/devices",
+                   "n_scale": int(ns.value), "bars": int(nf.value)},
+        "e2e": {"value": k / (e2e_ms / 1e3), "unit": UNIT, "ms_per_step": e2e_ms,
+                "steps": e2e_steps, "h2d_bytes_per_step": n * d * 8 * P,
+                "d2h_bytes_per_step": int(t.d2h_bytes)},
+        "roofline": None, "cpu_baseline": None, "clocks": clk.summary(),
+        "gpu_launches": int(L.ph0b_last_launch_count()) or None,
+    }
+    print(json.dumps(line), flush=True)
+    for a in (dg, dl, sc):
+        a.free()
+    L.ph0b_release_resources()
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -363,6 +440,9 @@ def main():
                     help="skip the timing of the drop-in entry point ph0b_h0_barcode")
     ap.add_argument("--sharded", action="store_true",
                     help="use the sharded multi-GPU pipeline even at N=1 (torchrun)")
+    ap.add_argument("--virtual", action="store_true",
+                    help="--gpus N without torchrun on a box with fewer GPUs: the in-process "
+                         "ranks share GPU 0")
     ap.add_argument("--replicas", action="store_true",
                     help="N>1: run N independent single-GPU replicas instead of the sharded path")
     args = ap.parse_args()
@@ -379,6 +459,9 @@ def main():
     import paper_2203_02527_b200 as pkg
 
     ws, rank, local = dist_env()
+    if ws == 1 and args.gpus > 1 and not args.sharded:
+        run_inproc_multi(args, cfg_name)
+        return
     if (ws > 1 and not args.replicas) or args.sharded:
         run_sharded(args, cfg_name)
         return

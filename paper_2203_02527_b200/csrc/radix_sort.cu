@@ -6,20 +6,23 @@
 // 8 bits per pass.  Every pass is stable and the input is the reference's u-major order,
 // so equal lengths end up ordered by (u, v) exactly as filtration.cpp:21-25 orders them.
 //
-// One kernel per digit (Adinets & Merrill's single-pass "onesweep"), persistent: each CTA
-// claims 4096-key tiles in increasing order with an atomic ticket (the next one while the
-// current one is still being written, its keys and columns prefetched into shared memory
-// with TMA bulk copies), ranks the tile's keys in-warp with shared-memory atomics on
-// per-warp digit counters (B200 resolves the same-address lanes of one ATOMS in lane
-// order — checked on the device at context creation; bit-sliced ballots otherwise),
-// publishes its per-digit counts, obtains the exclusive prefix over earlier tiles by
-// decoupled look-back on epoch-tagged status words, scatters the tile into shared memory in
-// digit order and writes it out so that each digit's run is a contiguous global run.  The
+// One kernel per digit (Adinets & Merrill's single-pass "onesweep"), persistent, launched as
+// thread-block clusters of two CTAs.  A cluster claims two consecutive 4096-key tiles at a
+// time with an atomic ticket (the next pair while the current one is still being written;
+// keys and columns are prefetched into shared memory with TMA bulk copies).  Each CTA ranks
+// its tile's keys in-warp with shared-memory atomics on per-warp digit counters (B200
+// resolves the same-address lanes of one ATOMS in lane order — checked on the device at
+// context creation; bit-sliced ballots otherwise) and pushes its per-digit counts into its
+// partner's shared memory (DSMEM stores tracked by an mbarrier).  One look-back status per
+// tile pair is published; the exclusive prefix over earlier pairs comes from a decoupled
+// look-back on epoch-tagged status words.  Each CTA then scatters its tile into shared memory
+// in digit order and writes it out so that each digit's run is a contiguous global run.  The
 // same pass counts the NEXT digit's histogram, so no separate upsweep over the keys is
-// needed.  Tickets make the look-back deadlock-free whatever else shares the GPU: every
-// tile a CTA waits on was claimed earlier by a CTA that is already running.
+// needed.  Tickets make the look-back deadlock-free whatever else shares the GPU: every pair
+// a CTA waits on was claimed earlier by a cluster that is already running.
 #include <cuda_runtime.h>
 
+#include <algorithm>
 #include <cstdint>
 #include <cstdlib>
 
@@ -102,7 +105,42 @@ __device__ __forceinline__ void mbar_wait_parity(uint64_t* bar, uint32_t parity)
 // restarting at tile - 1 in windows of 8; windows of 3 / 6 measured slower).
 constexpr int kLookbackWin = 4;
 
-template <bool kVals, bool kCountNext, bool kBallot>
+__device__ __forceinline__ uint32_t cluster_rank() {
+    uint32_t r;
+    asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+    return r;
+}
+__device__ __forceinline__ void cluster_arrive() {
+    asm volatile("barrier.cluster.arrive.release.aligned;" ::: "memory");
+}
+__device__ __forceinline__ void cluster_wait() {
+    asm volatile("barrier.cluster.wait.acquire.aligned;" ::: "memory");
+}
+// shared::cluster address of `p` (this CTA's shared memory) in cluster CTA `rank`
+__device__ __forceinline__ uint32_t dsmem_addr(const void* p, uint32_t rank) {
+    uint32_t r;
+    asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(smem_addr(p)), "r"(rank));
+    return r;
+}
+__device__ __forceinline__ void st_dsmem(uint32_t addr, uint32_t v) {
+    asm volatile("st.shared::cluster.u32 [%0], %1;" ::"r"(addr), "r"(v) : "memory");
+}
+// Asynchronous store into a cluster peer's shared memory that completes 4 bytes of the
+// transaction count of the peer's mbarrier (no cluster-wide barrier, no memory fence).
+__device__ __forceinline__ void st_async_dsmem(uint32_t addr, uint32_t v, uint32_t bar) {
+    asm volatile("st.async.shared::cluster.mbarrier::complete_tx::bytes.u32 [%0], %1, [%2];" ::"r"(
+                     addr),
+                 "r"(v), "r"(bar)
+                 : "memory");
+}
+
+// kC == 1: one CTA per tile, one look-back status per tile.
+// kC > 1 (thread-block cluster of kC CTAs): the cluster claims a super-tile of kC consecutive
+// tiles, CTA r sorts tile kC*s + r; every CTA pushes its per-digit counts into its peers'
+// shared memory with mbarrier-tracked asynchronous stores (CTA 0 also pushes the next
+// super-tile's ticket), CTA 0 publishes ONE look-back status per super-tile as soon as the
+// counts are in, so the look-back walks kC times fewer links (each covering kC*4096 keys).
+template <bool kVals, bool kCountNext, bool kBallot, int kC>
 __global__ void __launch_bounds__(kThreads, 2)
     k2_onesweep_p(const uint64_t* __restrict__ keys_in, uint64_t* __restrict__ keys_out,
                   const uint32_t* __restrict__ vals_in, uint32_t* __restrict__ vals_out,
@@ -122,11 +160,16 @@ __global__ void __launch_bounds__(kThreads, 2)
     __shared__ uint32_t s_bin_start[kBins];
     __shared__ uint32_t s_next[kCountNext ? kBins : 1];
     __shared__ uint32_t s_scan[kWarps];
-    __shared__ uint32_t s_tile[2];
+    __shared__ uint32_t s_tile[2];                       // (kC > 1: super-tile, by parity)
+    // kC > 1: counts of every cluster CTA, by iteration parity, and their mbarriers
+    __shared__ uint32_t s_cnt[kC > 1 ? 2 : 1][kC > 1 ? kC : 1][kC > 1 ? kBins : 1];
+    __shared__ __align__(8) uint64_t s_cbar[2];
     __shared__ __align__(8) uint64_t s_bar;
 
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const uint32_t t = tid;  // digit handled by this thread in the per-digit phases
+    const uint32_t cr = kC > 1 ? cluster_rank() : 0u;
+    const uint32_t num_super = (num_tiles + kC - 1) / kC;
     auto issue = [&](uint32_t tl) {
         const uint64_t b0 = (uint64_t)tl * kPTile;
         const uint64_t n = count - b0 < (uint64_t)kPTile ? count - b0 : (uint64_t)kPTile;
@@ -140,34 +183,57 @@ __global__ void __launch_bounds__(kThreads, 2)
     if (tid == 0) {
         asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_addr(&s_bar)));
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-        const uint32_t first = atomicAdd(ticket, 1u);
-        s_tile[0] = first;
-        if (first < num_tiles) issue(first);
+        if constexpr (kC == 1) {
+            const uint32_t first = atomicAdd(ticket, 1u);
+            s_tile[0] = first;
+            if (first < num_tiles) issue(first);
+        } else {
+            for (int q = 0; q < 2; ++q)
+                asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_addr(&s_cbar[q])));
+            asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+            if (cr == 0) {  // the cluster's first super-tile, to every CTA of the cluster
+                const uint32_t first = atomicAdd(ticket, 1u);
+                for (uint32_t q = 0; q < (uint32_t)kC; ++q)
+                    st_dsmem(dsmem_addr(&s_tile[0], q), first);
+            }
+        }
     }
     if (kCountNext) s_next[tid] = 0;
     {
         const uint32_t hcount = hist[(t + hist_rot) & 0xFFu];
         s_bin_start[t] = block_exclusive_scan(hcount, s_scan, nullptr);
     }
+    if constexpr (kC > 1) {
+        cluster_arrive();
+        cluster_wait();
+        if (tid == 0 && kC * s_tile[0] + cr < num_tiles) issue(kC * s_tile[0] + cr);
+    }
     __syncthreads();
-    uint32_t tile = s_tile[0];
-    uint32_t parity = 0;
+    uint32_t sup = s_tile[0];  // (super-)tile being processed
+    uint32_t parity = 0, it = 0, cpar = 0;  // cpar: phase bits of s_cbar[0..1]
     const uint32_t lt = lanemask_lt();
 
-    while (tile < num_tiles) {
+    while (sup < num_super) {
+        const uint32_t tile = kC * sup + cr;
         const uint64_t base = (uint64_t)tile * kPTile;
-        const uint64_t rem = count - base;
+        const uint64_t rem = tile < num_tiles ? count - base : 0;
         const uint32_t tile_n = rem < (uint64_t)kPTile ? (uint32_t)rem : (uint32_t)kPTile;
+        const uint32_t par = it & 1u;
 #pragma unroll
         for (int w = 0; w < kWarps; ++w) s_whist[w][tid] = 0;
         __syncthreads();
-        // the look-back's probe of tile - 1 goes out before this tile is even ranked: its
-        // latency hides behind the rank, scan and scatter phases (C5: 14.51 -> 13.83 ms per
-        // pass vs issuing it after this tile's aggregate is published)
+        // kC > 1: the next super-tile is claimed now; its latency hides behind this tile
+        uint32_t claimed = 0;
+        if (kC > 1 && cr == 0 && tid == 0) claimed = atomicAdd(ticket, 1u);
+        // the look-back's probe of the previous (super-)tile goes out before this tile is
+        // even ranked: its latency hides behind the rank, scan and scatter phases (C5: 14.51
+        // -> 13.83 ms per pass vs issuing it after this tile's aggregate is published)
         const uint64_t probe =
-            tile > 0 ? ld_relaxed_u64(status + (uint64_t)(tile - 1) * kBins + t) : 0ull;
-        mbar_wait_parity(&s_bar, parity);
-        parity ^= 1u;
+            sup > 0 ? ld_relaxed_u64(status + (uint64_t)(sup - 1) * kBins + t) : 0ull;
+        if (tile_n) {
+            mbar_wait_parity(&s_bar, parity);
+            parity ^= 1u;
+        }
 
         // ---- rank within the warp (keys from the staged tile) --------------------------
         uint64_t k[kPItems];
@@ -200,7 +266,7 @@ __global__ void __launch_bounds__(kThreads, 2)
         }
         __syncthreads();
 
-        // ---- per-digit counts; publish this tile's aggregate; tile-local starts ----------
+        // ---- per-digit counts; publish them; tile-local starts ----------------------------
         uint32_t wpre[kWarps];
         uint32_t cnt = 0;
 #pragma unroll
@@ -208,9 +274,54 @@ __global__ void __launch_bounds__(kThreads, 2)
             wpre[w] = cnt;
             cnt += s_whist[w][t];
         }
-        uint64_t* my_status = status + (uint64_t)tile * kBins + t;
-        st_relaxed_u64(my_status,
-                       pack_status(tile == 0 ? kStateInclusive : kStateAggregate, epoch, cnt));
+        uint64_t* my_status = status + (uint64_t)sup * kBins + t;
+        uint32_t before = 0, agg = cnt;  // kC > 1: counts of the earlier CTAs / whole cluster
+        auto gather = [&]() {  // (kC > 1) after the counts of every peer have landed
+            agg = 0;
+#pragma unroll
+            for (int q = 0; q < kC; ++q) {
+                const uint32_t c = s_cnt[par][q][t];
+                before += (uint32_t)q < cr ? c : 0u;
+                agg += c;
+            }
+        };
+        bool got = false;  // kC > 1: the cluster's counts for my digit are in
+        auto publish_agg = [&]() {
+            gather();
+            st_relaxed_u64(my_status,
+                           pack_status(sup == 0 ? kStateInclusive : kStateAggregate, epoch, agg));
+        };
+        if constexpr (kC == 1) {
+            st_relaxed_u64(my_status,
+                           pack_status(sup == 0 ? kStateInclusive : kStateAggregate, epoch, cnt));
+        } else {
+            // my counts into every CTA's slot [cr]; CTA 0 also hands out the next super-tile
+            s_cnt[par][cr][t] = cnt;
+            const uint32_t bytes = (kC - 1) * kBins * 4 + (cr != 0 ? 4u : 0u);
+            if (tid == 0)
+                asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(
+                                 smem_addr(&s_cbar[par])),
+                             "r"(bytes)
+                             : "memory");
+            for (uint32_t q = 0; q < (uint32_t)kC; ++q) {
+                if (q == cr) continue;
+                const uint32_t bar = dsmem_addr(&s_cbar[par], q);
+                st_async_dsmem(dsmem_addr(&s_cnt[par][cr][t], q), cnt, bar);
+                if (cr == 0 && tid == 0) st_async_dsmem(dsmem_addr(&s_tile[par ^ 1u], q), claimed, bar);
+            }
+            if (cr == 0 && tid == 0) s_tile[par ^ 1u] = claimed;
+            // CTA 0 waits for its peers' counts right away and publishes the super-tile's
+            // aggregate before its own scan; the others collect the counts after their
+            // scatter.  (C5, per pass: 12.96 ms; 13.09 ms when a peer that already has all
+            // counts publishes the aggregate too, 13.71 ms when every CTA publishes after its
+            // scatter — late and duplicate status stores lengthen successors' look-backs.)
+            // Each thread reads only its own digit's column.
+            if (cr == 0) {
+                mbar_wait_parity(&s_cbar[par], (cpar >> par) & 1u);
+                got = true;
+                publish_agg();
+            }
+        }
         const uint32_t tstart = block_exclusive_scan(cnt, s_scan, nullptr);
         // one lookup per key in the scatter: tile start of the digit + the warp's offset in it
 #pragma unroll
@@ -229,30 +340,41 @@ __global__ void __launch_bounds__(kThreads, 2)
                 if (kVals) so_v[dst] = st_v[pos];
             }
         }
-        __syncthreads();  // the stage buffer is free: claim and prefetch the next tile now
-        if (tid == 0) {
-            const uint32_t nx = atomicAdd(ticket, 1u);
-            s_tile[1] = nx;
-            if (nx < num_tiles) issue(nx);
+        __syncthreads();  // the stage buffer is free: prefetch the next tile now
+        uint32_t next_sup;
+        if constexpr (kC == 1) {
+            if (tid == 0) {
+                const uint32_t nx = atomicAdd(ticket, 1u);
+                s_tile[1] = nx;
+                if (nx < num_tiles) issue(nx);
+            }
+        } else {
+            if (!got) {  // (CTA r > 0 only) the counts of the earlier CTAs
+                mbar_wait_parity(&s_cbar[par], (cpar >> par) & 1u);
+                gather();
+            }
+            cpar ^= 1u << par;
+            next_sup = s_tile[par ^ 1u];
+            if (tid == 0 && kC * next_sup + cr < num_tiles) issue(kC * next_sup + cr);
         }
 
-        // ---- decoupled look-back, per digit ----------------------------------------------
+        // ---- decoupled look-back over earlier (super-)tiles, per digit --------------------
         uint32_t excl = 0;
-        if (tile > 0) {
+        if (sup > 0) {
             const uint32_t st0 = status_state(probe, epoch);
             if (st0 == kStateInclusive) {
                 excl = (uint32_t)probe;  // the early probe already has it
             } else if (st0 == 0) {
-                excl = lookback_window<kLookbackWin>(status + t, kBins, tile, epoch);
+                excl = lookback_window<kLookbackWin>(status + t, kBins, sup, epoch);
             } else {
                 excl = (uint32_t)probe +
-                       lookback_window<kLookbackWin>(status + t, kBins, tile - 1, epoch);
+                       lookback_window<kLookbackWin>(status + t, kBins, sup - 1, epoch);
             }
-            st_relaxed_u64(my_status, pack_status(kStateInclusive, epoch, excl + cnt));
+            if (cr == 0) st_relaxed_u64(my_status, pack_status(kStateInclusive, epoch, excl + agg));
         }
-        s_global[t] = s_bin_start[t] + excl - tstart;
+        s_global[t] = s_bin_start[t] + excl + before - tstart;
         __syncthreads();
-        const uint32_t next_tile = s_tile[1];
+        if constexpr (kC == 1) next_sup = s_tile[1];
 
         // ---- write out: consecutive threads -> consecutive positions of each digit run ---
 #pragma unroll 4
@@ -268,12 +390,17 @@ __global__ void __launch_bounds__(kThreads, 2)
                 if (kCountNext) atomicAdd(&s_next[(uint32_t)(rel >> next_shift) & 0xFFu], 1u);
             }
         }
-        tile = next_tile;
+        sup = next_sup;
+        ++it;
     }
     if (kCountNext) {
         __syncthreads();
         const uint32_t c = s_next[tid];
         if (c) atomicAdd(&next_hist[tid], c);
+    }
+    if constexpr (kC > 1) {  // no CTA leaves while a peer may still read its counts
+        cluster_arrive();
+        cluster_wait();
     }
 }
 
@@ -328,31 +455,65 @@ int rank_variant() {
     return g_rank_variant;
 }
 
-template <bool kVals, bool kCountNext, bool kBallot>
-int launch_pass_t(const SortArgs& a, int cur, uint32_t p, const SortPlan& plan, uint32_t rot,
+// CTAs per look-back super-tile.  C5, per pass: 13.70 ms with one CTA per look-back status,
+// 12.96-13.02 ms with clusters of 2, 21.3 ms with clusters of 4 (every super-tile waits for
+// the slowest of four CTAs before its aggregate is out); look-back windows of 2 / 3 / 6
+// super-tiles per round trip with clusters of 2: 13.42 / 13.06-13.09 / 13.07-13.08 ms.
+constexpr int kSortCluster = 2;
+
+template <bool kVals, bool kCountNext, bool kBallot, int kC>
+int launch_pass_c(const SortArgs& a, int cur, uint32_t p, const SortPlan& plan, uint32_t rot,
                   uint32_t* next_hist, cudaStream_t s, int num_sms) {
-    auto kern = k2_onesweep_p<kVals, kCountNext, kBallot>;
+    auto kern = k2_onesweep_p<kVals, kCountNext, kBallot, kC>;
     const size_t smem = (size_t)kPTile * 8 * 2 + (size_t)kPTile * 4 * 2;
     const int per_sm = kernel_blocks_per_sm((const void*)kern, kThreads, smem);
     if (per_sm < 1) return -1;
     const uint64_t tiles = (a.count + kPTile - 1) / kPTile;
-    uint64_t grid = (uint64_t)num_sms * per_sm;
-    if (grid > tiles) grid = tiles;
     const uint32_t next_shift = kCountNext ? plan.shift[p + 1] : 0u;
-    kern<<<(unsigned)grid, kThreads, smem, s>>>(
-        a.keys[cur], a.keys[cur ^ 1], kVals ? a.vals[cur] : nullptr,
-        kVals ? a.vals[cur ^ 1] : nullptr, a.count, a.kmin, plan.shift[p], next_shift,
-        a.hist + kBins * p, rot, a.status, a.epoch_base + p, next_hist, (uint32_t)tiles,
-        a.tile_counter + p);
-    return 1;
+    cudaLaunchConfig_t cfg{};
+    cudaLaunchAttribute attr[1];
+    cfg.blockDim = dim3(kThreads);
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = s;
+    uint64_t grid = (uint64_t)num_sms * per_sm;
+    if (kC > 1) {
+        attr[0].id = cudaLaunchAttributeClusterDimension;
+        attr[0].val.clusterDim.x = kC;
+        attr[0].val.clusterDim.y = 1;
+        attr[0].val.clusterDim.z = 1;
+        cfg.attrs = attr;
+        cfg.numAttrs = 1;
+        cfg.gridDim = dim3(kC);
+        int clusters = 0;
+        if (cudaOccupancyMaxActiveClusters(&clusters, (void*)kern, &cfg) != cudaSuccess ||
+            clusters < 1) {
+            cudaGetLastError();
+            return -1;
+        }
+        // tickets keep a cluster that starts late from blocking anyone: size the grid by
+        // the SM count, not by the (conservative) cluster occupancy estimate
+        const uint64_t supers = (tiles + kC - 1) / kC;
+        grid = std::min<uint64_t>(grid / kC, supers) * kC;
+    } else if (grid > tiles) {
+        grid = tiles;
+    }
+    cfg.gridDim = dim3((unsigned)grid);
+    const cudaError_t e = cudaLaunchKernelEx(
+        &cfg, kern, (const uint64_t*)a.keys[cur], a.keys[cur ^ 1],
+        (const uint32_t*)(kVals ? a.vals[cur] : nullptr), kVals ? a.vals[cur ^ 1] : nullptr,
+        a.count, a.kmin, plan.shift[p], next_shift, (const uint32_t*)(a.hist + kBins * p), rot,
+        a.status, a.epoch_base + p, next_hist, (uint32_t)tiles, a.tile_counter + p);
+    return e == cudaSuccess ? 1 : -1;
 }
 
 template <bool kVals, bool kCountNext>
 int launch_pass(const SortArgs& a, int cur, uint32_t p, const SortPlan& plan, uint32_t rot,
                 uint32_t* next_hist, cudaStream_t s, int num_sms) {
     return rank_variant() == 3
-               ? launch_pass_t<kVals, kCountNext, false>(a, cur, p, plan, rot, next_hist, s, num_sms)
-               : launch_pass_t<kVals, kCountNext, true>(a, cur, p, plan, rot, next_hist, s, num_sms);
+               ? launch_pass_c<kVals, kCountNext, false, kSortCluster>(a, cur, p, plan, rot,
+                                                                       next_hist, s, num_sms)
+               : launch_pass_c<kVals, kCountNext, true, kSortCluster>(a, cur, p, plan, rot,
+                                                                      next_hist, s, num_sms);
 }
 
 // Self-test of the ordering property rank variant 3 relies on.  Returns true when every

@@ -14,7 +14,8 @@ pytestmark = pytest.mark.gpu
 
 @pytest.mark.parametrize("env", [{"PH0B_MAX_PASSES": "1"}, {"PH0B_MAX_PASSES": "2"},
                                  {"PH0B_MAX_PASSES": "3"}, {"PH0B_RANK": "2"},
-                                 {"PH0B_RANK": "3", "PH0B_MAX_PASSES": "8"}])
+                                 {"PH0B_RANK": "3", "PH0B_MAX_PASSES": "8"},
+                                 {"PH0B_RANK": "2", "PH0B_MAX_PASSES": "2"}])
 def test_variant_parity(env):
     e = dict(os.environ, **env)
     res = subprocess.run([sys.executable, str(HERE / "gpu_variant_check.py")], env=e,
