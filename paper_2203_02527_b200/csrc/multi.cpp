@@ -162,6 +162,7 @@ public:
     int run(const double* X, uint64_t n, uint64_t d, uint32_t layout, uint64_t* death_grade,
             double* death_length, uint64_t* n_finite, uint64_t* essential, double* scale,
             uint64_t scale_capacity, uint64_t* n_scale, ph0b_stage_times* times) {
+        NvtxRange nvtx_("ph0b multi-GPU pipeline");
         const auto t0 = std::chrono::steady_clock::now();
         const uint32_t P = (uint32_t)ranks_.size();
         int rc = init();

@@ -3,6 +3,7 @@
 #include "pipeline.h"
 
 #include <cuda.h>
+#include <nvtx3/nvToolsExt.h>
 
 #include <algorithm>
 #include <chrono>
@@ -170,6 +171,9 @@ uint32_t max_sort_passes() {
 }
 
 }  // namespace
+
+NvtxRange::NvtxRange(const char* name) { nvtxRangePushA(name); }
+NvtxRange::~NvtxRange() { nvtxRangePop(); }
 
 Context::Context(int device) : device_(device) {}
 
@@ -429,6 +433,7 @@ Status Context::run_host_input(const double* X, uint64_t n, uint64_t d, uint32_t
 Status Context::stage_distances(const double* dX, uint64_t n, uint64_t d, uint32_t layout,
                                 uint64_t u_lo, uint64_t u_hi, cudaStream_t st, uint64_t* count,
                                 uint64_t* kmin, uint64_t* kmax) {
+    NvtxRange nvtx_("K1 distances");
     const uint64_t ldx = std::max<uint64_t>(128, (n + 127) / 128 * 128);
     PH0B_TRY(cudaMemsetAsync(small_, 0xFF, 8, st), "memset");        // min = ~0
     PH0B_TRY(cudaMemsetAsync(small_ + 1, 0, 3 * 8, st), "memset");   // max, n_scale, flag
@@ -469,6 +474,7 @@ Status Context::sort_unique_range(uint64_t* kb0, uint32_t* vb0, uint64_t* kb1, u
                                   double* scale_out, const uint64_t* d_base, uint64_t* d_count,
                                   uint32_t* grade_out, cudaStream_t st, int* res,
                                   uint32_t* passes, const std::function<Status()>* after_enqueue) {
+    NvtxRange nvtx_("K2 sort + K3 unique");
     uint64_t* kb[2] = {kb0, kb1};
     uint32_t* vb[2] = {vb0, vb1};
     int src = 0;
@@ -561,6 +567,7 @@ Status Context::stage_sort_unique(uint64_t k, uint64_t kmin, uint64_t kmax, bool
 
 Status Context::stage_reduce(const uint32_t* uv, uint64_t count, uint32_t n, cudaStream_t st,
                              ReduceStats* rst, const uint32_t* init_comp, uint32_t target) {
+    NvtxRange nvtx_("K4 column reduction");
     ReduceState rs{};
     rs.n = n;
     rs.k = count;
@@ -582,6 +589,7 @@ Status Context::stage_reduce(const uint32_t* uv, uint64_t count, uint32_t n, cud
 }
 
 Status Context::stage_collect(uint32_t m, uint64_t count, uint64_t grade_offset, cudaStream_t st) {
+    NvtxRange nvtx_("K5 collect");
     if (m == 0) return Status::ok();
     Status s = sort_survivors(m, count, st);
     if (!s.good()) return s;
@@ -593,6 +601,7 @@ Status Context::stage_collect(uint32_t m, uint64_t count, uint64_t grade_offset,
 
 Status Context::run(const double* dX, uint64_t n, uint64_t d, uint32_t layout,
                     cudaStream_t stream, StopAfter stop, bool want_grade, RunOutputs* out) {
+    NvtxRange nvtx_("ph0b pipeline (device)");
     Status s = reserve(n, d);
     if (!s.good()) return s;
     cudaStream_t st = stream ? stream : stream_;
@@ -813,6 +822,7 @@ Status Context::enqueue_stream(uint64_t cbase, uint64_t nch, const std::vector<u
 
 Status Context::stream_scale(const double* d_scale, uint64_t n, double* host_scale,
                              uint64_t capacity, cudaStream_t st, uint64_t* moved) {
+    NvtxRange nvtx_("D to host (packed ring)");
     *moved = 0;
     if (n == 0) return Status::ok();
     if (n > capacity)
@@ -876,6 +886,7 @@ Status Context::stream_scale(const double* d_scale, uint64_t n, double* host_sca
 Status Context::run_host_overlapped(const double* X, uint64_t n, uint64_t d, uint32_t layout,
                                     cudaStream_t st, double* host_scale, uint64_t scale_capacity,
                                     RunOutputs* out) {
+    NvtxRange nvtx_("ph0b pipeline (host, bucketed D stream)");
     Status s = reserve(n, d);
     if (!s.good()) return s;
     const uint64_t k = n * (n - (n > 0)) / 2;
@@ -1240,6 +1251,7 @@ Status Context::run_host_overlapped(const double* X, uint64_t n, uint64_t d, uin
 }
 
 Status Context::stage_kruskal(uint64_t count, uint32_t n, cudaStream_t st, uint32_t* merges) {
+    NvtxRange nvtx_("K6 GPU Kruskal");
     if (n > 65536) return {PH0B_ERR_TOO_LARGE, "union-find forest is limited to 65536 points"};
     uint32_t* d_count = reinterpret_cast<uint32_t*>(d_mapped_ + 250);
     volatile uint32_t* h_count = reinterpret_cast<volatile uint32_t*>(h_mapped_ + 250);
@@ -1256,6 +1268,7 @@ Status Context::stage_kruskal(uint64_t count, uint32_t n, cudaStream_t st, uint3
 
 Status Context::reduced_supports(const RunOutputs& r, uint32_t n, bool want_x,
                                  cudaStream_t stream) {
+    NvtxRange nvtx_("reduced supports");
     cudaStream_t st = stream ? stream : stream_;
     uint32_t* d_err = reinterpret_cast<uint32_t*>(d_mapped_ + 251);
     volatile uint32_t* h_err = reinterpret_cast<volatile uint32_t*>(h_mapped_ + 251);

@@ -17,6 +17,15 @@
 
 namespace ph0b {
 
+// NVTX range over a host-side stage (visible in Nsight Systems / ncu --nvtx; no-op unless a
+// tool is attached).
+struct NvtxRange {
+    explicit NvtxRange(const char* name);
+    ~NvtxRange();
+    NvtxRange(const NvtxRange&) = delete;
+    NvtxRange& operator=(const NvtxRange&) = delete;
+};
+
 struct Status {
     int code = PH0B_OK;
     std::string msg;
