@@ -332,13 +332,10 @@ int run_reduction(ReduceState& st, cudaStream_t s, int num_sms, uint32_t& epoch,
         cudaStreamSynchronize(s);
     };
 
-    // labels in shared memory for the window filter (PH0B_SMEM_FILTER=0: through L1)
-    static const bool smem_env = [] {
-        const char* e = getenv("PH0B_SMEM_FILTER");
-        return !(e && e[0] == '0');
-    }();
+    // labels in shared memory for the window filter (N <= 65536; C5 reduce 2.65 -> 2.53 ms
+    // vs gathering them through L1)
     const size_t fsmem = ((size_t)n * 2 + 15) & ~(size_t)15;
-    bool smem_filter = smem_env && fsmem <= 200 * 1024 && !col_ids(n);
+    bool smem_filter = fsmem <= 200 * 1024 && !col_ids(n);
     if (smem_filter && cudaFuncSetAttribute(k4_filter_range_s,
                                             cudaFuncAttributeMaxDynamicSharedMemorySize,
                                             (int)fsmem) != cudaSuccess) {

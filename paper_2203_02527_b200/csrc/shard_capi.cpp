@@ -8,6 +8,7 @@
 
 #include <algorithm>
 #include <cstring>
+#include <map>
 #include <string>
 #include <mutex>
 #include <vector>
@@ -47,19 +48,18 @@ struct ShardScratch {
     int recv_buffer = 0;            // ping-pong buffer holding the received slice
 };
 
+// One scratch per context.  A std::map: its elements never move, so the reference a rank
+// thread holds stays valid while other threads add their contexts' scratch (the in-process
+// multi-GPU path runs one thread per context).
 std::mutex g_scratch_mu;
-std::vector<std::pair<Context*, ShardScratch>>& all_scratch() {
-    static std::vector<std::pair<Context*, ShardScratch>> all;
-    return all;
+std::map<Context*, ShardScratch>& all_scratch() {
+    static auto* all = new std::map<Context*, ShardScratch>();  // outlives static teardown
+    return *all;
 }
 
 ShardScratch& scratch(Context* c) {
     std::lock_guard<std::mutex> lk(g_scratch_mu);
-    auto& all = all_scratch();
-    for (auto& p : all)
-        if (p.first == c) return p.second;
-    all.emplace_back(c, ShardScratch{});
-    return all.back().second;
+    return all_scratch()[c];
 }
 
 cudaStream_t pick(Context* c, void* stream) {
@@ -130,17 +130,15 @@ namespace ph0b {
 void shard_scratch_release(Context* c) {
     std::lock_guard<std::mutex> lk(g_scratch_mu);
     auto& all = all_scratch();
-    for (size_t i = 0; i < all.size(); ++i) {
-        if (all[i].first != c) continue;
-        ShardScratch& sc = all[i].second;
-        cudaSetDevice(c->device());
-        void* ps[] = {sc.d_spl, sc.d_totals, sc.d_bminmax, sc.d_table, sc.d_counts,
-                      sc.d_sample, sc.d_cand_uv, sc.d_peer};
-        for (void* p : ps)
-            if (p) cudaFree(p);
-        all.erase(all.begin() + (long)i);
-        return;
-    }
+    const auto it = all.find(c);
+    if (it == all.end()) return;
+    ShardScratch& sc = it->second;
+    cudaSetDevice(c->device());
+    void* ps[] = {sc.d_spl, sc.d_totals, sc.d_bminmax, sc.d_table, sc.d_counts,
+                  sc.d_sample, sc.d_cand_uv, sc.d_peer};
+    for (void* p : ps)
+        if (p) cudaFree(p);
+    all.erase(it);
 }
 }  // namespace ph0b
 
