@@ -152,6 +152,17 @@ inline Barcode h0_barcode(const double* x, std::size_t n, std::size_t d,
     return detail::run_into(x, n, d, scale, detail::opts(ropts, device));
 }
 
+// The same on several GPUs of this node (ph0b_options.n_gpus / devices; an ordinal may repeat).
+inline Barcode h0_barcode_multi(const double* x, std::size_t n, std::size_t d,
+                                const std::vector<std::int32_t>& devices,
+                                std::vector<double>* scale = nullptr,
+                                const ReductionOptions& ropts = {}) {
+    ph0b_options o = detail::opts(ropts, devices.empty() ? 0 : devices[0]);
+    o.n_gpus = static_cast<std::uint32_t>(devices.size());
+    o.devices = devices.data();
+    return detail::run_into(x, n, d, scale, o);
+}
+
 // kruskal_barcode (oracle.cpp:32-46): union-find over the GPU filtration (ph0b_kruskal_barcode).
 inline Barcode kruskal_barcode(const double* x, std::size_t n, std::size_t d,
                                std::vector<double>* scale = nullptr, int device = 0) {

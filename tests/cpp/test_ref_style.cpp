@@ -234,6 +234,30 @@ TEST_CASE("acceptance: oracle equivalence and bar-count law on 200 clouds") {  /
     }
 }
 
+TEST_CASE("drop-in adapter on a large cloud: D straight into a reused vector, multi-GPU") {
+    // K = 7.2e7 >= 2^26: the bucketed path that streams D while sorting, written into the
+    // caller's vector; a second call reuses its storage; virtual ranks on one GPU agree
+    const Cloud c = uniform(12000, 3, 77);
+    std::vector<double> scale;
+    const ph0b::Barcode a = barcode(c, &scale);
+    const std::vector<double> first = scale;
+    const ph0b::Barcode b = barcode(c, &scale);
+    CHECK(scale == first);
+    REQUIRE(a.finite.size() == 11999);
+    REQUIRE(b.finite.size() == a.finite.size());
+    for (std::size_t j = 0; j < a.finite.size(); ++j) {
+        CHECK(b.finite[j].death_grade == a.finite[j].death_grade);
+        CHECK(scale[a.finite[j].death_grade - 1] == a.finite[j].death_length);
+    }
+    for (std::size_t i = 1; i < scale.size(); ++i) REQUIRE(scale[i - 1] < scale[i]);
+    std::vector<double> scale2;
+    const ph0b::Barcode m = ph0b::h0_barcode_multi(c.x.data(), c.n, c.d, {0, 0, 0}, &scale2);
+    CHECK(scale2 == scale);
+    REQUIRE(m.finite.size() == a.finite.size());
+    for (std::size_t j = 0; j < a.finite.size(); ++j)
+        CHECK(m.finite[j].death_grade == a.finite[j].death_grade);
+}
+
 TEST_CASE("errors mirror the reference's exceptions") {
     Cloud bad = from_rows({{1.0, 0.0}, {0.0, 0.0}});
     bad.x[1] = INFINITY;  // point_cloud.cpp:17
