@@ -145,6 +145,14 @@ __global__ void __launch_bounds__(kUThreads, 3)
     // the key before each tile is loaded one tile ahead (its latency hides behind a tile)
     uint64_t k_before_next =
         tile < num_tiles && tile > 0 ? keys[(uint64_t)tile * kUT - 1] : 0ull;
+    // kMode 2: the tile's owned range and D offset, also loaded one tile ahead (C5: their
+    // exposed latency was ~30 % of the write pass's stall samples)
+    int2 own_next = make_int2(0, 0);
+    uint64_t off_next = 0;
+    if (kMode == 2 && tile < num_tiles) {
+        own_next = tile_own[tile];
+        off_next = tile_offsets[tile];
+    }
     const uint64_t base0 = d_base ? *d_base : 0ull;  // D index of this range's first length
     uint32_t phase[2] = {0, 0};
     int b = 0;
@@ -175,10 +183,15 @@ __global__ void __launch_bounds__(kUThreads, 3)
         // bookkeeping; its exact value matters for the first flag only when the run
         // fix-ups are off, i.e. when nothing rewrites it)
         if (next < num_tiles) k_before_next = keys[(uint64_t)next * kUT - 1];
+        const int2 ow = own_next;
+        const uint64_t tile_off = off_next;
+        if (kMode == 2 && next < num_tiles) {
+            own_next = tile_own[next];
+            off_next = tile_offsets[next];
+        }
 
         uint32_t os = 0, oe = tn;
         if (kMode == 2) {
-            const int2 ow = tile_own[tile];
             os = (uint32_t)ow.x;
             oe = (uint32_t)ow.y;
         } else if (low_bits) {
@@ -218,7 +231,13 @@ __global__ void __launch_bounds__(kUThreads, 3)
                         --st;
                     }
                     const bool from_prev = st == 0 && tile_start > 0 && p == p_before;
-                    if (first && !from_prev && st < tn) claims |= 1u << j;
+                    if (first && !from_prev && st < tn) {
+                        claims |= 1u << j;
+                        // the run's columns are loaded after the claims barrier: start
+                        // bringing them into L1 now (their latency was ~35 % of this pass's
+                        // stall samples, all threads waiting at the barrier behind it)
+                        asm volatile("prefetch.global.L1 [%0];" ::"l"(vals + tile_start + st));
+                    }
                 }
                 starts = claims;
             }
@@ -314,7 +333,7 @@ __global__ void __launch_bounds__(kUThreads, 3)
             }
             continue;  // (the loop-top barrier orders the buffer reuse)
         }
-        const uint64_t base = base0 + tile_offsets[tile];
+        const uint64_t base = base0 + tile_off;
         uint64_t run = base + warp_base;
         const uint32_t lt = lanemask_lt();
 #pragma unroll
