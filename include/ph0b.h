@@ -97,7 +97,7 @@ typedef struct ph0b_stage_times {
     uint32_t reduce_rounds;
     uint64_t columns_scanned; /* edge columns streamed by the reduction */
     float sort_passes_ms;     /* the radix passes alone (sort_ms minus the digit histogram) */
-    uint32_t reserved0;
+    uint32_t reduce_iterations; /* parallel resolution rounds of the reduction (hook + jump) */
     uint64_t d2h_bytes;       /* host-output calls: bytes actually moved device -> host
                                  (D is shipped delta-encoded: 3-4 B per distinct length) */
 } ph0b_stage_times;
@@ -261,6 +261,16 @@ int ph0b_shard_sort_unique(ph0b_context* ctx, uint64_t count, uint64_t kmin, uin
 int ph0b_shard_reduce(ph0b_context* ctx, uint64_t n, uint64_t count, uint64_t grade_offset,
                       void* stream, uint64_t* m, const uint32_t** d_uv,
                       const uint64_t** d_grade, const double** d_length);
+/* The same, continuing the forest left by the key ranges before this one (the reference's
+ * left-to-right reduction cut at range boundaries): init_labels (host, n entries; NULL:
+ * singletons) are the preceding ranges' final tree labels, the reduction stops after
+ * `target` surviving columns (0: n - 1), and final_labels (host, optional) receives this
+ * range's final labels for the next range.  Survivors' outputs as ph0b_shard_reduce. */
+int ph0b_shard_reduce_continue(ph0b_context* ctx, uint64_t n, uint64_t count,
+                               uint64_t grade_offset, const uint32_t* init_labels,
+                               uint32_t target, void* stream, uint64_t* m,
+                               const uint32_t** d_uv, const uint64_t** d_grade,
+                               const double** d_length, uint32_t* final_labels);
 /* Column reduction of `count` columns given in filtration order (device supports): host
  * indices of the surviving columns, ascending. */
 int ph0b_reduce_columns(ph0b_context* ctx, const uint32_t* d_uv, uint64_t count, uint64_t n,

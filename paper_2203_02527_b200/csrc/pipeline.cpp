@@ -655,6 +655,7 @@ Status Context::run(const double* dX, uint64_t n, uint64_t d, uint32_t layout,
         if (!s.good()) return s;
         PH0B_TRY(cudaEventRecord(ev_[4], st), "event");
         r.times.reduce_rounds = rst.rounds;
+        r.times.reduce_iterations = rst.iterations;
         r.times.columns_scanned = rst.scanned;
         const uint32_t m = rst.survivors;
         if (m != n - 1)
@@ -1240,6 +1241,7 @@ Status Context::run_host_overlapped(const double* X, uint64_t n, uint64_t d, uin
     r.n_finite = m;
     r.essential = n - m;
     r.times.reduce_rounds = rst.rounds;
+    r.times.reduce_iterations = rst.iterations;
     r.times.columns_scanned = rst.scanned;
     cudaEventElapsedTime(&r.times.distance_ms, ev_[0], ev_[1]);
     cudaEventElapsedTime(&r.times.sort_ms, ev_[1], ev_[2]);

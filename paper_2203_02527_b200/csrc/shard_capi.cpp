@@ -377,6 +377,50 @@ int ph0b_shard_reduce(ph0b_context* ctx, uint64_t n, uint64_t count, uint64_t gr
     return PH0B_OK;
 }
 
+int ph0b_shard_reduce_continue(ph0b_context* ctx, uint64_t n, uint64_t count,
+                               uint64_t grade_offset, const uint32_t* init_labels,
+                               uint32_t target, void* stream, uint64_t* m,
+                               const uint32_t** d_uv, const uint64_t** d_grade,
+                               const double** d_length, uint32_t* final_labels) {
+    if (!ctx) return ph0b::capi_fail(PH0B_ERR_INVALID_ARGUMENT, "null context");
+    Context* c = reinterpret_cast<Context*>(ctx);
+    std::lock_guard<std::mutex> lk(c->mu);
+    cudaStream_t st = pick(c, stream);
+    c->launches = 0;
+    const uint32_t* d_init = nullptr;
+    if (init_labels && n) {  // the forest left by the preceding key ranges (host labels)
+        if (cudaMemcpyAsync(c->lows_buffer(), init_labels, n * 4, cudaMemcpyHostToDevice, st))
+            return ph0b::capi_fail(PH0B_ERR_CUDA, "H2D forest labels");
+        d_init = c->lows_buffer();
+    }
+    ph0b::ReduceStats rst;
+    Status s = count ? c->stage_reduce(c->vals(c->cur()), count, (uint32_t)n, st, &rst, d_init,
+                                       target)
+                     : Status::ok();
+    if (s.good() && rst.survivors) s = c->stage_collect(rst.survivors, count, grade_offset, st);
+    if (!s.good()) return ph0b::capi_fail(s);
+    ShardScratch& sc = scratch(c);
+    int rc = ensure(reinterpret_cast<void**>(&sc.d_cand_uv), &sc.cand_cap, (n + 1) * 4);
+    if (rc) return rc;
+    c->launches += ph0b::launch_gather_u32(c->vals(c->cur()), c->surv_sorted(), rst.survivors,
+                                           sc.d_cand_uv, st);
+    ph0b::capi_set_launches(c->launches);
+    if (final_labels && n) {
+        const uint32_t* src = count ? c->comp() : d_init;  // nothing reduced: labels unchanged
+        if (src && cudaMemcpyAsync(final_labels, src, n * 4, cudaMemcpyDeviceToHost, st))
+            return ph0b::capi_fail(PH0B_ERR_CUDA, "D2H forest labels");
+        if (!src)
+            for (uint64_t v = 0; v < n; ++v) final_labels[v] = (uint32_t)v;
+    }
+    if (cudaGetLastError() != cudaSuccess || cudaStreamSynchronize(st))
+        return ph0b::capi_fail(PH0B_ERR_CUDA, "shard reduce");
+    if (m) *m = rst.survivors;
+    if (d_uv) *d_uv = sc.d_cand_uv;
+    if (d_grade) *d_grade = c->death_grade();
+    if (d_length) *d_length = c->death_length();
+    return PH0B_OK;
+}
+
 int ph0b_reduce_columns(ph0b_context* ctx, const uint32_t* d_uv, uint64_t count, uint64_t n,
                         void* stream, uint32_t* idx_host, uint64_t* n_out) {
     if (!ctx) return ph0b::capi_fail(PH0B_ERR_INVALID_ARGUMENT, "null context");

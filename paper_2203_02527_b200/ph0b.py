@@ -41,7 +41,7 @@ EXPORTED_SYMBOLS = [
     "ph0b_shard_partition_count", "ph0b_shard_recv_peer",
     "ph0b_shard_scatter_peers", "ph0b_ipc_get_handle", "ph0b_ipc_open_handle", "ph0b_ipc_close",
     "ph0b_scale_release", "ph0b_host_cache_trim", "ph0b_reduced_supports",
-    "ph0b_release_resources",
+    "ph0b_release_resources", "ph0b_shard_reduce_continue",
 ]
 
 
@@ -67,7 +67,7 @@ class StageTimes(C.Structure):
                 ("reduce_ms", C.c_float), ("collect_ms", C.c_float), ("total_ms", C.c_float),
                 ("sort_passes", C.c_uint32), ("reduce_rounds", C.c_uint32),
                 ("columns_scanned", C.c_uint64), ("sort_passes_ms", C.c_float),
-                ("reserved0", C.c_uint32), ("d2h_bytes", C.c_uint64)]
+                ("reduce_iterations", C.c_uint32), ("d2h_bytes", C.c_uint64)]
 
     def as_dict(self):
         return {f: getattr(self, f) for f, _ in self._fields_}

@@ -6,15 +6,14 @@ exchange step.
              stable partition by splitter -> all-to-all-v (NCCL) of (length, column)
              local radix sort + unique  -> D slice r (D is sharded, contiguous in global order)
              all-gather |D_r| -> grade offsets
-             local column reduction of the slice -> <= N-1 candidate columns
-             gather candidates -> rank 0: column reduction over <= P(N-1) columns -> bars
+             column reduction of the key ranges in order, each continuing the forest the
+             earlier ranges left (their tree labels); stops at N-1 survivors -> bars
 
 Exactness: rows are assigned in increasing u and every partition is stable, so what a rank
 receives (sources in rank order) is in u-major order and the local stable sort produces the
 global (length, u, v) order restricted to its key range; equal lengths never straddle ranks
-(splitters are key values).  A column that reduces to zero inside its own key range closes a
-cycle of earlier columns, so it is a cycle globally; the survivors of all ranges, reduced again
-in global order, are exactly the reference's surviving columns (the minimum spanning forest).
+(splitters are key values).  Reducing the ranges in order, each from the forest the earlier
+ranges left, is the reference's left-to-right reduction itself, cut at range boundaries.
 
 `Comm` hides the transport: torch.distributed (NCCL on GPUs, gloo for the CPU tests) or a
 thread-based comm that runs P virtual ranks in one process (single-GPU parity tests).
@@ -303,6 +302,29 @@ class DeviceBackend:
                                             C.byref(moved)))
         return int(moved.value)
 
+    def reduce_continue(self, n, count, grade_offset, labels, target):
+        """Local reduction continuing the forest of the ranges before this one (host labels
+        or None); returns the survivors' (uv, grade, length) and this range's final labels."""
+        m, up, gp, lp = C.c_uint64(), C.c_void_p(), C.c_void_p(), C.c_void_p()
+        lab_in = (np.ascontiguousarray(labels, np.uint32) if labels is not None else None)
+        lab_out = np.empty(max(n, 1), np.uint32)
+        fn = self.L.ph0b_shard_reduce_continue
+        if not fn.argtypes:
+            fn.restype = C.c_int
+            fn.argtypes = [C.c_void_p, C.c_uint64, C.c_uint64, C.c_uint64, C.c_void_p, C.c_uint32,
+                           C.c_void_p, C.POINTER(C.c_uint64), C.POINTER(C.c_void_p),
+                           C.POINTER(C.c_void_p), C.POINTER(C.c_void_p), C.c_void_p]
+        _b._check(fn(self.h, n, count, grade_offset,
+                     C.c_void_p(lab_in.ctypes.data) if lab_in is not None else None,
+                     max(0, int(target)), None, C.byref(m), C.byref(up), C.byref(gp),
+                     C.byref(lp), C.c_void_p(lab_out.ctypes.data)))
+        self._count()
+        m = m.value
+        uv = _dev_view(up.value, m, "<i4", self.device).cpu().numpy().view(np.uint32)
+        g = _dev_view(gp.value, m, "<i8", self.device).cpu().numpy().view(np.uint64)
+        ln = _dev_view(lp.value, m, "<f8", self.device).cpu().numpy()
+        return uv.copy(), g.copy(), ln.copy(), lab_out[:n].copy()
+
     def reduce(self, n, count, grade_offset):
         m, up, gp, lp = C.c_uint64(), C.c_void_p(), C.c_void_p(), C.c_void_p()
         _b._check(self.L.ph0b_shard_reduce(self.h, n, count, grade_offset, None, C.byref(m),
@@ -379,18 +401,30 @@ def h0_barcode_sharded(x_ptr, n: int, d: int, comm, backend, layout=_b.COL_MAJOR
     n_distinct, scale = backend.sort_unique(count, kmin, kmax)
     nds = comm.allgather_obj(int(n_distinct)) if P > 1 else [int(n_distinct)]
     offset = int(sum(nds[:r]))
-    uv, grade, length = backend.reduce(n, count, offset)
-    cands = comm.allgather_obj((uv, grade, length)) if P > 1 else [(uv, grade, length)]
+    # column reduction: the key ranges in filtration order, each continuing the forest the
+    # ranges before it left (their final tree labels, N u32) — the reference's left-to-right
+    # reduction (reduction.cpp:33-49) cut at range boundaries, so no final re-reduction; it
+    # stops as soon as n-1 columns survived (at C5 within the first range)
+    labels, found = None, 0
+    mine = (np.zeros(0, np.uint32), np.zeros(0, np.uint64), np.zeros(0))
+    for turn in range(P):
+        if found >= n - 1:
+            break
+        state = None
+        if r == turn:
+            uv, grade, length, labels_out = backend.reduce_continue(n, count, offset, labels,
+                                                                    n - 1 - found)
+            mine = (uv, grade, length)
+            state = (len(uv), labels_out)
+        if P > 1:
+            state = comm.allgather_obj(state)[turn]
+        found += state[0]
+        labels = state[1]
+    parts = comm.allgather_obj(mine) if P > 1 else [mine]
     dg = dl = None
     if r == 0:
-        all_uv = np.concatenate([c[0] for c in cands]) if cands else np.zeros(0, np.uint32)
-        all_g = np.concatenate([c[1] for c in cands]) if cands else np.zeros(0, np.uint64)
-        all_l = np.concatenate([c[2] for c in cands]) if cands else np.zeros(0)
-        if P > 1:
-            idx = backend.reduce_columns(all_uv, n)
-            dg, dl = all_g[idx], all_l[idx]
-        else:
-            dg, dl = all_g, all_l
+        dg = np.concatenate([np.asarray(p_[1], np.uint64) for p_ in parts])
+        dl = np.concatenate([np.asarray(p_[2], np.float64) for p_ in parts])
     ess = n - (n - 1 if n >= 1 else 0)
     return ShardResult(rank=r, parts=P, death_grade=dg, death_length=dl, essential_count=ess,
                        scale_offset=offset, n_scale_local=int(n_distinct),

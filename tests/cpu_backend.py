@@ -135,6 +135,31 @@ class NumpyBackend:
         self.D = np.unique(self.keys)
         return len(self.D), self.D.view(np.float64)
 
+    def reduce_continue(self, n, count, offset, labels, target):
+        """Kruskal in filtration order from the forest `labels` (root labels; None: singletons),
+        stopping after `target` survivors; final labels = each vertex's tree minimum."""
+        parent = np.arange(n) if labels is None else np.asarray(labels, np.int64).copy()
+
+        def find(x):
+            while parent[x] != x:
+                parent[x] = parent[parent[x]]
+                x = parent[x]
+            return x
+
+        keep = []
+        for i, e in enumerate(self.vals):
+            if len(keep) >= target:
+                break
+            a, b = find(int(e) >> 16), find(int(e) & 0xFFFF)
+            if a != b:
+                lo, hi = min(a, b), max(a, b)
+                parent[hi] = lo  # the root stays the tree minimum
+                keep.append(i)
+        keep = np.array(keep, np.int64)
+        g = offset + 1 + np.searchsorted(self.D, self.keys[keep])
+        lab = np.array([find(v) for v in range(n)], np.uint32)
+        return (self.vals[keep], g.astype(np.uint64), self.keys[keep].view(np.float64), lab)
+
     def reduce(self, n, count, offset):
         keep = kruskal(self.vals, n)
         g = offset + 1 + np.searchsorted(self.D, self.keys[keep])

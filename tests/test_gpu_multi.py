@@ -59,7 +59,7 @@ def test_small_clouds_take_single_gpu_path():
         same(pkg.h0_barcode(X, devices=[0, 0]), pkg.h0_barcode(X))
 
 
-@pytest.mark.parametrize("cfg,ranks", [("C4", 2), ("C4", 8), ("C5", 8)])
+@pytest.mark.parametrize("cfg,ranks", [("C4", 2), ("C4", 8), ("C5", 2), ("C5", 4), ("C5", 8)])
 def test_multi_vs_reference_full_size(cfg, ranks):
     g = np.load(ob.ROOT / "tests" / "golden" / f"ref_kruskal_{cfg}.npz")
     X = pkg.config_cloud(cfg)
