@@ -352,6 +352,16 @@ int run_multi_gpu(const std::vector<int>& devices, const double* X, uint64_t n, 
     std::lock_guard<std::mutex> lk(g_runners_mu);  // one multi-GPU run at a time
     auto& slot = runners()[devices];
     if (!slot) slot = std::make_unique<MultiRunner>(devices);
+    int rc = slot->run(X, n, d, layout, death_grade, death_length, n_finite, essential, scale,
+                       scale_capacity, n_scale, times);
+    if (rc != PH0B_ERR_OUT_OF_MEMORY || runners().size() == 1) return rc;
+    // out of device memory while other device lists' runners hold theirs: free those, retry
+    for (auto it = runners().begin(); it != runners().end();) {
+        if (it->first != devices)
+            it = runners().erase(it);
+        else
+            ++it;
+    }
     return slot->run(X, n, d, layout, death_grade, death_length, n_finite, essential, scale,
                   scale_capacity, n_scale, times);
 }

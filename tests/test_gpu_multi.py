@@ -72,7 +72,7 @@ def test_multi_vs_reference_full_size(cfg, ranks):
     assert np.array_equal(bits(bc.death_length), bits(g["death_length"]))
 
 
-@pytest.fixture(scope="module", autouse=True)
+@pytest.fixture(autouse=True)
 def _release_runners():
     yield
-    pkg.lib().ph0b_release_resources()  # the 8 virtual ranks' buffers (C5: ~50 GB)
+    pkg.lib().ph0b_release_resources()  # the virtual ranks' buffers (C5: ~50 GB per list)
