@@ -105,12 +105,12 @@ public:
 
     int init() {
         const unsigned hw = std::thread::hardware_concurrency();
-        const unsigned per = std::max(1u, (hw > 1 ? hw - 1 : 1) / (unsigned)ranks_.size());
+        if (!pool_) pool_ = std::make_shared<DecodePool>(hw > 2 ? hw - 1 : 1);
         for (auto& r : ranks_) {
             if (r.h) continue;
             const int rc = ph0b_context_create(r.device, &r.h);
             if (rc) return rc;
-            r.ctx()->set_decode_threads(per);
+            r.ctx()->set_decode_pool(pool_);  // one host decoder pool for every rank's D slice
         }
         // NVLink P2P between every pair of distinct devices (the partition kernel stores into
         // its peers' receive buffers)
@@ -327,6 +327,7 @@ public:
 
 private:
     std::vector<Rank> ranks_;
+    std::shared_ptr<DecodePool> pool_;
 };
 
 }  // namespace

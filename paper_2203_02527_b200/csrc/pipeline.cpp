@@ -743,7 +743,7 @@ Status Context::prepare_stream(uint64_t k, uint32_t B) {
         }();
         const unsigned hw = std::thread::hardware_concurrency();
         const unsigned dflt = decode_threads_ ? decode_threads_ : (hw > 2 ? hw - 1 : 1);
-        pool_ = std::make_unique<DecodePool>(env_threads > 0 ? (unsigned)env_threads : dflt);
+        pool_ = std::make_shared<DecodePool>(env_threads > 0 ? (unsigned)env_threads : dflt);
     }
     return Status::ok();
 }

@@ -126,6 +126,10 @@ public:
     // host threads decoding this context's D stream (0: cores - 1); set before the first
     // host-output call (several contexts of one process share the cores)
     void set_decode_threads(unsigned t) { decode_threads_ = t; }
+    // or share one pool between contexts (the multi-GPU path: the ranks' D slices stream at
+    // the same time; each rank's pieces stay in submission order, so no piece waits on a
+    // piece queued behind it)
+    void set_decode_pool(std::shared_ptr<DecodePool> p) { pool_ = std::move(p); }
 
     std::mutex mu;
     int device() const { return device_; }
@@ -198,7 +202,7 @@ private:
     uint64_t* h_pieceoff_ = nullptr;  uint64_t* d_pieceoff_ = nullptr;  // mapped
     uint64_t h_pieceoff_cap_ = 0;
     uint8_t* h_craw_ = nullptr;    uint64_t h_craw_cap_ = 0;
-    std::unique_ptr<DecodePool> pool_;
+    std::shared_ptr<DecodePool> pool_;
     std::vector<cudaEvent_t> bucket_ev_;
     Status grow_host(void** p, uint64_t* cap, uint64_t need);
     uint32_t* part_counts_ = nullptr; uint64_t part_counts_cap_ = 0;
