@@ -146,56 +146,74 @@ __device__ __forceinline__ void finish_block(uint64_t kmin, uint64_t kmax, uint3
             if (sh_hist[b]) atomicAdd(&hist0[b], sh_hist[b]);
 }
 
-// Shared-memory TMA path, d <= 32 (D = 0: runtime d).
+// Shared-memory TMA path, d <= 32 (D = 0: runtime d).  kStages point-tile pairs in flight,
+// each with a "full" mbarrier (TMA completion) and an "empty" one (every warp arrives when it
+// is done with the pair): warps move from tile to tile on their own, and thread 0 refills a
+// stage as soon as the last warp has left it — no CTA-wide barrier per tile.
+template <int D>
+constexpr int distance_stages() { return D > 0 && D <= 16 ? 3 : 2; }
+
 template <int D>
 __global__ void __launch_bounds__(kThreads)
     k1_distance_tma(const __grid_constant__ CUtensorMap tmap, uint32_t n, uint32_t dd,
                     uint32_t nb, uint32_t total_tiles, uint32_t t0, uint32_t u_lo, uint32_t u_hi,
                     uint64_t e_off, uint64_t* __restrict__ keys,
                     uint32_t* __restrict__ vals, uint64_t* minmax, uint32_t* hist0) {
+    constexpr int S = distance_stages<D>();
     extern __shared__ __align__(128) double smem[];
-    __shared__ uint64_t bar[2];
+    __shared__ uint64_t full[S], empty[S];
     __shared__ uint32_t sh_hist[256];
     __shared__ uint64_t sh_min[kWarps], sh_max[kWarps];
     const int dim = D > 0 ? D : (int)dd;
     const uint32_t tile_elems = kTile * dim;   // doubles per {128, d} box
-    // buffer b: [u-tile | v-tile]
-    double* buf[2] = {smem, smem + 2 * tile_elems};
-    const uint32_t bytes = 2u * tile_elems * 8u;
+    const uint32_t bytes = 2u * tile_elems * 8u;  // stage s: [u-tile | v-tile]
+    auto stage = [&](int s_) { return smem + (size_t)s_ * 2 * tile_elems; };
 
     for (int b = threadIdx.x; b < 256; b += kThreads) sh_hist[b] = 0;
     if (threadIdx.x == 0) {
-        mbar_init(&bar[0], 1);
-        mbar_init(&bar[1], 1);
+        for (int s_ = 0; s_ < S; ++s_) {
+            mbar_init(&full[s_], 1);
+            mbar_init(&empty[s_], kWarps);
+        }
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
     __syncthreads();
 
-    uint32_t tile = blockIdx.x;
-    auto issue = [&](uint32_t t, int b) {
+    auto issue = [&](uint32_t t, int s_) {
         uint32_t bu, bv;
         tile_coords(t + t0, nb, bu, bv);
         asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-        mbar_expect_tx(&bar[b], bytes);
-        tma_load_2d(buf[b], &tmap, &bar[b], (int)(bu * kTile), 0);
-        tma_load_2d(buf[b] + tile_elems, &tmap, &bar[b], (int)(bv * kTile), 0);
+        mbar_expect_tx(&full[s_], bytes);
+        tma_load_2d(stage(s_), &tmap, &full[s_], (int)(bu * kTile), 0);
+        tma_load_2d(stage(s_) + tile_elems, &tmap, &full[s_], (int)(bv * kTile), 0);
     };
-    if (threadIdx.x == 0 && tile < total_tiles) issue(tile, 0);
+    if (threadIdx.x == 0)
+        for (int s_ = 0; s_ < S - 1; ++s_) {
+            const uint32_t t = blockIdx.x + (uint32_t)s_ * gridDim.x;
+            if (t < total_tiles) issue(t, s_);
+        }
 
     uint64_t kmin = ~0ull, kmax = 0;
-    uint32_t phase[2] = {0, 0};
-    int b = 0;
-    for (; tile < total_tiles; tile += gridDim.x) {
-        mbar_wait(&bar[b], phase[b]);
-        phase[b] ^= 1u;
-        __syncthreads();  // everyone is done with buf[b^1] (previous tile)
-        const uint32_t next = tile + gridDim.x;
-        if (threadIdx.x == 0 && next < total_tiles) issue(next, b ^ 1);
+    uint32_t it = 0;
+    for (uint32_t tile = blockIdx.x; tile < total_tiles; tile += gridDim.x, ++it) {
+        const int s_ = (int)(it % S);
+        mbar_wait(&full[s_], (it / S) & 1u);
+        if (threadIdx.x == 0) {  // refill the stage left at iteration it - 1
+            const uint32_t next = tile + (uint32_t)(S - 1) * gridDim.x;
+            if (next < total_tiles) {
+                const int sn = (int)((it + S - 1) % S);
+                if (it >= 1) mbar_wait(&empty[sn], ((it - 1) / S) & 1u);
+                issue(next, sn);
+            }
+        }
         uint32_t bu, bv;
         tile_coords(tile + t0, nb, bu, bv);
-        tile_edges<D>(buf[b], buf[b] + tile_elems, kTile, dim, n, bu * kTile, bv * kTile, u_lo,
-                      u_hi, e_off, keys, vals, kmin, kmax, hist0 ? sh_hist : nullptr);
-        b ^= 1;
+        tile_edges<D>(stage(s_), stage(s_) + tile_elems, kTile, dim, n, bu * kTile, bv * kTile,
+                      u_lo, u_hi, e_off, keys, vals, kmin, kmax, hist0 ? sh_hist : nullptr);
+        __syncwarp();
+        if ((threadIdx.x & 31) == 0)
+            asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(&empty[s_]))
+                         : "memory");
     }
     __syncthreads();
     finish_block(kmin, kmax, sh_hist, sh_min, sh_max, minmax, hist0);
@@ -280,7 +298,7 @@ template <int D>
 int launch_tma(const DistanceArgs& a, const CUtensorMap& map, uint32_t nb, uint32_t total,
                uint32_t t0, cudaStream_t s, int num_sms) {
     const uint32_t dim = D > 0 ? D : a.d;
-    const size_t smem = 4ull * kTile * dim * sizeof(double);
+    const size_t smem = 2ull * distance_stages<D>() * kTile * dim * sizeof(double);
     auto kern = k1_distance_tma<D>;
     const int per_sm = kernel_blocks_per_sm((const void*)kern, kThreads, smem);
     if (per_sm < 1) return 0;
