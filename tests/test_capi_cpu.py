@@ -159,3 +159,46 @@ def test_host_packed_decoder_roundtrip():
                               C.c_void_p(bad.ctypes.data), C.c_void_p(one.ctypes.data), 1, 1024,
                               C.c_void_p(one.ctypes.data))
     assert rc == pkg.ph0b.PH0B_ERR_INVALID_ARGUMENT
+
+
+def test_abi3_sized_options_still_accepted():
+    """An ABI-3 caller's ph0b_options ends at `workers` (20 bytes): still parsed (its
+    workers == 0 reaches the reference's message), never read past its end."""
+    import ctypes as C
+    o = ph0b.Options(20, 0, 0, 1, 0)
+    X = np.zeros((3, 2))
+    res = ph0b.Result()
+    rc = pkg.lib().ph0b_h0_barcode(C.c_void_p(X.ctypes.data), 3, 2, ph0b.COL_MAJOR, C.byref(o),
+                                   C.byref(res))
+    assert rc == ph0b.PH0B_ERR_INVALID_ARGUMENT
+    assert b"worker count must be at least 1" in pkg.lib().ph0b_last_error()
+    o.struct_size = 16
+    rc = pkg.lib().ph0b_h0_barcode(C.c_void_p(X.ctypes.data), 3, 2, ph0b.COL_MAJOR, C.byref(o),
+                                   C.byref(res))
+    assert rc == ph0b.PH0B_ERR_INVALID_ARGUMENT
+    assert b"struct_size too small" in pkg.lib().ph0b_last_error()
+
+
+def test_kruskal_flag_limited_to_65536_before_any_device_work():
+    X = np.zeros((65537, 1))
+    with pytest.raises(pkg.Ph0bError, match="65536"):
+        pkg.kruskal_barcode(X)
+
+
+def test_null_context_rejected():
+    import ctypes as C
+    L = pkg.lib()
+    fn = L.ph0b_run_device
+    assert fn(None, None, 0, 0, 0, None, None) == ph0b.PH0B_ERR_INVALID_ARGUMENT
+    assert b"null context" in L.ph0b_last_error()
+    assert L.ph0b_context_reserve(None, 1, 1) == ph0b.PH0B_ERR_INVALID_ARGUMENT
+    assert L.ph0b_context_workspace_bytes(None) == 0
+    L.ph0b_shard_sample.argtypes = [C.c_void_p, C.c_uint64, C.c_void_p]
+    assert L.ph0b_shard_sample(None, 4, None) == ph0b.PH0B_ERR_INVALID_ARGUMENT
+
+
+def test_release_functions_callable_without_gpu():
+    L = pkg.lib()
+    L.ph0b_host_cache_trim()
+    L.ph0b_release_resources()
+    L.ph0b_scale_release(None)
