@@ -76,3 +76,35 @@ def test_multi_vs_reference_full_size(cfg, ranks):
 def _release_runners():
     yield
     pkg.lib().ph0b_release_resources()  # the virtual ranks' buffers (C5: ~50 GB per list)
+
+
+def _into(X, devices, capacity):
+    import ctypes as C
+    from paper_2203_02527_b200 import ph0b
+    Xf = np.asfortranarray(X)
+    n, d = X.shape
+    opt = ph0b._opts(0, 0, 1, True, devices)
+    dg = np.empty(n, np.uint64)
+    dl = np.empty(n)
+    sc = np.empty(max(capacity, 1))
+    nf, ess, ns = C.c_uint64(), C.c_uint64(), C.c_uint64()
+    rc = pkg.lib().ph0b_h0_barcode_into(C.c_void_p(Xf.ctypes.data), n, d, ph0b.COL_MAJOR,
+                                        C.byref(opt), C.c_void_p(dg.ctypes.data),
+                                        C.c_void_p(dl.ctypes.data), C.byref(nf), C.byref(ess),
+                                        C.c_void_p(sc.ctypes.data), capacity, C.byref(ns), None)
+    return rc, pkg.lib().ph0b_last_error().decode(), ns.value, sc
+
+
+def test_multi_into_capacity_and_bad_device():
+    from paper_2203_02527_b200 import ph0b
+    X = np.random.default_rng(4).normal(size=(3000, 3))
+    ref = pkg.h0_barcode(X)
+    rc, msg, ns, sc = _into(X, [0, 0, 0], len(ref.scale))
+    assert rc == 0 and ns == len(ref.scale)
+    assert np.array_equal(sc[:ns].view(np.uint64), ref.scale.view(np.uint64))
+    rc, msg, _, _ = _into(X, [0, 0, 0], len(ref.scale) - 1)
+    assert rc == ph0b.PH0B_ERR_CAPACITY and "too small" in msg
+    import torch
+    bad = torch.cuda.device_count() + 3
+    rc, msg, _, _ = _into(X, [0, bad], len(ref.scale))
+    assert rc != 0 and msg
