@@ -94,7 +94,7 @@ int usage() {
     std::cerr << "usage: ph0b {generate|compute|oracle} [options]\n"
                  "  generate --n N [--dim 2] [--seed 1] [--out -]\n"
                  "  compute  (--in FILE | --n N [--dim 2] [--seed 1]) [--workers 1]"
-                 " [--pivot on|off] [--show-essential] [--out -]\n"
+                 " [--pivot on|off] [--gpus 1] [--show-essential] [--out -]\n"
                  "  oracle   (--in FILE | --n N [--dim 2] [--seed 1]) [--show-essential]"
                  " [--out -]\n";
     return 109;
@@ -120,7 +120,7 @@ int main(int argc, char** argv) {
         if (cmd == "compute") {
             const Args a = parse_args(argc, argv, 2,
                                       {"--in", "--n", "--dim", "--seed", "--workers", "--pivot",
-                                       "--out"},
+                                       "--gpus", "--out"},
                                       {"--show-essential"});
             const std::string pivot = get(a, "--pivot", "on");
             if (pivot != "on" && pivot != "off")
@@ -129,9 +129,14 @@ int main(int argc, char** argv) {
             // 0 and 1 both mean the sequential reduction; the result is identical anyway.
             const std::uint64_t workers = to_u64("--workers", get(a, "--workers", "1"));
             const ph0b::Cloud c = load_cloud(a);
-            const ph0b::Barcode bc = ph0b::h0_barcode(
-                c.x.data(), c.n, c.d, nullptr,
-                ph0b::ReductionOptions{pivot == "on", (unsigned)(workers > 1 ? workers : 1)});
+            const ph0b::ReductionOptions ro{pivot == "on", (unsigned)(workers > 1 ? workers : 1)};
+            // --gpus G (not in the reference CLI): the same bars on GPUs 0..G-1 of this node
+            const std::uint64_t gpus = to_u64("--gpus", get(a, "--gpus", "1"));
+            std::vector<std::int32_t> devs;
+            for (std::uint64_t g = 0; g < gpus; ++g) devs.push_back((std::int32_t)g);
+            const ph0b::Barcode bc =
+                gpus > 1 ? ph0b::h0_barcode_multi(c.x.data(), c.n, c.d, devs, nullptr, ro)
+                         : ph0b::h0_barcode(c.x.data(), c.n, c.d, nullptr, ro);
             write_output(get(a, "--out", "-"),
                          ph0b::format_barcode(bc, a.flag.count("--show-essential") > 0));
             return 0;
