@@ -1,0 +1,69 @@
+"""GPU: seeded random clouds of mixed shapes through every entry point, each against the C
+oracle (oracle/ph0_oracle.c, pinned to the reference): the drop-in call, the context host
+path, the multi-GPU path (virtual ranks), the reduced supports and the GPU Kruskal barcode.
+Shapes mix uniform / clustered / lattice / duplicated / tiny-scale points, N across the sort
+and distance tile boundaries, d in 1..20."""
+import numpy as np
+import pytest
+
+import oracle_bridge as ob
+import paper_2203_02527_b200 as pkg
+
+pytestmark = pytest.mark.gpu
+
+
+def bits(a):
+    return np.asarray(a, np.float64).view(np.uint64)
+
+
+def cloud(seed):
+    rng = np.random.default_rng(seed)
+    n = int(rng.choice([2, 3, 17, 127, 128, 129, 300, 1000, 2049, 3000]))
+    d = int(rng.integers(1, 21))
+    kind = seed % 6
+    if kind == 0:
+        X = rng.uniform(-1, 1, size=(n, d))
+    elif kind == 1:
+        c = rng.uniform(-10, 10, size=(5, d))
+        X = c[rng.integers(0, 5, n)] + 0.1 * rng.normal(size=(n, d))
+    elif kind == 2:  # integer lattice values: many exact ties
+        X = rng.integers(0, 5, size=(n, d)).astype(np.float64)
+    elif kind == 3:  # duplicated points
+        base = rng.normal(size=(max(1, n // 4), d))
+        X = base[rng.integers(0, len(base), n)]
+    elif kind == 4:  # tiny scale (subnormal-adjacent lengths)
+        X = rng.normal(size=(n, d)) * 1e-300
+    else:  # far-apart groups
+        X = rng.normal(size=(n, d)) + 1e6 * (rng.integers(0, 3, size=(n, 1)))
+    return X
+
+
+@pytest.mark.parametrize("seed", range(36))
+def test_random_cloud_all_entry_points(seed):
+    X = cloud(seed)
+    n = X.shape[0]
+    ref = ob.oracle_filtration_and_bars(X, reduction_limit=1000)
+    bc = pkg.h0_barcode(X)
+    assert bc.essential_count == ref["essential"]
+    assert np.array_equal(bc.death_grade, ref["death_grade"])
+    assert np.array_equal(bits(bc.death_length), bits(ref["death_length"]))
+    assert np.array_equal(bits(bc.scale), bits(ref["scale"]))
+    ctx = pkg.Context(0)
+    dg, dl, sc = np.empty(n, np.uint64), np.empty(n), np.empty(max(len(ref["scale"]), 1))
+    nf, ess, ns, _ = ctx.run_host(np.ascontiguousarray(X), dg, dl, sc, layout=pkg.ph0b.ROW_MAJOR)
+    ctx.close()
+    assert nf == len(ref["death_grade"]) and ess == ref["essential"]
+    assert np.array_equal(dg[:nf], ref["death_grade"])
+    assert np.array_equal(bits(sc[:ns]), bits(ref["scale"]))
+    ranks = 2 + seed % 3
+    mg = pkg.h0_barcode(X, devices=[0] * ranks)
+    assert np.array_equal(mg.death_grade, ref["death_grade"])
+    assert np.array_equal(bits(mg.scale), bits(ref["scale"]))
+    if n >= 2:
+        cols, lo, hi = pkg.reduced_supports(X)
+        sp = ob.reduce_sparse(ob.filtration(X), stop_at_spanning=True)
+        assert np.array_equal(cols, sp["columns"])
+        assert np.array_equal(lo, sp["rows_lo"]) and np.array_equal(hi, sp["rows_hi"])
+        kr = pkg.kruskal_barcode(X, return_scale=False)
+        assert np.array_equal(kr.death_grade, ref["death_grade"])
+    pkg.lib().ph0b_release_resources()
