@@ -20,16 +20,23 @@ int kernel_blocks_per_sm(const void* kern, int threads, size_t smem) {
     using Key = std::tuple<int, const void*, size_t, int>;
     static std::mutex mu;
     static std::map<Key, int> cache;
+    // the opt-in is a per-kernel maximum: it is only ever raised, so a launch with less
+    // shared memory never lowers it under a cached larger size (kernels whose shared memory
+    // depends on N or d are launched with several sizes)
+    static std::map<std::pair<int, const void*>, size_t> opted;
     const Key key{dev, kern, smem, threads};
     std::lock_guard<std::mutex> lock(mu);
     const auto it = cache.find(key);
     if (it != cache.end()) return it->second;
+    size_t& cur = opted[{dev, kern}];
     // (the opt-in also covers dynamic + static shared memory crossing 48 KB together)
-    if (smem > 0 &&
-        cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) !=
+    if (smem > cur) {
+        if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) !=
             cudaSuccess) {
-        cudaGetLastError();
-        return 0;  // not cached: a later call may retry
+            cudaGetLastError();
+            return 0;  // not cached: a later call may retry
+        }
+        cur = smem;
     }
     int per_sm = 0;
     if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, threads, smem) !=

@@ -336,12 +336,8 @@ int run_reduction(ReduceState& st, cudaStream_t s, int num_sms, uint32_t& epoch,
     // vs gathering them through L1)
     const size_t fsmem = ((size_t)n * 2 + 15) & ~(size_t)15;
     bool smem_filter = fsmem <= 200 * 1024 && !col_ids(n);
-    if (smem_filter && cudaFuncSetAttribute(k4_filter_range_s,
-                                            cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                            (int)fsmem) != cudaSuccess) {
-        cudaGetLastError();
+    if (smem_filter && kernel_blocks_per_sm((const void*)k4_filter_range_s, kFThreads, fsmem) < 1)
         smem_filter = false;
-    }
     uint64_t pos = 0;
     uint64_t window = std::min<uint64_t>(st.k, std::max<uint64_t>(8ull * n, 1u << 16));
     uint32_t survivors = 0;
