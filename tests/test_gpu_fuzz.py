@@ -67,3 +67,39 @@ def test_random_cloud_all_entry_points(seed):
         kr = pkg.kruskal_barcode(X, return_scale=False)
         assert np.array_equal(kr.death_grade, ref["death_grade"])
     pkg.lib().ph0b_release_resources()
+
+
+@pytest.mark.parametrize("kind", ["lattice3d", "dups", "tiny", "far"])
+def test_bucketed_host_path_vs_device_path(kind):
+    """K >= 2^26 takes the bucketed host path (partition, per-bucket sorts, packed D stream);
+    the device path (one global sort) is its reference here, bit for bit."""
+    import torch
+    rng = np.random.default_rng(len(kind))
+    n = 12000
+    if kind == "lattice3d":
+        X = rng.integers(0, 23, size=(n, 3)).astype(np.float64)
+    elif kind == "dups":
+        X = rng.normal(size=(n // 8, 5))[rng.integers(0, n // 8, n)]
+    elif kind == "tiny":
+        X = rng.normal(size=(n, 2)) * 1e-200
+    else:
+        X = rng.normal(size=(n, 4)) + 1e8 * rng.integers(0, 4, size=(n, 1))
+    ctx = pkg.Context(0)
+    xt = torch.from_numpy(np.asfortranarray(X).ravel(order="F").copy()).cuda()
+    r = ctx.run_device(xt.data_ptr(), n, X.shape[1])
+    cai = {"shape": (int(r.n_scale),), "typestr": "<i8", "data": (int(r.d_scale), False),
+           "version": 3, "strides": None}
+    D_dev = torch.as_tensor(type("C", (), {"__cuda_array_interface__": cai})(),
+                            device="cuda").cpu().numpy().view(np.uint64).copy()
+    g_dev = torch.as_tensor(type("C", (), {"__cuda_array_interface__": dict(
+        cai, shape=(int(r.n_finite),), data=(int(r.d_death_grade), False))})(),
+        device="cuda").cpu().numpy().view(np.uint64).copy()
+    dg, dl, sc = np.empty(n, np.uint64), np.empty(n), np.empty(int(r.n_scale))
+    nf, ess, ns, _ = ctx.run_host(np.asfortranarray(X), dg, dl, sc)
+    ctx.close()
+    assert ns == r.n_scale and nf == r.n_finite and ess == r.essential_count
+    assert np.array_equal(sc.view(np.uint64), D_dev)
+    assert np.array_equal(dg[:nf], g_dev)
+    bc = pkg.h0_barcode(X)  # the drop-in call, also bucketed at this size
+    assert np.array_equal(bc.scale.view(np.uint64), D_dev)
+    assert np.array_equal(bc.death_grade, g_dev)
