@@ -117,9 +117,15 @@ __global__ void __launch_bounds__(kUThreads, 3)
     __shared__ uint32_t s_warp_tot[kUWarps];
     __shared__ int s_own[2];
     __shared__ uint32_t s_ext_tot;
+    // kMode 1: run starts to fix, one per thread after the claims barrier (the claiming thread
+    // keeps any beyond kRunList: a tile's runs then cost one run of latency, not several)
+    constexpr uint32_t kRunList = kMode == 1 ? 512 : 1;
+    __shared__ uint32_t s_runs[kRunList];
+    __shared__ uint32_t s_nruns;
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     auto pre = [&](uint64_t kk) { return (kk - kmin) >> low_bits; };
     if (tid == 0) {
+        if (kMode == 1) s_nruns = 0;
         asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(u_smem(&s_bar[0])));
         asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(u_smem(&s_bar[1])));
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
@@ -232,23 +238,37 @@ __global__ void __launch_bounds__(kUThreads, 3)
                     }
                     const bool from_prev = st == 0 && tile_start > 0 && p == p_before;
                     if (first && !from_prev && st < tn) {
-                        claims |= 1u << j;
                         // the run's columns are loaded after the claims barrier: start
                         // bringing them into L1 now (their latency was ~35 % of this pass's
                         // stall samples, all threads waiting at the barrier behind it)
                         asm volatile("prefetch.global.L1 [%0];" ::"l"(vals + tile_start + st));
+                        const uint32_t slot = atomicAdd(&s_nruns, 1u);
+                        if (slot < kRunList)
+                            s_runs[slot] = st;
+                        else
+                            claims |= 1u << j;  // list full: this thread fixes it itself
                     }
                 }
                 starts = claims;
             }
             __syncthreads();  // every claim is made before any run is reordered
-            while (starts) {
-                const uint32_t j = (uint32_t)(__ffs(starts) - 1);
-                starts &= starts - 1;
-                const uint32_t inv = item_pos(j);
-                const uint64_t p = pre(s_k[inv]);
-                uint32_t i = inv - 1;  // prefixes never change: safe to re-walk while others fix
-                while (i > 0 && pre(s_k[i - 1]) == p) --i;
+            const uint32_t listed = s_nruns < kRunList ? s_nruns : kRunList;
+            bool mine = tid < listed;  // thread t fixes listed run t, then its own overflow
+            while (mine || starts) {
+                uint32_t i;
+                uint64_t p;
+                if (mine) {
+                    mine = false;
+                    i = s_runs[tid];
+                    p = pre(s_k[i]);
+                } else {
+                    const uint32_t j = (uint32_t)(__ffs(starts) - 1);
+                    starts &= starts - 1;
+                    const uint32_t inv = item_pos(j);
+                    p = pre(s_k[inv]);
+                    i = inv - 1;  // prefixes never change: safe to re-walk while others fix
+                    while (i > 0 && pre(s_k[i - 1]) == p) --i;
+                }
                 const uint64_t g = tile_start + i;
                 uint32_t len = 2;
                 while (i + len < staged && len <= kMaxRun && pre(s_k[i + len]) == p) ++len;
@@ -282,6 +302,7 @@ __global__ void __launch_bounds__(kUThreads, 3)
             }
             __syncthreads();
             if (tid == 0) {
+                s_nruns = 0;  // the run list is free again (next tile: after two barriers)
                 uint32_t st = 0;
                 if (tile_start > 0)
                     while (st < tn && pre(s_k[st]) == p_before) ++st;
