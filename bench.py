@@ -625,6 +625,19 @@ def main():
                 "alg_bytes_per_launch": alg_bytes, "avg_launch_ms": round(pass_ms, 4),
                 "passes": passes}
 
+    # K1's FP64 roofline (the second-largest kernel): FP64 instructions per edge counted from
+    # the SASS of k1_distance_tma (profiles/fp64_peak_r02.txt: 31.23 at d = 8), against the
+    # measured DADD/DMUL issue peak of this pool's B200s (tools/fp64_peak.cu)
+    k1 = None
+    if d == 8 and stage_sums.get("distance_ms"):
+        dms = stage_sums["distance_ms"] / args.steps
+        inst = 31.23 * k
+        k1 = {"kernel": "k1_distance_tma<8>", "bound": "fp64 (sqrt-sequence latency)",
+              "achieved": round(inst / (dms / 1e3) / 1e12, 2), "peak": 18.5,
+              "unit": "T FP64 instr/s", "frac": round(inst / (dms / 1e3) / 1e12 / 18.5, 3),
+              "inst_per_edge": 31.23, "avg_launch_ms": round(dms, 3),
+              "peak_source": "measured, profiles/fp64_peak_r02.txt"}
+
     cpu = None
     if rank == 0 and not args.no_cpu_baseline:
         cpu = cpu_baseline_record(cfg_name, n)
@@ -648,8 +661,8 @@ def main():
                     "d2h_bytes_per_step": d2h, "ms_per_step": e2e_ms / e2e_steps,
                     "steps": e2e_steps, "api": "ph0b_run_host (pinned host X, D, bars)", "check": e2e_check},
             "e2e_dropin": dropin,
-            "roofline": roofline, "cpu_baseline": cpu, "clocks": clk.summary(),
-            "gpu_launches": launches, "stage_ms": stage_ms,
+            "roofline": roofline, "roofline_k1": k1, "cpu_baseline": cpu,
+            "clocks": clk.summary(), "gpu_launches": launches, "stage_ms": stage_ms,
             "sort_passes": passes,
         }
         print(json.dumps(line), flush=True)

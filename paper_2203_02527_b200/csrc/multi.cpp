@@ -95,12 +95,10 @@ public:
     }
     ~MultiRunner() {
         for (auto& r : ranks_) {
-            if (r.dX) {
-                cudaSetDevice(r.device);
-                cudaFree(r.dX);
-            }
+            if (r.dX && cudaSetDevice(r.device) == cudaSuccess) cudaFree(r.dX);
             if (r.h) ph0b_context_destroy(r.h);
         }
+        cudaGetLastError();
     }
 
     int init() {
@@ -351,6 +349,15 @@ int run_multi_gpu(const std::vector<int>& devices, const double* X, uint64_t n, 
                   uint64_t* n_finite, uint64_t* essential, double* scale,
                   uint64_t scale_capacity, uint64_t* n_scale, ph0b_stage_times* times) {
     std::lock_guard<std::mutex> lk(g_runners_mu);  // one multi-GPU run at a time
+    struct DeviceGuard {  // the caller's current device is left as it was
+        int dev = 0;
+        DeviceGuard() {
+            if (cudaGetDevice(&dev) != cudaSuccess) cudaGetLastError();
+        }
+        ~DeviceGuard() {
+            if (cudaSetDevice(dev) != cudaSuccess) cudaGetLastError();
+        }
+    } device_guard;
     auto& slot = runners()[devices];
     if (!slot) slot = std::make_unique<MultiRunner>(devices);
     int rc = slot->run(X, n, d, layout, death_grade, death_length, n_finite, essential, scale,

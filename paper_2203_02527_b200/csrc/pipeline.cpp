@@ -178,7 +178,12 @@ NvtxRange::~NvtxRange() { nvtxRangePop(); }
 Context::Context(int device) : device_(device) {}
 
 Context::~Context() {
-    cudaSetDevice(device_);
+    // (a context whose init() failed may name an invalid device: leave no error behind for
+    // the next, unrelated CUDA call of this thread to report)
+    if (cudaSetDevice(device_) != cudaSuccess) {
+        cudaGetLastError();
+        return;
+    }
     void* ps[] = {xin_,  xpad_, keys_[0], keys_[1], vals_[0], vals_[1], status_,
                   grade_, comp_, best_, surv_, surv_sorted_, lows_, cand_[0], cand_[1],
                   survkeys_[0], survkeys_[1], death_grade_, death_length_, hist_, counters_,
@@ -203,6 +208,7 @@ Context::~Context() {
     for (auto& e : ev_)
         if (e) cudaEventDestroy(e);
     if (stream_) cudaStreamDestroy(stream_);
+    cudaGetLastError();
 }
 
 Status Context::init() {
