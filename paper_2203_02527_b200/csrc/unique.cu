@@ -116,7 +116,6 @@ __global__ void __launch_bounds__(kUThreads, 3)
     __shared__ __align__(8) uint64_t s_bar[2];
     __shared__ uint32_t s_warp_tot[kUWarps];
     __shared__ int s_own[2];
-    __shared__ uint32_t s_ext_tot;
     // kMode 1: run starts to fix, one per thread after the claims barrier (the claiming thread
     // keeps any beyond kRunList: a tile's runs then cost one run of latency, not several)
     constexpr uint32_t kRunList = kMode == 1 ? 512 : 1;
@@ -197,6 +196,7 @@ __global__ void __launch_bounds__(kUThreads, 3)
         }
 
         uint32_t os = 0, oe = tn;
+        uint32_t ext_tot = 0;  // (kMode 1, thread 0)
         if (kMode == 2) {
             os = (uint32_t)ow.x;
             oe = (uint32_t)ow.y;
@@ -251,6 +251,24 @@ __global__ void __launch_bounds__(kUThreads, 3)
                 }
                 starts = claims;
             }
+            if (tid == kUThreads - 1) {
+                // the owned range depends on prefixes only, which the fix-ups never change:
+                // it is found here, beside the claims, not serially after the fix-ups
+                uint32_t st = 0;
+                if (tile_start > 0)
+                    while (st < tn && pre(s_k[st]) == p_before) ++st;
+                uint32_t e = tn;
+                if (e > st && e < staged) {
+                    const uint64_t pl = pre(s_k[e - 1]);
+                    while (e < staged && pre(s_k[e]) == pl) ++e;
+                }
+                // this tile's last run runs past the staged window: its end (and the next
+                // tile's first owned position) is not visible here — sorted or not, redo
+                if (st < tn && e == staged && ext_end < count) atomicOr(redo, 1u);
+                if (st >= tn) st = e = tn;
+                s_own[0] = (int)st;
+                s_own[1] = (int)e;
+            }
             __syncthreads();  // every claim is made before any run is reordered
             const uint32_t listed = s_nruns < kRunList ? s_nruns : kRunList;
             bool mine = tid < listed;  // thread t fixes listed run t, then its own overflow
@@ -300,30 +318,14 @@ __global__ void __launch_bounds__(kUThreads, 3)
                     vals[g + a] = lv[a];
                 }
             }
-            __syncthreads();
-            if (tid == 0) {
-                s_nruns = 0;  // the run list is free again (next tile: after two barriers)
-                uint32_t st = 0;
-                if (tile_start > 0)
-                    while (st < tn && pre(s_k[st]) == p_before) ++st;
-                uint32_t e = tn;
-                if (e > st && e < staged) {
-                    const uint64_t pl = pre(s_k[e - 1]);
-                    while (e < staged && pre(s_k[e]) == pl) ++e;
-                }
-                // this tile's last run runs past the staged window: its end (and the next
-                // tile's first owned position) is not visible here — sorted or not, redo
-                if (st < tn && e == staged && ext_end < count) atomicOr(redo, 1u);
-                if (st >= tn) st = e = tn;
-                uint32_t ext = 0;
-                for (uint32_t g = tn; g < e; ++g) ext += s_k[g] != s_k[g - 1] ? 1u : 0u;
-                s_own[0] = (int)st;
-                s_own[1] = (int)e;
-                s_ext_tot = ext;
-            }
-            __syncthreads();
+            __syncthreads();  // runs fixed; the owned range is in s_own
             os = (uint32_t)s_own[0];
             oe = (uint32_t)s_own[1];
+            if (tid == 0) {
+                s_nruns = 0;  // the run list is free again (next tile: after two barriers)
+                // distinct lengths of this tile's last run past the tile end (fixed keys)
+                for (uint32_t g = tn; g < oe; ++g) ext_tot += s_k[g] != s_k[g - 1] ? 1u : 0u;
+            }
         }
 
         // ---- flags and counts (keys from shared memory) ------------------------------------
@@ -349,7 +351,7 @@ __global__ void __launch_bounds__(kUThreads, 3)
         }
         if (kMode == 1) {  // counts and owned range of this tile for the scan
             if (tid == 0) {
-                tile_counts[tile] = main_tot + (low_bits ? s_ext_tot : 0u);
+                tile_counts[tile] = main_tot + ext_tot;
                 tile_own[tile] = make_int2((int)os, (int)oe);
             }
             continue;  // (the loop-top barrier orders the buffer reuse)
