@@ -254,6 +254,7 @@ public:
         // ---- the column reduction continues the forest from range to range ------------------
         uint32_t found = 0;
         const uint32_t need = n >= 1 ? (uint32_t)(n - 1) : 0;
+        int last = -1;  // the last rank that reduced (ranks with an empty range are skipped)
         for (uint32_t i = 0; i < P; ++i) {
             Rank& r = ranks_[i];
             r.m = 0;
@@ -263,8 +264,8 @@ public:
             cudaSetDevice(r.device);
             cudaStream_t st = c->own_stream();
             const uint32_t* init = nullptr;
-            if (found > 0) {  // continue rank i-1's forest: its labels, copied peer to peer
-                const Rank& p = ranks_[i - 1];
+            if (last >= 0) {  // continue that rank's forest: its labels, copied peer to peer
+                const Rank& p = ranks_[last];
                 if (cudaMemcpyPeerAsync(c->lows_buffer(), r.device, p.ctx()->comp(), p.device,
                                         n * 4, st) != cudaSuccess)
                     return capi_fail(PH0B_ERR_CUDA, "peer copy of the forest labels");
@@ -282,6 +283,7 @@ public:
             launches += c->launches;
             r.m = rst.survivors;
             found += rst.survivors;
+            last = (int)i;
         }
         if (found != need)
             return capi_fail(PH0B_ERR_CUDA, "internal error: reduction produced " +

@@ -3,6 +3,8 @@ oracle (oracle/ph0_oracle.c, pinned to the reference): the drop-in call, the con
 path, the multi-GPU path (virtual ranks), the reduced supports and the GPU Kruskal barcode.
 Shapes mix uniform / clustered / lattice / duplicated / tiny-scale points, N across the sort
 and distance tile boundaries, d in 1..20."""
+import os
+
 import numpy as np
 import pytest
 
@@ -38,7 +40,8 @@ def cloud(seed):
     return X
 
 
-@pytest.mark.parametrize("seed", range(36))
+# PH0B_FUZZ_SEEDS widens the sweep for soak runs (profiles/fuzz_soak_r02.log)
+@pytest.mark.parametrize("seed", range(int(os.environ.get("PH0B_FUZZ_SEEDS", "36"))))
 def test_random_cloud_all_entry_points(seed):
     X = cloud(seed)
     n = X.shape[0]

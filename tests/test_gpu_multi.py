@@ -53,6 +53,22 @@ def test_far_clusters_forest_continues_across_ranges():
     assert np.array_equal(bits(bc.scale), bits(ref["scale"]))
 
 
+@pytest.mark.parametrize("values,ranks", [(5, 4), (5, 8), (2, 3), (3, 8)])
+def test_fewer_lengths_than_ranks(values, ranks):
+    """A 1-D lattice with a handful of coordinates has fewer distinct lengths than ranks, so
+    some key ranges are empty (the splitters coincide); the forest must continue from the
+    last rank that reduced, not from an empty neighbour (fuzz seed 416 found this)."""
+    rng = np.random.default_rng(values * 10 + ranks)
+    for n in (300, 1000):
+        X = rng.integers(0, values, size=(n, 1)).astype(np.float64)
+        ref = ob.oracle_filtration_and_bars(X)
+        bc = pkg.h0_barcode(X, devices=[0] * ranks)
+        assert bc.essential_count == ref["essential"]
+        assert np.array_equal(bc.death_grade, ref["death_grade"])
+        assert np.array_equal(bits(bc.death_length), bits(ref["death_length"]))
+        assert np.array_equal(bits(bc.scale), bits(ref["scale"]))
+
+
 def test_small_clouds_take_single_gpu_path():
     for n in (0, 1, 2, 5, 40):
         X = np.random.default_rng(n).normal(size=(n, 2))
