@@ -106,3 +106,49 @@ def test_bucketed_host_path_vs_device_path(kind):
     bc = pkg.h0_barcode(X)  # the drop-in call, also bucketed at this size
     assert np.array_equal(bc.scale.view(np.uint64), D_dev)
     assert np.array_equal(bc.death_grade, g_dev)
+
+
+def edge_cloud(seed):
+    """Edge shapes: a handful of coordinates (fewer distinct lengths than ranks), coordinates
+    whose differences overflow (lengths of +inf), signed zeros, d beyond the TMA/register
+    paths, N at the sort-tile boundaries (K = 4095/4096/4097 ... at N = 91/92)."""
+    rng = np.random.default_rng(10_000 + seed)
+    kind = seed % 5
+    if kind == 0:  # 1..3 coordinate values
+        n = int(rng.choice([40, 91, 92, 300, 1500]))
+        X = rng.integers(0, 1 + seed % 3, size=(n, int(rng.integers(1, 4)))).astype(np.float64)
+    elif kind == 1:  # overflow: some squared differences are +inf
+        n = int(rng.choice([50, 200, 700]))
+        X = rng.uniform(-1, 1, size=(n, 2)) * 1e154
+        X[rng.integers(0, n, max(1, n // 10))] *= 1e154
+    elif kind == 2:  # signed zeros and exact duplicates
+        n = int(rng.choice([64, 129, 1000]))
+        X = rng.choice([-0.0, 0.0, 1.0, -1.0], size=(n, int(rng.integers(1, 5))))
+    elif kind == 3:  # high d: shared-memory / generic distance paths
+        n = int(rng.choice([91, 92, 257, 1025]))
+        X = rng.normal(size=(n, int(rng.integers(21, 65))))
+    else:  # N around the tile sizes, mixed scales
+        n = int(rng.choice([90, 91, 92, 93, 127, 128, 129, 181, 182, 2897, 2898]))
+        X = rng.normal(size=(n, 3)) * 10.0 ** rng.integers(-5, 6, size=(n, 1))
+    return X
+
+
+@pytest.mark.parametrize("seed", range(int(os.environ.get("PH0B_FUZZ_EDGE", "20"))))
+def test_edge_clouds_all_entry_points(seed):
+    X = edge_cloud(seed)
+    n = X.shape[0]
+    ref = ob.oracle_filtration_and_bars(X, reduction_limit=1000)
+    for bc in (pkg.h0_barcode(X), pkg.h0_barcode(X, devices=[0] * (2 + seed % 7))):
+        assert bc.essential_count == ref["essential"]
+        assert np.array_equal(bc.death_grade, ref["death_grade"])
+        assert np.array_equal(bits(bc.death_length), bits(ref["death_length"]))
+        assert np.array_equal(bits(bc.scale), bits(ref["scale"]))
+    ctx = pkg.Context(0)
+    dg, dl, sc = np.empty(n, np.uint64), np.empty(n), np.empty(max(len(ref["scale"]), 1))
+    nf, ess, ns, _ = ctx.run_host(np.ascontiguousarray(X), dg, dl, sc, layout=pkg.ph0b.ROW_MAJOR)
+    ctx.close()
+    assert nf == len(ref["death_grade"]) and ess == ref["essential"]
+    assert np.array_equal(bits(sc[:ns]), bits(ref["scale"]))
+    kr = pkg.kruskal_barcode(X, return_scale=False)
+    assert np.array_equal(kr.death_grade, ref["death_grade"])
+    pkg.lib().ph0b_release_resources()
