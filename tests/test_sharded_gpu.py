@@ -46,7 +46,7 @@ def run_virtual(X, parts):
 
 @pytest.mark.parametrize("exchange", ["peer", "collective"])
 @pytest.mark.parametrize("parts", [1, 2, 3, 4])
-@pytest.mark.parametrize("cloud", ["C2", "lattice", "C1"])
+@pytest.mark.parametrize("cloud", ["C2", "lattice", "C1", "fewvals"])
 def test_virtual_ranks_match_oracle(parts, cloud, exchange, monkeypatch):
     """exchange='peer': the partition kernel of each virtual rank stores its parts straight
     into the other ranks' receive buffers (the peer-memory path; here all on one device);
@@ -54,6 +54,8 @@ def test_virtual_ranks_match_oracle(parts, cloud, exchange, monkeypatch):
     monkeypatch.setenv("PH0B_EXCHANGE", exchange)
     if cloud == "lattice":
         X = np.array([[x, y] for x in range(24) for y in range(24)], np.float64)
+    elif cloud == "fewvals":  # 3 distinct lengths: key ranges of some ranks are empty
+        X = np.random.default_rng(3).integers(0, 3, size=(300, 1)).astype(np.float64)
     elif cloud == "C2":
         X = pkg.config_cloud("C2", 900)
     else:
