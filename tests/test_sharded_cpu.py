@@ -77,6 +77,21 @@ def test_sharded_orchestration_matches_oracle(world, exchange):
     assert sum(r[6] for r in res) == X.shape[0] * (X.shape[0] - 1) // 2
 
 
+def test_sharded_empty_key_ranges():
+    """Two distinct lengths and three ranks: at least one rank's key range is empty, and the
+    forest must pass through it unchanged (world_size 3 over gloo)."""
+    import oracle_bridge as ob
+
+    X = np.random.default_rng(5).integers(0, 2, size=(80, 1)).astype(np.float64)
+    res = run_world(X, 3)
+    ref = ob.oracle_filtration_and_bars(X)
+    D = np.concatenate([r[2] for r in res])
+    assert np.array_equal(D.view(np.uint64), ref["scale"].view(np.uint64))
+    assert np.array_equal(res[0][3], ref["death_grade"])
+    assert res[0][5] == ref["essential"]
+    assert min(len(r[2]) for r in res) == 0  # the case this test is about
+
+
 def test_row_ranges_balanced():
     from paper_2203_02527_b200.sharded import row_ranges
     for n, p in ((10, 3), (1000, 8), (65536, 8), (5, 8)):
