@@ -151,4 +151,13 @@ def test_edge_clouds_all_entry_points(seed):
     assert np.array_equal(bits(sc[:ns]), bits(ref["scale"]))
     kr = pkg.kruskal_barcode(X, return_scale=False)
     assert np.array_equal(kr.death_grade, ref["death_grade"])
+    # the filtration surfaces: u-major lengths, the sorted columns with grades, claimed lows
+    f = ob.filtration(X)
+    assert np.array_equal(bits(pkg.pairwise_distances(X)), bits(ob.pairwise(X)))
+    u, v, g, scale = pkg.build_filtration(X)
+    assert np.array_equal(u, f["u"]) and np.array_equal(v, f["v"])
+    assert np.array_equal(g, f["grade"]) and np.array_equal(bits(scale), bits(f["scale"]))
+    if n >= 2:  # (the claimed low of a surviving column is its reduced support's high row)
+        sp = ob.reduce_sparse(f, stop_at_spanning=True)
+        assert np.array_equal(pkg.claimed_lows(X), sp["rows_hi"])
     pkg.lib().ph0b_release_resources()
