@@ -608,6 +608,7 @@ int ph0b_pairwise_distances(const double* X, uint64_t n, uint64_t d, uint32_t la
     Opts o;
     int rc = parse(opt, n, layout, &o);
     if (rc) return rc;
+    if (n >= 2 && !lengths) return fail(PH0B_ERR_INVALID_ARGUMENT, "null output");
     if (n * d && !X) return fail(PH0B_ERR_INVALID_ARGUMENT, "null point cloud");
     if (!all_finite(X, n * d))
         return fail(PH0B_ERR_NONFINITE, "point cloud contains non-finite coordinates");

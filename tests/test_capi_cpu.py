@@ -202,3 +202,16 @@ def test_release_functions_callable_without_gpu():
     L.ph0b_host_cache_trim()
     L.ph0b_release_resources()
     L.ph0b_scale_release(None)
+
+
+def test_null_outputs_rejected_before_any_device_work():
+    import ctypes as C
+    L = pkg.lib()
+    X = np.zeros((3, 2))
+    o = ph0b.Options(C.sizeof(ph0b.Options), 0, 0, 1, 1)
+    for fn, args in ((L.ph0b_pairwise_distances, (None,)),
+                     (L.ph0b_claimed_lows, (None, None)),
+                     (L.ph0b_reduced_supports, (None, None, None, None))):
+        rc = fn(C.c_void_p(X.ctypes.data), 3, 2, ph0b.COL_MAJOR, C.byref(o), *args)
+        assert rc == ph0b.PH0B_ERR_INVALID_ARGUMENT
+        assert b"null output" in L.ph0b_last_error()
