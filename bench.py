@@ -537,7 +537,10 @@ def main():
     def run_e2e():
         return ctx.run_host(Xh, dg.array, dl.array, sc.array, stream=stream.cuda_stream)
 
-    run_e2e()
+    # W untimed calls, like the device path (the context also settles its D2H ring geometry
+    # here: pipeline.cpp ring_choice())
+    for _ in range(max(1, args.warmup)):
+        run_e2e()
     barrier()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     e0.record(stream)
@@ -591,7 +594,8 @@ def main():
             L.ph0b_result_free(C.byref(res))
             return out, ok
 
-        dropin_step()  # warm: sizes the context, faults in the cached result buffer once
+        for _ in range(max(1, args.warmup)):  # warm: sizes the context, faults in the cached
+            dropin_step()                     # result buffer once, settles the ring geometry
         t0 = time.perf_counter()
         oks = []
         for _ in range(e2e_steps):

@@ -97,23 +97,33 @@ uint64_t d2h_chunk_elems() {
     return v;
 }
 
-// Streamed D2H ring of the compressed host path: PH0B_RING_SLOTS slots (default 10) of
-// PH0B_RING_CHUNKS 1024-value packed chunks (<= 8 MiB at the default 2048), filled on
-// PH0B_RING_STREAMS copy streams (default 2) and decoded by PH0B_RING_SUBTASKS pool tasks
-// per piece (default 32).  8 MiB copies keep the per-copy and stream-memop overheads below
-// 5 % of the PCIe time (tools/ring_bench.cu); the 80 MiB ring replaces a k*4-byte pinned
-// staging buffer (8.6 GB at C5).  Measured sweeps: tools/ring_sweep.sh, DESIGN.md.
-uint32_t ring_piece_chunks() {  // 1024-value packed chunks per piece
-    static const uint32_t v = [] {
-        const char* e = getenv("PH0B_RING_CHUNKS");
-        const int x = e ? atoi(e) : 2048;
-        return (uint32_t)(x < 1 ? 1 : (x > 16384 ? 16384 : x));
-    }();
+// Streamed D2H ring of the compressed host path: slots of packed 1024-value chunks, filled on
+// PH0B_RING_STREAMS copy streams (default 2) and decoded by PH0B_RING_SUBTASKS pool tasks per
+// piece (default 32); a ring of tens of MiB replaces a k*4-byte pinned staging buffer (8.6 GB
+// at C5).  Two geometries, chosen per context by measurement (ring_choice()): 10 slots of
+// 8 MiB pieces (2048 chunks) and 16 slots of 2 MiB pieces (512 chunks).  Which one is faster
+// depends on the box (C5 e2e, tools/box_probe.sh, same CPU model, L3 and host-memory
+// bandwidth everywhere): on most boxes of the pool 16 x 2 MiB gives 224-228 ms against
+// 237-267 ms, on others 10 x 8 MiB gives 184-194 ms against 225-227.  PH0B_RING_CHUNKS /
+// PH0B_RING_SLOTS fix a geometry (tools/ring_sweep.sh), PH0B_RING_TUNE=0 fixes the first.
+constexpr uint32_t kRingGeom[2][2] = {{2048, 10}, {512, 16}};  // {chunks per piece, slots}
+
+int env_ring(const char* name, int lo, int hi) {  // 0 = unset
+    const char* e = getenv(name);
+    if (!e) return 0;
+    const int x = atoi(e);
+    return x < lo ? lo : (x > hi ? hi : x);
+}
+
+bool ring_fixed() {
+    static const bool v = env_ring("PH0B_RING_CHUNKS", 1, 16384) ||
+                          env_ring("PH0B_RING_SLOTS", 2, 256) ||
+                          (getenv("PH0B_RING_TUNE") && getenv("PH0B_RING_TUNE")[0] == '0');
     return v;
 }
 
-uint64_t ring_slot_bytes() {  // a piece at 4 bytes per value + slack for the decoder's reads
-    return (uint64_t)ring_piece_chunks() * kPackChunk * 4 + 128;
+uint64_t ring_slot_bytes(uint32_t g) {  // a piece at 4 bytes per value + slack for the decoder
+    return (uint64_t)g * kPackChunk * 4 + 128;
 }
 
 uint32_t ring_subtasks() {
@@ -121,15 +131,6 @@ uint32_t ring_subtasks() {
         const char* e = getenv("PH0B_RING_SUBTASKS");
         const int x = e ? atoi(e) : 32;
         return (uint32_t)(x < 1 ? 1 : (x > 256 ? 256 : x));
-    }();
-    return v;
-}
-
-uint32_t ring_slots() {
-    static const uint32_t v = [] {
-        const char* e = getenv("PH0B_RING_SLOTS");
-        const int x = e ? atoi(e) : 10;
-        return (uint32_t)(x < 2 ? 2 : (x > 256 ? 256 : x));
     }();
     return v;
 }
@@ -245,7 +246,7 @@ Status Context::init() {
 }
 
 Status Context::ensure_ring() {
-    const uint64_t need = (uint64_t)ring_slots() * ring_slot_bytes();
+    const uint64_t need = (uint64_t)ring_r_ * ring_slot_bytes(ring_g_);
     Status s = grow_host(reinterpret_cast<void**>(&h_ring_), &h_ring_cap_, need);
     if (!s.good()) return s;
     if (!h_ringflags_) {
@@ -701,7 +702,7 @@ Status Context::prepare_stream(uint64_t k, uint32_t B) {
     // (<= 4 per value + slack), chunk bases, widths, offsets (device) and offsets within
     // a piece; pinned mirrors of the per-chunk metadata; mapped piece boundaries
     const uint64_t chunks = k / kPackChunk + B + 64;
-    const uint64_t pieces = chunks / ring_piece_chunks() + B + 2;
+    const uint64_t pieces = chunks / ring_g_ + B + 2;
     if (!(s = grow(reinterpret_cast<void**>(&d_delta_), &d_delta_cap_,
                    chunks * kPackChunk * 4 + 64 * B)).good() ||
         !(s = grow(reinterpret_cast<void**>(&d_cbase_), &d_cbase_cap_, chunks * 8)).good() ||
@@ -763,7 +764,7 @@ Status Context::enqueue_stream(uint64_t cbase, uint64_t nch, const std::vector<u
                                const uint8_t* d_src, const volatile uint64_t* bounds,
                                cudaEvent_t meta_ev, double* host_scale, uint64_t capacity,
                                volatile int* overflow, uint64_t* moved, uint64_t* enq_ns) {
-    const uint32_t G = ring_piece_chunks(), R = ring_slots(), NS = ring_subtasks();
+    const uint32_t G = ring_g_, R = ring_r_, NS = ring_subtasks();
     const uint64_t npieces = poffs.size() - 1;
     cudaStream_t cs = copy_stream_;
     PH0B_TRY(cudaStreamWaitEvent(cs, enc_ev_, 0), "wait");
@@ -787,7 +788,7 @@ Status Context::enqueue_stream(uint64_t cbase, uint64_t nch, const std::vector<u
         const uint32_t slot = (uint32_t)(ring_seq_ % R);
         const uint32_t gen = (uint32_t)(ring_seq_ / R + 1);
         ++ring_seq_;
-        uint8_t* ring = reinterpret_cast<uint8_t*>(h_ring_) + (uint64_t)slot * ring_slot_bytes();
+        uint8_t* ring = reinterpret_cast<uint8_t*>(h_ring_) + (uint64_t)slot * ring_slot_bytes(G);
         const auto e0 = std::chrono::steady_clock::now();
         if (!stream_wait_u32(cs, reinterpret_cast<uint64_t>(d_ringflags_ + R + slot), gen - 1))
             return {PH0B_ERR_CUDA, "D2H ring: stream wait failed"};
@@ -838,10 +839,11 @@ Status Context::stream_scale(const double* d_scale, uint64_t n, double* host_sca
     if (!copy_stream_) PH0B_TRY(cudaStreamCreateWithFlags(&copy_stream_, cudaStreamNonBlocking),
                                 "cudaStreamCreate");
     Trace tr;
+    if (!ring_g_) ring_choice(0);  // (a geometry is set before the first prepare_stream)
     Status s = prepare_stream(n, 1);
     if (!s.good()) return s;
     tr.mark("stream_scale: prepared");
-    const uint32_t G = ring_piece_chunks();
+    const uint32_t G = ring_g_;
     volatile int overflow = 0;
     struct PoolGuard {
         DecodePool* p;
@@ -890,7 +892,67 @@ Status Context::stream_scale(const double* d_scale, uint64_t n, double* host_sca
     return Status::ok();
 }
 
+void Context::set_ring_geometry(uint32_t g, uint32_t r) {
+    if (g == ring_g_ && r == ring_r_) return;
+    ring_g_ = g;
+    ring_r_ = r;
+    // no copy or decode of an earlier call is outstanding here: restart the slot generations
+    if (h_ringflags_) std::memset(h_ringflags_, 0, 512 * 4);
+    ring_seq_ = 0;
+    for (auto& x : ring_done_) x.store(0);
+}
+
+// The ring geometry for a host-path call over k edges (and sets it): the first call of a
+// size runs geometry 0 unmeasured (first-touch and allocation costs), the second is timed
+// with geometry 0, the third with geometry 1, and every later call keeps the faster.
+int Context::ring_choice(uint64_t k) {
+    if (ring_fixed()) {
+        const int g = env_ring("PH0B_RING_CHUNKS", 1, 16384);
+        const int r = env_ring("PH0B_RING_SLOTS", 2, 256);
+        set_ring_geometry(g ? (uint32_t)g : kRingGeom[0][0], r ? (uint32_t)r : kRingGeom[0][1]);
+        return -1;
+    }
+    int c = ring_pick_;
+    if (c < 0) {
+        if (k && k != ring_tune_k_) {
+            ring_tune_k_ = k;
+            ring_calls_ = 0;
+        }
+        c = (k && ring_calls_ >= 2) ? 1 : 0;
+    }
+    set_ring_geometry(kRingGeom[c][0], kRingGeom[c][1]);
+    return k ? c : -1;
+}
+
+void Context::ring_record(uint64_t k, double ms) {
+    if (ring_pick_ >= 0 || k != ring_tune_k_) return;
+    if (ring_calls_ == 1) ring_ms_[0] = ms;
+    if (ring_calls_ == 2) {
+        ring_ms_[1] = ms;
+        ring_pick_ = ring_ms_[1] < ring_ms_[0] ? 1 : 0;
+        if (getenv("PH0B_TRACE"))
+            fprintf(stderr, "[ph0b trace] D2H ring: %u x %u chunks %.1f ms, %u x %u chunks %.1f ms"
+                    " -> %u x %u\n", kRingGeom[0][1], kRingGeom[0][0], ring_ms_[0],
+                    kRingGeom[1][1], kRingGeom[1][0], ring_ms_[1], kRingGeom[ring_pick_][1],
+                    kRingGeom[ring_pick_][0]);
+    }
+    ++ring_calls_;
+}
+
 Status Context::run_host_overlapped(const double* X, uint64_t n, uint64_t d, uint32_t layout,
+                                    cudaStream_t st, double* host_scale,
+                                    uint64_t scale_capacity, RunOutputs* out) {
+    const uint64_t k = n * (n - (n > 0)) / 2;
+    const int c = ring_choice(k);
+    const auto t0 = std::chrono::steady_clock::now();
+    Status s = run_host_overlapped_impl(X, n, d, layout, st, host_scale, scale_capacity, out);
+    if (s.good() && c >= 0)
+        ring_record(k, std::chrono::duration<double, std::milli>(
+                           std::chrono::steady_clock::now() - t0).count());
+    return s;
+}
+
+Status Context::run_host_overlapped_impl(const double* X, uint64_t n, uint64_t d, uint32_t layout,
                                     cudaStream_t st, double* host_scale, uint64_t scale_capacity,
                                     RunOutputs* out) {
     NvtxRange nvtx_("ph0b pipeline (host, bucketed D stream)");
@@ -1002,7 +1064,7 @@ Status Context::run_host_overlapped(const double* X, uint64_t n, uint64_t d, uin
     //    slice bounds from device words and the copies are sized by the bucket's edge count
     //    (an upper bound of its |D|), so bucket b's copies are enqueued while bucket b+1 sorts.
     //  * uncompressed: plain D2H of the slice in medium chunks once the bucket is sorted.
-    const uint32_t G = ring_piece_chunks();
+    const uint32_t G = ring_g_;
     std::vector<uint64_t> nch_ub(B), cb(B + 1, 0), rb(B + 1, 0);
     for (uint32_t b = 0; b < B; ++b) {
         nch_ub[b] = (tot[b] + kPackChunk - 1) / kPackChunk;

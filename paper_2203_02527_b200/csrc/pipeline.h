@@ -92,6 +92,9 @@ public:
     // Host-output run with the D2H of D overlapped with the sort: edges are split into
     // key-range buckets (one stable partition pass), each bucket is sorted + deduplicated
     // in turn and its slice of D streams to the host while the next bucket sorts.
+    Status run_host_overlapped_impl(const double* X, uint64_t n, uint64_t d, uint32_t layout,
+                                    cudaStream_t stream, double* host_scale,
+                                    uint64_t scale_capacity, RunOutputs* out);
     Status run_host_overlapped(const double* X, uint64_t n, uint64_t d, uint32_t layout,
                                cudaStream_t st, double* host_scale, uint64_t scale_capacity,
                                RunOutputs* out);
@@ -176,6 +179,15 @@ private:
     uint32_t* d_ringflags_ = nullptr;
     uint64_t ring_seq_ = 0;
     std::atomic<uint64_t> ring_done_[256] = {};  // per slot: decode tasks completed (monotone)
+    // ring geometry (1024-value chunks per piece, slots) of this call, and its per-context
+    // choice between the two measured geometries (ring_geometry(), pipeline.cpp)
+    uint32_t ring_g_ = 0, ring_r_ = 0;
+    int ring_calls_ = 0, ring_pick_ = -1;
+    uint64_t ring_tune_k_ = 0;
+    double ring_ms_[2] = {0.0, 0.0};
+    void set_ring_geometry(uint32_t g, uint32_t r);
+    int ring_choice(uint64_t k);
+    void ring_record(uint64_t k, double ms);
     cudaEvent_t enc_ev_ = nullptr;
     std::vector<cudaStream_t> ring_streams_;  // [0] = copy_stream_
     Status ensure_ring();
