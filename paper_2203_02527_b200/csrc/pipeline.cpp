@@ -902,9 +902,11 @@ void Context::set_ring_geometry(uint32_t g, uint32_t r) {
     for (auto& x : ring_done_) x.store(0);
 }
 
-// The ring geometry for a host-path call over k edges (and sets it): the first call of a
-// size runs geometry 0 unmeasured (first-touch and allocation costs), the second is timed
-// with geometry 0, the third with geometry 1, and every later call keeps the faster.
+// The ring geometry for a host-path call over k edges (and sets it).  Calls of one size: the
+// first runs geometry 0 unmeasured (allocation and first-touch costs), the 2nd and 4th are
+// timed with geometry 0, the 3rd with geometry 1 — compared only when all three moved the
+// same D (same edge count and |D|; otherwise the timing restarts) — and every later call keeps
+// the faster (geometry 0's better time against geometry 1's: one slow call does not decide).
 int Context::ring_choice(uint64_t k) {
     if (ring_fixed()) {
         const int g = env_ring("PH0B_RING_CHUNKS", 1, 16384);
@@ -918,17 +920,23 @@ int Context::ring_choice(uint64_t k) {
             ring_tune_k_ = k;
             ring_calls_ = 0;
         }
-        c = (k && ring_calls_ >= 2) ? 1 : 0;
+        c = (k && ring_calls_ == 2) ? 1 : 0;
     }
     set_ring_geometry(kRingGeom[c][0], kRingGeom[c][1]);
     return k ? c : -1;
 }
 
-void Context::ring_record(uint64_t k, double ms) {
+void Context::ring_record(uint64_t k, uint64_t n_scale, double ms) {
     if (ring_pick_ >= 0 || k != ring_tune_k_) return;
-    if (ring_calls_ == 1) ring_ms_[0] = ms;
-    if (ring_calls_ == 2) {
+    if (ring_calls_ == 1) {
+        ring_ms_[0] = ms;
+        ring_tune_d_ = n_scale;
+    } else if (n_scale != ring_tune_d_) {  // another cloud: this call counts as a first one
+        ring_calls_ = 0;
+    } else if (ring_calls_ == 2) {
         ring_ms_[1] = ms;
+    } else if (ring_calls_ == 3) {
+        ring_ms_[0] = std::min(ring_ms_[0], ms);
         ring_pick_ = ring_ms_[1] < ring_ms_[0] ? 1 : 0;
         if (getenv("PH0B_TRACE"))
             fprintf(stderr, "[ph0b trace] D2H ring: %u x %u chunks %.1f ms, %u x %u chunks %.1f ms"
@@ -947,8 +955,8 @@ Status Context::run_host_overlapped(const double* X, uint64_t n, uint64_t d, uin
     const auto t0 = std::chrono::steady_clock::now();
     Status s = run_host_overlapped_impl(X, n, d, layout, st, host_scale, scale_capacity, out);
     if (s.good() && c >= 0)
-        ring_record(k, std::chrono::duration<double, std::milli>(
-                           std::chrono::steady_clock::now() - t0).count());
+        ring_record(k, out ? out->n_scale : 0, std::chrono::duration<double, std::milli>(
+                                         std::chrono::steady_clock::now() - t0).count());
     return s;
 }
 

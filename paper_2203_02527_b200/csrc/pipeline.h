@@ -183,11 +183,11 @@ private:
     // choice between the two measured geometries (ring_geometry(), pipeline.cpp)
     uint32_t ring_g_ = 0, ring_r_ = 0;
     int ring_calls_ = 0, ring_pick_ = -1;
-    uint64_t ring_tune_k_ = 0;
+    uint64_t ring_tune_k_ = 0, ring_tune_d_ = 0;
     double ring_ms_[2] = {0.0, 0.0};
     void set_ring_geometry(uint32_t g, uint32_t r);
     int ring_choice(uint64_t k);
-    void ring_record(uint64_t k, double ms);
+    void ring_record(uint64_t k, uint64_t n_scale, double ms);
     cudaEvent_t enc_ev_ = nullptr;
     std::vector<cudaStream_t> ring_streams_;  // [0] = copy_stream_
     Status ensure_ring();

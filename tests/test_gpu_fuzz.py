@@ -161,3 +161,28 @@ def test_edge_clouds_all_entry_points(seed):
         sp = ob.reduce_sparse(f, stop_at_spanning=True)
         assert np.array_equal(pkg.claimed_lows(X), sp["rows_hi"])
     pkg.lib().ph0b_release_resources()
+
+
+def test_host_path_ring_geometry_switch_same_context():
+    """One context, five bucketed host-path calls: the 3rd runs the other D2H ring geometry
+    (the ring's slot generations restart at each change), the 5th the faster.  Every call's D
+    and bars must be identical."""
+    rng = np.random.default_rng(99)
+    n = 12000  # K = 7.2e7 >= 2^26: the bucketed, D-streaming path
+    X = rng.normal(size=(n, 3)) + 40.0 * rng.integers(0, 3, size=(n, 1))
+    ctx = pkg.Context(0)
+    first = None
+    for _ in range(5):
+        dg, dl, sc = np.empty(n, np.uint64), np.empty(n), np.empty(n * (n - 1) // 2)
+        nf, ess, ns, _ = ctx.run_host(np.asfortranarray(X), dg, dl, sc)
+        cur = (nf, ess, ns, dg[:nf].copy(), dl[:nf].view(np.uint64).copy(),
+               sc[:ns].view(np.uint64).copy())
+        if first is None:
+            first = cur
+        else:
+            assert cur[:3] == first[:3]
+            assert all(np.array_equal(a, b) for a, b in zip(cur[3:], first[3:]))
+    ctx.close()
+    bc = pkg.h0_barcode(X)
+    assert np.array_equal(bc.scale.view(np.uint64), first[5])
+    assert np.array_equal(bc.death_grade, first[3])
