@@ -2,6 +2,7 @@
 outputs (tests/golden, produced by oracle/_ref).  Bar: bit-exact D, bit-exact ordered bars,
 identical essential count and claimed lows (integer/byte work and the exact f64 fold)."""
 import hashlib
+from pathlib import Path
 
 import numpy as np
 import pytest
@@ -345,3 +346,19 @@ def test_scale_to_host_matches_device_d(cfg):
     assert 0 < moved.value <= r.n_scale * 8 + (r.n_scale // 1024 + 1) * 13
     out.free()
     ctx.close()
+
+
+def test_lattice128_claimed_lows_and_supports():
+    """128 x 128 lattice (K = 1.34e8, ties spanning thousands of sort tiles): claimed lows and
+    the survivors' reduced supports against the C oracle's sparse reduction
+    (tests/golden/make_golden_lattice.py) — they depend on the (u, v) order inside each tie
+    group, so an unstable in-warp rank (ATOMS lane order) would show here."""
+    G = np.load(Path(__file__).resolve().parent / "golden" / "lattice128_supports.npz")
+    X = np.array([[x, y] for x in range(128) for y in range(128)], np.float64)
+    assert np.array_equal(pkg.claimed_lows(X), G["rows_hi"])
+    cols, lo, hi = pkg.reduced_supports(X)
+    assert np.array_equal(cols, G["columns"])
+    assert np.array_equal(lo, G["rows_lo"]) and np.array_equal(hi, G["rows_hi"])
+    bc = pkg.h0_barcode(X)
+    assert np.array_equal(bc.death_grade, G["death_grade"])
+    assert len(bc.scale) == int(G["n_scale"])
