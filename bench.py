@@ -247,7 +247,7 @@ def run_sharded(args, cfg_name):
     """N > 1 (torchrun, one rank per GPU): the sharded pipeline of sharded.py — rows split
     across ranks, splitter partition whose kernel stores each part straight into its
     destination rank's receive buffer over NVLink (CUDA IPC; PH0B_EXCHANGE=collective: send
-    buffer + NCCL all-to-all-v instead), D sharded, local + final column reductions.  Total
+    buffer + NCCL all-to-all-v instead), D sharded, the column reduction handed from rank to rank.  Total
     work fixed as N grows (strong scaling of the C5 problem)."""
     import numpy as np
     import torch
