@@ -114,8 +114,10 @@ __global__ void __launch_bounds__(kUThreads, 3)
                 int2* __restrict__ tile_own, const uint64_t* __restrict__ tile_offsets) {
     extern __shared__ __align__(128) uint64_t up_dyn[];
     __shared__ __align__(8) uint64_t s_bar[2];
-    __shared__ uint32_t s_warp_tot[kUWarps];
-    __shared__ int s_own[2];
+    // by buffer parity: in the count pass a warp may start the next tile while slower warps
+    // still read this tile's totals and owned range (no barrier at the loop top there)
+    __shared__ uint32_t s_warp_tot[2][kUWarps];
+    __shared__ int s_own[2][2];
     // kMode 1: run starts to fix, one per thread after the claims barrier (the claiming thread
     // keeps any beyond kRunList: a tile's runs then cost one run of latency, not several)
     constexpr uint32_t kRunList = kMode == 1 ? 512 : 1;
@@ -179,7 +181,10 @@ __global__ void __launch_bounds__(kUThreads, 3)
                 : "memory");
             phase[b] ^= 1u;
         }
-        __syncthreads();  // everyone is done with the other buffer: prefetch into it
+        // everyone is done with the other buffer: prefetch into it.  (The count pass needs no
+        // barrier here: every read of the other buffer precedes the previous tile's last
+        // barrier, which thread 0 — the one issuing the copy — has passed.)
+        if (kMode == 2) __syncthreads();
         const uint32_t next = tile + gridDim.x;
         if (tid == 0 && next < num_tiles) issue(next, b ^ 1);
         const uint64_t k_before = k_before_next;
@@ -266,8 +271,8 @@ __global__ void __launch_bounds__(kUThreads, 3)
                 // tile's first owned position) is not visible here — sorted or not, redo
                 if (st < tn && e == staged && ext_end < count) atomicOr(redo, 1u);
                 if (st >= tn) st = e = tn;
-                s_own[0] = (int)st;
-                s_own[1] = (int)e;
+                s_own[b][0] = (int)st;
+                s_own[b][1] = (int)e;
             }
             __syncthreads();  // every claim is made before any run is reordered
             const uint32_t listed = s_nruns < kRunList ? s_nruns : kRunList;
@@ -319,8 +324,8 @@ __global__ void __launch_bounds__(kUThreads, 3)
                 }
             }
             __syncthreads();  // runs fixed; the owned range is in s_own
-            os = (uint32_t)s_own[0];
-            oe = (uint32_t)s_own[1];
+            os = (uint32_t)s_own[b][0];
+            oe = (uint32_t)s_own[b][1];
             if (tid == 0) {
                 s_nruns = 0;  // the run list is free again (next tile: after two barriers)
                 // distinct lengths of this tile's last run past the tile end (fixed keys)
@@ -341,13 +346,13 @@ __global__ void __launch_bounds__(kUThreads, 3)
             ball[i] = __ballot_sync(0xffffffffu, f);
             total += __popc(ball[i]);
         }
-        if (lane == 0) s_warp_tot[warp] = total;
+        if (lane == 0) s_warp_tot[b][warp] = total;
         __syncthreads();
         uint32_t warp_base = 0, main_tot = 0;
 #pragma unroll
         for (int w = 0; w < kUWarps; ++w) {
-            warp_base += (w < warp) ? s_warp_tot[w] : 0u;
-            main_tot += s_warp_tot[w];
+            warp_base += (w < warp) ? s_warp_tot[b][w] : 0u;
+            main_tot += s_warp_tot[b][w];
         }
         if (kMode == 1) {  // counts and owned range of this tile for the scan
             if (tid == 0) {
