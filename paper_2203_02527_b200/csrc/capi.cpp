@@ -114,8 +114,8 @@ public:
             std::lock_guard<std::mutex> lk(mu_);
             size_t best = idle_.size();
             for (size_t i = 0; i < idle_.size(); ++i)
-                if (idle_[i].second >= bytes &&
-                    (best == idle_.size() || idle_[i].second < idle_[best].second))
+                if (idle_[i].second.len >= bytes &&
+                    (best == idle_.size() || idle_[i].second.len < idle_[best].second.len))
                     best = i;
             if (best != idle_.size()) {
                 const auto e = idle_[best];
@@ -125,16 +125,27 @@ public:
             }
         }
         const size_t len = (bytes + (size_t(2) << 20) - 1) & ~((size_t(2) << 20) - 1);
-        void* p = mmap(nullptr, len, PROT_READ | PROT_WRITE, MAP_PRIVATE | MAP_ANONYMOUS, -1, 0);
-        if (p == MAP_FAILED) return nullptr;
-        madvise(p, len, MADV_HUGEPAGE);
+        void* p = nullptr;
+        if (pinned_results()) {  // page-locked: the decoders write it as fast as a caller's
+                                 // pinned buffer (an anonymous mapping measured slower)
+            if (cudaHostAlloc(&p, len, cudaHostAllocDefault) != cudaSuccess) {
+                cudaGetLastError();
+                p = nullptr;
+            }
+        }
+        const bool pinned = p != nullptr;
+        if (!p) {
+            p = mmap(nullptr, len, PROT_READ | PROT_WRITE, MAP_PRIVATE | MAP_ANONYMOUS, -1, 0);
+            if (p == MAP_FAILED) return nullptr;
+            madvise(p, len, MADV_HUGEPAGE);
+        }
         std::lock_guard<std::mutex> lk(mu_);
-        live_[p] = len;
+        live_[p] = Buf{len, pinned};
         return p;
     }
     void give(void* p) {
         if (!p) return;
-        std::vector<std::pair<void*, size_t>> drop;
+        std::vector<std::pair<void*, Buf>> drop;
         {
             std::lock_guard<std::mutex> lk(mu_);
             const auto it = live_.find(p);
@@ -149,21 +160,38 @@ public:
                 idle_.erase(idle_.begin());
             }
         }
-        for (auto& e : drop) munmap(e.first, e.second);
+        for (auto& e : drop) release(e);
     }
     void trim() {
-        std::vector<std::pair<void*, size_t>> drop;
+        std::vector<std::pair<void*, Buf>> drop;
         {
             std::lock_guard<std::mutex> lk(mu_);
             drop.swap(idle_);
         }
-        for (auto& e : drop) munmap(e.first, e.second);
+        for (auto& e : drop) release(e);
     }
 
 private:
+    struct Buf {
+        size_t len;
+        bool pinned;  // cudaHostAlloc (else an anonymous mapping)
+    };
+    static bool pinned_results() {  // PH0B_PINNED_RESULTS=0: anonymous mappings only
+        static const bool v = [] {
+            const char* e = getenv("PH0B_PINNED_RESULTS");
+            return !(e && e[0] == '0');
+        }();
+        return v;
+    }
+    static void release(const std::pair<void*, Buf>& e) {
+        if (e.second.pinned)
+            cudaFreeHost(e.first);
+        else
+            munmap(e.first, e.second.len);
+    }
     std::mutex mu_;
-    std::map<void*, size_t> live_;
-    std::vector<std::pair<void*, size_t>> idle_;
+    std::map<void*, Buf> live_;
+    std::vector<std::pair<void*, Buf>> idle_;
 };
 
 ResultCache& result_cache() {
