@@ -15,7 +15,6 @@
 #include "../../include/ph0b.h"
 #include "colcodec.h"
 #include "host_decode.h"
-#include "kernels.h"
 #include "pipeline.h"
 
 using ph0b::Context;
@@ -129,7 +128,10 @@ public:
         void* p = nullptr;
         if (pinned_results()) {  // page-locked: the decoders write it as fast as a caller's
                                  // pinned buffer (an anonymous mapping measured slower)
-            p = ph0b::pinned_alloc(len);
+            if (cudaHostAlloc(&p, len, cudaHostAllocDefault) != cudaSuccess) {
+                cudaGetLastError();
+                p = nullptr;
+            }
         }
         const bool pinned = p != nullptr;
         if (!p) {
@@ -183,7 +185,7 @@ private:
     }
     static void release(const std::pair<void*, Buf>& e) {
         if (e.second.pinned)
-            ph0b::pinned_free(e.first);
+            cudaFreeHost(e.first);
         else
             munmap(e.first, e.second.len);
     }
@@ -262,8 +264,17 @@ const char* ph0b_last_error(void) { return g_last_error.c_str(); }
 uint32_t ph0b_abi_version(void) { return PH0B_ABI_VERSION; }
 uint64_t ph0b_last_launch_count(void) { return g_last_launches; }
 
-void* ph0b_host_alloc(uint64_t bytes) { return ph0b::pinned_alloc(bytes); }
-void ph0b_host_free(void* p) { ph0b::pinned_free(p); }
+void* ph0b_host_alloc(uint64_t bytes) {
+    void* p = nullptr;
+    if (cudaHostAlloc(&p, bytes ? bytes : 1, cudaHostAllocDefault) != cudaSuccess) {
+        cudaGetLastError();
+        return nullptr;
+    }
+    return p;
+}
+void ph0b_host_free(void* p) {
+    if (p) cudaFreeHost(p);
+}
 
 int ph0b_context_create(int device, ph0b_context** out) {
     if (!out) return fail(PH0B_ERR_INVALID_ARGUMENT, "null context pointer");

@@ -15,9 +15,6 @@ namespace ph0b {
 // kernel, smem, threads); thread-safe.
 int kernel_blocks_per_sm(const void* kern, int threads, size_t smem);
 int device_sm_count();
-// page-locked host memory (host_mem.cpp): cudaHostAlloc, or THP + cudaHostRegister
-void* pinned_alloc(size_t bytes);
-void pinned_free(void* p);
 
 // ---- K1: tiled upper-triangle distance kernel (distance.cu) ----------------------------
 struct DistanceArgs {

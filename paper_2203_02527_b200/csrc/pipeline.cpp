@@ -193,9 +193,8 @@ Context::~Context() {
     for (void* p : ps)
         if (p) cudaFree(p);
     pool_.reset();
-    for (void* p : {(void*)h_ring_, (void*)h_cbase_, (void*)h_craw_, (void*)h_cpoff_})
-        pinned_free(p);
-    for (void* p : {(void*)h_ringflags_, (void*)h_pieceoff_})
+    for (void* p : {(void*)h_ring_, (void*)h_ringflags_, (void*)h_cbase_, (void*)h_craw_,
+                    (void*)h_cpoff_, (void*)h_pieceoff_})
         if (p) cudaFreeHost(p);
     for (void* p : {(void*)d_coff_, (void*)d_cpoff_})
         if (p) cudaFree(p);
@@ -289,14 +288,16 @@ bool Context::stream_memops_ok() {
 
 Status Context::grow_host(void** p, uint64_t* cap, uint64_t need) {
     if (need <= *cap) return Status::ok();
-    pinned_free(*p);
+    if (*p) cudaFreeHost(*p);
     *p = nullptr;
     *cap = 0;
     need = (need + 4095) & ~4095ull;
-    *p = pinned_alloc(need);
-    if (!*p)
+    const cudaError_t e = cudaHostAlloc(p, need, cudaHostAllocDefault);
+    if (e != cudaSuccess) {
+        cudaGetLastError();
         return {PH0B_ERR_OUT_OF_MEMORY, "pinned host allocation of " + std::to_string(need) +
-                                            " bytes failed"};
+                                            " bytes failed (" + cudaGetErrorString(e) + ")"};
+    }
     *cap = need;
     return Status::ok();
 }
